@@ -1,0 +1,245 @@
+/*
+ * catgnn.h — C ABI of the B200-native CATGNN per-partition training step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/gnnpart/train.hpp, proj/src/train.cpp).  The
+ * reference exposes a statically linked C++ namespace (`gnnpart::`) with no FFI
+ * layer; every entry point below names the reference function it replaces.
+ * INTEGRATION.md shows the binding a maintainer adds on the reference side.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross the ABI.
+ *  - Return codes mirror the reference CLI's error categories
+ *    (proj/include/gnnpart/common.hpp:16-24, proj/tools/gnnpart.cpp:387-399):
+ *    0 ok, 2 ConfigError (bad parameters), 3 DataError (bad/inconsistent input),
+ *    4 internal error (incl. CUDA failures).  The message of the last failure
+ *    on the calling thread is returned by catgnn_last_error().  No exceptions
+ *    cross the ABI.
+ *  - The caller owns every host buffer it passes; the library owns device
+ *    memory behind opaque handles, released by the matching *_destroy call.
+ *  - All device work runs on the stream of the catgnn_ctx the object was
+ *    created on.  A handle is not thread-safe.
+ *  - Host float parameters/features are float32 row-major; the device computes
+ *    in float32 (tensor-core GEMMs in TF32 with float32 accumulation).
+ */
+#ifndef CATGNN_H
+#define CATGNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CATGNN_OK 0
+#define CATGNN_ECONFIG 2
+#define CATGNN_EDATA 3
+#define CATGNN_EINTERNAL 4
+
+typedef struct catgnn_ctx_s* catgnn_ctx;         /* device + stream + scratch */
+typedef struct catgnn_artifact_s* catgnn_artifact; /* host view of a stored artifact */
+typedef struct catgnn_shard_s* catgnn_shard;     /* device-resident shard (CSR, features, roles) */
+typedef struct catgnn_model_s* catgnn_model;     /* GNN replica: params + optimizer state */
+typedef struct catgnn_comm_s* catgnn_comm;       /* NCCL communicator (one rank per GPU) */
+
+const char* catgnn_last_error(void);
+int catgnn_version(void);
+
+/* ---------------------------------------------------------------- context */
+/* stream: a cudaStream_t to run on, or NULL to create a private stream. */
+int catgnn_ctx_create(int device, void* stream, catgnn_ctx* out);
+int catgnn_ctx_destroy(catgnn_ctx ctx);
+int catgnn_ctx_synchronize(catgnn_ctx ctx);
+/* Number of CUDA kernels this library launched on ctx since creation (evidence
+ * for bench.py's gpu_launches; counts launches, not graph replays). */
+uint64_t catgnn_ctx_launch_count(catgnn_ctx ctx);
+/* Device time (ms) accumulated by the aggregation kernel (K2) and the GEMM
+ * kernel (K3) while timing is enabled (CUDA events on ctx's stream). */
+int catgnn_ctx_set_kernel_timing(catgnn_ctx ctx, int enable);
+int catgnn_ctx_kernel_time(catgnn_ctx ctx, double* agg_ms, uint64_t* agg_launches,
+                           double* gemm_ms, uint64_t* gemm_launches);
+
+/* -------------------------------------------------- artifact (A1-A3 input) */
+/* Reads manifest.json, part-<i>/{edges.bin,nodes.tsv}, labels.tsv and verifies
+ * every count like read_partitions (proj/src/store.cpp:269-333). */
+int catgnn_artifact_open(const char* dir, catgnn_artifact* out);
+int catgnn_artifact_close(catgnn_artifact a);
+typedef struct {
+  uint32_t num_partitions;
+  uint64_t num_nodes;
+  uint64_t num_edges;
+  uint32_t feature_dim;
+  int has_features;
+  int has_meta;
+  int add_reverse;
+  double replication_factor;          /* recomputed: metrics.cpp:9-12 */
+  double manifest_replication_factor; /* as stored by write_partitions */
+} catgnn_artifact_info;
+int catgnn_artifact_get_info(catgnn_artifact a, catgnn_artifact_info* info);
+/* Per-partition counts as in the manifest. */
+int catgnn_artifact_part_counts(catgnn_artifact a, uint32_t part, uint64_t* nodes,
+                                uint64_t* owned, uint64_t* edges);
+/* Replica / halo map of one partition, in node-table (= local row) order:
+ * external id, owner flag, role (0 none, 1 train, 2 val, 3 test) and the home
+ * partition (owner partition of that node; == part for owners). */
+int catgnn_artifact_replica_map(catgnn_artifact a, uint32_t part, uint64_t* ext_ids,
+                                uint8_t* owner, uint8_t* role, uint32_t* home);
+
+/* ------------------------------------------------------------ shards (A3-A4) */
+/* load_training_data (train.cpp:216-287) for one shard: part >= 0 is a
+ * partition shard (local row i = i-th record of part-<i>/nodes.tsv; features
+ * from part-<i>/features.bin or gathered from the global feature file);
+ * part == -1 is the global shard (full edge stream, no dedup).  input/features
+ * override the paths recorded in the manifest when non-NULL/non-empty. */
+int catgnn_shard_load(catgnn_ctx ctx, catgnn_artifact a, int32_t part, const char* input,
+                      const char* features, catgnn_shard* out);
+/* build_adjacency (train.cpp:30-47) on the device from host local pairs
+ * (pairs[2k], pairs[2k+1]) in edge order.  features may be NULL (dim 0). */
+int catgnn_shard_create(catgnn_ctx ctx, uint32_t rows, const uint32_t* pairs, uint64_t num_edges,
+                        const float* features, uint32_t dim, catgnn_shard* out);
+/* Shard from an in-memory partition (what complete_edges produced): node table
+ * (ascending external ids, owner flags, roles), external-id edges in stream
+ * order, labels per local row, and features per local row (rows x dim). */
+int catgnn_shard_create_from_part(catgnn_ctx ctx, uint64_t rows, const uint64_t* ext_ids,
+                                  const uint8_t* owner, const uint8_t* role,
+                                  const int32_t* labels, const uint64_t* edges_ext,
+                                  uint64_t num_edges, const float* features, uint32_t dim,
+                                  catgnn_shard* out);
+int catgnn_shard_destroy(catgnn_shard s);
+/* Labels and role rows in local row space (train rows = owner && role==train). */
+int catgnn_shard_set_labels(catgnn_shard s, const int32_t* labels, const uint32_t* train_rows,
+                            uint64_t n_train, const uint32_t* val_rows, uint64_t n_val,
+                            const uint32_t* test_rows, uint64_t n_test);
+/* Re-upload features (host rows x dim) into the resident device buffer. */
+int catgnn_shard_upload_features(catgnn_shard s, const float* features, uint32_t dim);
+typedef struct {
+  uint64_t rows;
+  uint64_t nnz;
+  uint32_t dim;
+  uint32_t classes; /* max(label)+1 over the shard, >= 1 */
+  uint64_t n_train, n_val, n_test;
+  uint64_t heavy_rows; /* rows split across several aggregation tasks */
+  uint64_t tasks;      /* aggregation work items */
+} catgnn_shard_info;
+int catgnn_shard_get_info(catgnn_shard s, catgnn_shard_info* info);
+/* Bit-exact export of the device CSR (offsets widened to u64). */
+int catgnn_csr_export(catgnn_shard s, uint64_t* offsets, uint32_t* neighbors);
+int catgnn_shard_role_rows(catgnn_shard s, int role, uint32_t* rows);
+int catgnn_shard_labels(catgnn_shard s, int32_t* labels);
+/* which: 0 = input features, 1 = SGC-propagated features. */
+int catgnn_shard_export_features(catgnn_shard s, int which, float* out);
+
+/* ---------------------------------------------------------- SGC path (A5-A13) */
+/* sgc_propagate (train.cpp:49-65): hops rounds of (x_i + sum_j x_j)/(1+deg_i),
+ * stored in the shard's propagated buffer. */
+int catgnn_sgc_propagate(catgnn_shard s, uint32_t hops);
+/* softmax_loss / softmax_gradient (train.cpp:74-94) over the listed rows of the
+ * propagated features.  W is dim x classes row-major, b is classes. */
+int catgnn_softmax_loss(catgnn_shard s, const float* W, const float* b, uint32_t classes,
+                        const uint32_t* rows, uint64_t n_rows, double* loss);
+int catgnn_softmax_gradient(catgnn_shard s, const float* W, const float* b, uint32_t classes,
+                            const uint32_t* rows, uint64_t n_rows, float* gW, float* gb);
+/* train_epochs (train.cpp:96-128) for n replicas at once, one shard each:
+ * W[i]/b[i] are host in/out parameter buffers; replica i uses seeds[i]. */
+int catgnn_train_epochs(uint32_t n, const catgnn_shard* shards, float* const* W, float* const* b,
+                        uint32_t classes, double lr, uint32_t batch, uint64_t epoch_begin,
+                        uint64_t epoch_end, const uint64_t* seeds);
+/* sync_weights (train.cpp:139-152). */
+int catgnn_sync_weights(const uint64_t* counts, uint32_t n, double* alpha);
+/* model_average (train.cpp:154-172) of n host parameter blocks of `count`
+ * floats each (W and b flattened); result into out. */
+int catgnn_model_average_host(catgnn_ctx ctx, uint32_t n, const float* const* params,
+                              uint64_t count, const uint64_t* train_counts, float* out);
+/* evaluate_micro_f1 (train.cpp:174-198) on the propagated features. */
+int catgnn_evaluate_micro_f1(catgnn_shard s, const float* W, const float* b, uint32_t classes,
+                             const uint32_t* mask_rows, uint64_t n_mask, double* f1);
+
+typedef struct {
+  uint32_t epochs;    /* TrainConfig (train.hpp:42-48) */
+  double lr;
+  uint32_t batch;
+  uint32_t prop_hops;
+  uint64_t seed;
+} catgnn_train_config;
+typedef struct {
+  float* W;           /* out: dim x classes (caller-allocated, may be NULL) */
+  float* b;           /* out: classes */
+  uint32_t dim, classes;
+  uint64_t* hist_epoch; uint64_t* hist_syncs; double* hist_val; double* hist_test;
+  uint64_t hist_capacity;
+  uint64_t n_hist;
+  uint64_t averaging_ops;
+} catgnn_dist_result;
+/* distributed_train (train.cpp:289-340) over p partition shards + the global
+ * shard for evaluation; workers q must divide p (results are independent of q). */
+int catgnn_distributed_train(uint32_t p, const catgnn_shard* shards, catgnn_shard global,
+                             uint32_t workers, uint32_t sync_interval,
+                             const catgnn_train_config* cfg, catgnn_dist_result* result);
+
+/* ------------------------------------------------- GNN models (north-star rows) */
+#define CATGNN_MODEL_GCN 1  /* h' = D^-1/2 (A+I) D^-1/2 h W^T + b           */
+#define CATGNN_MODEL_SAGE 2 /* h' = h W_s^T + mean_N(h) W_n^T + b          */
+#define CATGNN_MODEL_GIN 3  /* h' = ((1+eps) h + sum_N h) W^T + b, eps = 0 */
+#define CATGNN_OPT_SGD 0
+#define CATGNN_OPT_ADAM 1
+typedef struct {
+  int kind;
+  uint32_t layers;
+  uint32_t in_dim;
+  uint32_t hidden;
+  uint32_t classes;
+  int optimizer;
+  double lr;
+  double beta1, beta2, eps; /* Adam */
+  uint64_t seed;            /* init: splitmix of seed_for(seed, layer) */
+} catgnn_model_config;
+int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_model* out);
+int catgnn_model_destroy(catgnn_model m);
+uint64_t catgnn_model_num_params(catgnn_model m);
+/* Flat parameter vector: per layer W (row-major, shape given by
+ * catgnn_model_layer_shape) followed by b. */
+int catgnn_model_layer_shape(catgnn_model m, uint32_t layer, uint32_t* w_rows, uint32_t* w_cols,
+                             uint64_t* offset_w, uint64_t* offset_b);
+int catgnn_model_get_params(catgnn_model m, float* out);
+int catgnn_model_set_params(catgnn_model m, const float* in);
+int catgnn_model_copy_params(catgnn_model dst, catgnn_model src);
+int catgnn_model_get_grads(catgnn_model m, float* out);
+/* One local iteration: full-batch forward + backward over the shard, loss on
+ * the shard's train rows (mean CE), then one optimizer step.  loss may be NULL
+ * (then no device->host read happens). */
+int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss);
+/* Forward + backward only (no update); gradients readable by get_grads. */
+int catgnn_model_forward_backward(catgnn_model m, catgnn_shard s, double* loss);
+/* Forward only; logits rows x classes into out (host) when out != NULL;
+ * micro-F1 over role rows (2 val, 3 test) when f1 != NULL. */
+int catgnn_model_forward(catgnn_model m, catgnn_shard s, float* logits, int role, double* f1);
+/* Debug export of layer activations after forward/backward:
+ * what 0 = layer output H_l (post activation), 1 = pre-activation Z_l,
+ * 2 = dZ_l.  out holds rows x width(layer) floats. */
+int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, uint32_t* width);
+/* In-process model averaging (train.cpp:154-172): dst = sum_i alpha_i src_i,
+ * alpha from sync_weights(train_counts); dst may alias one of src. */
+int catgnn_model_average(uint32_t n, const catgnn_model* src, const uint64_t* train_counts,
+                         catgnn_model dst);
+
+/* ---------------------------------------------------------- multi-GPU (C1) */
+int catgnn_comm_unique_id(char id[128]);
+int catgnn_comm_create(catgnn_ctx ctx, int nranks, int rank, const char id[128], catgnn_comm* out);
+int catgnn_comm_destroy(catgnn_comm c);
+/* Model averaging across ranks: params <- allreduce_sum(alpha * params) where
+ * alpha = this rank's share (sum of its replicas' alphas is folded by the
+ * caller via catgnn_model_scale). */
+int catgnn_model_scale(catgnn_model m, double alpha);
+int catgnn_model_allreduce(catgnn_model m, catgnn_comm c);
+
+/* ------------------------------------------------------------- utilities */
+/* Tensor-core GEMM test hook: C[M x N] = A[M x K] . B[N x K]^T (all host,
+ * row-major float32), computed by the tcgen05 TF32 kernel. */
+int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
+                   const float* B, float* C, uint32_t split_k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CATGNN_H */

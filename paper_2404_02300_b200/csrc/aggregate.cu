@@ -1,0 +1,332 @@
+// K2 — neighbourhood aggregation, the B200 restatement of the gather loop of
+// gnnpart::sgc_propagate (/root/reference/proj/src/train.cpp:55-62) generalised
+// to the north-star layers (SGC mean-with-self, GCN-norm, SAGE-mean, GIN-sum).
+//
+//   out[r] = epi( post(deg_r) * ( self * pre[r]*in[r] + sum_{j in N(r)} pre[j]*in[j] ) )
+//   epi    = (+ residual[r]) (+ bias) (ReLU) (* [mask[r] > 0])
+//
+// Roofline: HBM-bound gather.  Algorithmic bytes per pass =
+//   nnz*(4 + 4*width) + rows*(4*width*(1+self) + 8)
+// (int32 column index + one fp32 row per edge; own row read when self, output
+// row written, int64 offset read).  The kernel is persistent: warps pull work
+// units (see csr.cu build_plan) from an atomic counter, prefetching the next
+// unit index while the current one streams.  Inside a unit a warp walks whole
+// rows: 32 column indices per coalesced load, then neighbour rows gathered with
+// 128-bit read-only loads, UNROLL neighbours in flight per lane group.  Rows
+// narrower than 128 floats are processed by sub-warp groups (LPN lanes per
+// neighbour, 32/LPN neighbours at once) reduced with xor-shuffles.  Rows with
+// more than U neighbours are chunked; chunk partials are combined in chunk
+// order by agg_fixup_kernel, so results are deterministic.
+#include <algorithm>
+#include <map>
+
+#include "shard.hpp"
+
+namespace catgnn {
+
+namespace {
+
+struct AggKernelArgs {
+  const int64_t* __restrict__ row_ptr;
+  const int32_t* __restrict__ col;
+  const int4* __restrict__ units;
+  const int4* __restrict__ heavy;
+  unsigned long long n_units;
+  unsigned long long n_heavy;
+  unsigned int* counter;
+  float* __restrict__ partials;  // [n_chunks][w4*4]
+  uint32_t U;
+  const float* __restrict__ in;
+  uint32_t in_ld, in_col;
+  float* __restrict__ out;
+  uint32_t out_ld, out_col;
+  uint32_t w4;
+  const float* __restrict__ pre;
+  int self;
+  int norm;
+  const float* __restrict__ bias;
+  const float* __restrict__ residual;
+  uint32_t res_ld, res_col;
+  int relu;
+  const float* __restrict__ mask;
+  uint32_t mask_ld, mask_col;
+};
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void fma4(float4& a, float s, const float4& v) {
+  a.x = fmaf(s, v.x, a.x);
+  a.y = fmaf(s, v.y, a.y);
+  a.z = fmaf(s, v.z, a.z);
+  a.w = fmaf(s, v.w, a.w);
+}
+__device__ __forceinline__ void add4(float4& a, const float4& v) {
+  a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+}
+__device__ __forceinline__ float4 shfl_xor4(const float4& v, int m) {
+  return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                     __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+
+__device__ __forceinline__ float post_scale(int norm, float deg) {
+  switch (norm) {
+    case kNormSgc: return 1.0f / (1.0f + deg);
+    case kNormGcn: return 1.0f / sqrtf(1.0f + deg);
+    case kNormMean: return deg > 0.f ? 1.0f / deg : 0.0f;
+    default: return 1.0f;
+  }
+}
+
+// Final epilogue for one output row.  `acc` holds the neighbour sum for the
+// float4 columns c4 = li + LPN*q.
+template <int VPL, int LPN>
+__device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, float deg,
+                                             const float4 (&acc)[VPL], int li) {
+  const float post = post_scale(p.norm, deg);
+  const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) {
+    const uint32_t c4 = li + LPN * q;
+    if (c4 >= p.w4) continue;
+    float4 a = acc[q];
+    if (p.self) fma4(a, selfs, ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4));
+    a.x *= post; a.y *= post; a.z *= post; a.w *= post;
+    if (p.residual) add4(a, ldg4(p.residual + (size_t)r * p.res_ld + p.res_col + c4 * 4));
+    if (p.bias) add4(a, ldg4(p.bias + c4 * 4));
+    if (p.relu) {
+      a.x = fmaxf(a.x, 0.f); a.y = fmaxf(a.y, 0.f); a.z = fmaxf(a.z, 0.f); a.w = fmaxf(a.w, 0.f);
+    }
+    if (p.mask) {
+      float4 m = ldg4(p.mask + (size_t)r * p.mask_ld + p.mask_col + c4 * 4);
+      a.x = m.x > 0.f ? a.x : 0.f; a.y = m.y > 0.f ? a.y : 0.f;
+      a.z = m.z > 0.f ? a.z : 0.f; a.w = m.w > 0.f ? a.w : 0.f;
+    }
+    *reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4) = a;
+  }
+}
+
+// Sum of pre[j]*in[j] over edges [e0, e1) into acc (reduced across groups).
+template <int VPL, int LPN, bool PRE>
+__device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64_t e1,
+                                       float4 (&acc)[VPL], int lane) {
+  constexpr int G = 32 / LPN;  // neighbours processed side by side
+  constexpr int UNROLL = VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8);
+  const int g = lane / LPN, li = lane % LPN;
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t e = e0; e < e1; e += 32) {
+    const int n = (int)((e1 - e) < 32 ? (e1 - e) : 32);
+    const int myj = lane < n ? __ldg(p.col + e + lane) : 0;
+    float mys = 1.0f;
+    if (PRE) mys = lane < n ? __ldg(p.pre + myj) : 0.0f;
+    for (int kb = 0; kb < n; kb += G * UNROLL) {
+      float4 v[UNROLL][VPL];
+      float s[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int kk = kb + u * G + g;
+        const int j = __shfl_sync(0xffffffffu, myj, kk & 31);
+        s[u] = PRE ? __shfl_sync(0xffffffffu, mys, kk & 31) : 1.0f;
+        const bool ok = kk < n;
+        const float* src = p.in + (size_t)j * p.in_ld + p.in_col;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const uint32_t c4 = li + LPN * q;
+          v[u][q] = (ok && c4 < p.w4) ? ldg4(src + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          if (PRE) fma4(acc[q], s[u], v[u][q]);
+          else add4(acc[q], v[u][q]);
+        }
+    }
+  }
+#pragma unroll
+  for (int m = LPN; m < 32; m <<= 1)
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], m));
+}
+
+template <int VPL, int LPN, bool PRE>
+__global__ void __launch_bounds__(256, 2) agg_kernel(const AggKernelArgs p) {
+  const int lane = threadIdx.x & 31;
+  const int li = lane % LPN;
+  const bool writer = lane < LPN;
+  unsigned int u = 0;
+  if (lane == 0) u = atomicAdd(p.counter, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < p.n_units) {
+    unsigned int next = 0;
+    if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
+    const int4 w = __ldg(p.units + u);
+    float4 acc[VPL];
+    if (w.z < 0) {
+      for (int64_t r = w.x; r < w.y; ++r) {
+        const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
+        gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
+        if (writer) epilogue_row<VPL, LPN>(p, r, (float)(e1 - e0), acc, li);
+      }
+    } else {
+      const int64_t r = w.x;
+      const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
+      const int64_t e0 = rb + (int64_t)w.y * p.U;
+      const int64_t e1 = (re < e0 + (int64_t)p.U) ? re : e0 + (int64_t)p.U;
+      gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
+      if (writer) {
+        float* dst = p.partials + (size_t)w.z * p.w4 * 4;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const uint32_t c4 = li + LPN * q;
+          if (c4 < p.w4) *reinterpret_cast<float4*>(dst + c4 * 4) = acc[q];
+        }
+      }
+    }
+    u = __shfl_sync(0xffffffffu, next, 0);
+  }
+}
+
+// One warp per split row: sum its chunk partials in chunk order, then the
+// same epilogue as a light row.
+template <int VPL>
+__global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t h = wid; h < p.n_heavy; h += nw) {
+    const int4 hv = __ldg(p.heavy + h);
+    const int64_t r = hv.x;
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < hv.z; ++c) {
+      const float* src = p.partials + (size_t)(hv.y + c) * p.w4 * 4;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const uint32_t c4 = lane + 32 * q;
+        if (c4 < p.w4) add4(acc[q], *reinterpret_cast<const float4*>(src + c4 * 4));
+      }
+    }
+    const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
+    epilogue_row<VPL, 32>(p, r, deg, acc, lane);
+  }
+}
+
+using AggFn = void (*)(const AggKernelArgs);
+
+template <int VPL, int LPN>
+AggFn pick_pre(bool pre) {
+  return pre ? agg_kernel<VPL, LPN, true> : agg_kernel<VPL, LPN, false>;
+}
+
+// Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
+constexpr uint32_t kMaxSlab4 = 256;
+
+AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
+  if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre); }
+  if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre); }
+  if (w4 <= 16) { *lpn_out = 16; return pick_pre<1, 16>(pre); }
+  *lpn_out = 32;
+  switch ((w4 + 31) / 32) {
+    case 1: return pick_pre<1, 32>(pre);
+    case 2: return pick_pre<2, 32>(pre);
+    case 3: return pick_pre<3, 32>(pre);
+    case 4: return pick_pre<4, 32>(pre);
+    case 5: return pick_pre<5, 32>(pre);
+    case 6: return pick_pre<6, 32>(pre);
+    case 7: return pick_pre<7, 32>(pre);
+    default: return pick_pre<8, 32>(pre);
+  }
+}
+
+AggFn pick_fixup(uint32_t w4) {
+  switch ((w4 + 31) / 32) {
+    case 1: return agg_fixup_kernel<1>;
+    case 2: return agg_fixup_kernel<2>;
+    case 3: return agg_fixup_kernel<3>;
+    case 4: return agg_fixup_kernel<4>;
+    case 5: return agg_fixup_kernel<5>;
+    case 6: return agg_fixup_kernel<6>;
+    case 7: return agg_fixup_kernel<7>;
+    default: return agg_fixup_kernel<8>;
+  }
+}
+
+int blocks_per_sm(AggFn fn) {
+  static std::map<AggFn, int> cache;
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int b = 0;
+  CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 256, 0));
+  b = std::max(1, b);
+  cache[fn] = b;
+  return b;
+}
+
+}  // namespace
+
+void aggregate(catgnn_shard_s* s, const AggArgs& a) {
+  catgnn_ctx ctx = s->ctx;
+  if (a.width % 4 || a.in_ld % 4 || a.out_ld % 4 || a.in_col % 4 || a.out_col % 4 ||
+      (a.residual && (a.res_ld % 4 || a.res_col % 4)) || (a.mask && (a.mask_ld % 4 || a.mask_col % 4)))
+    throw ConfigError("aggregation widths/strides must be multiples of 4 floats");
+  if (a.in == a.out && a.in) throw ConfigError("aggregation cannot run in place");
+  if (s->rows == 0 || a.width == 0) return;
+  const uint32_t W4 = a.width / 4;
+  for (uint32_t c4 = 0; c4 < W4; c4 += kMaxSlab4) {
+    const uint32_t w4 = std::min(kMaxSlab4, W4 - c4);
+    AggKernelArgs p{};
+    p.row_ptr = s->row_ptr.p;
+    p.col = s->col.p;
+    p.units = s->units.p;
+    p.heavy = s->heavy.p;
+    p.n_units = s->n_units;
+    p.n_heavy = s->n_heavy;
+    p.counter = ctx->scratch_buf<unsigned int>("k2_counter", 1);
+    p.partials = s->n_chunks ? ctx->scratch_buf<float>("k2_partials", s->n_chunks * (size_t)w4 * 4)
+                             : nullptr;
+    p.U = s->unit_cost;
+    p.in = a.in;
+    p.in_ld = a.in_ld;
+    p.in_col = a.in_col + c4 * 4;
+    p.out = a.out;
+    p.out_ld = a.out_ld;
+    p.out_col = a.out_col + c4 * 4;
+    p.w4 = w4;
+    p.pre = a.pre;
+    p.self = a.self;
+    p.norm = a.norm;
+    p.bias = a.bias ? a.bias + c4 * 4 : nullptr;
+    p.residual = a.residual;
+    p.res_ld = a.res_ld;
+    p.res_col = a.res_col + c4 * 4;
+    p.relu = a.relu;
+    p.mask = a.mask;
+    p.mask_ld = a.mask_ld;
+    p.mask_col = a.mask_col + c4 * 4;
+    int lpn = 32;
+    AggFn fn = pick_kernel(w4, a.pre != nullptr, &lpn);
+    const int bps = blocks_per_sm(fn);
+    const uint64_t warps_needed = std::max<uint64_t>(1, s->n_units);
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)ctx->num_sms * bps, (warps_needed + 7) / 8));
+    CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
+    int t = ctx->begin_timed(0);
+    fn<<<grid, 256, 0, ctx->stream>>>(p);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+    if (s->n_heavy) {
+      AggFn fx = pick_fixup(w4);
+      const unsigned g2 = (unsigned)std::min<uint64_t>((s->n_heavy + 7) / 8, (uint64_t)ctx->num_sms * 8);
+      fx<<<g2, 256, 0, ctx->stream>>>(p);
+      CG_CHECK_LAUNCH();
+      ctx->launches++;
+    }
+    ctx->end_timed(t);
+  }
+}
+
+}  // namespace catgnn

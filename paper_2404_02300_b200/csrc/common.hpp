@@ -1,0 +1,128 @@
+// Internal plumbing shared by every translation unit of libcatgnn.so:
+// error categories (mirroring proj/include/gnnpart/common.hpp:16-24),
+// CUDA checking, device buffers and the per-device context.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "catgnn.h"
+
+namespace catgnn {
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InternalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void set_last_error(const std::string& msg);
+
+// Runs fn, translating exceptions into the ABI's return codes.
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return CATGNN_OK;
+  } catch (const ConfigError& e) {
+    set_last_error(std::string("bad-config: ") + e.what());
+    return CATGNN_ECONFIG;
+  } catch (const DataError& e) {
+    set_last_error(std::string("bad-input: ") + e.what());
+    return CATGNN_EDATA;
+  } catch (const std::exception& e) {
+    set_last_error(std::string("internal: ") + e.what());
+    return CATGNN_EINTERNAL;
+  }
+}
+
+#define CG_CUDA(expr)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::catgnn::InternalError(std::string("CUDA: ") + cudaGetErrorString(e_) + " (" + \
+                                    #expr + ") at " + __FILE__ + ":" +                      \
+                                    std::to_string(__LINE__));                              \
+  } while (0)
+
+#define CG_CHECK_LAUNCH() CG_CUDA(cudaGetLastError())
+
+// Owning device buffer (cudaMalloc; grow-only reserve for scratch).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) return;
+    CG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void reserve(size_t count) {
+    if (count > n) alloc(count);
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+inline uint32_t round_up(uint32_t x, uint32_t m) { return (x + m - 1) / m * m; }
+inline uint64_t round_up64(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace catgnn
+
+// Per-device context: stream, SM count, scratch pool, launch accounting and
+// optional per-kernel event timing for the roofline measurement.
+struct catgnn_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  uint64_t launches = 0;
+  // kernel timing (K2 aggregation, K3 GEMM)
+  bool timing = false;
+  struct Pending {
+    cudaEvent_t a, b;
+    int kind;  // 0 agg, 1 gemm
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double agg_ms = 0, gemm_ms = 0;
+  uint64_t agg_n = 0, gemm_n = 0;
+  // named grow-only scratch buffers
+  std::map<std::string, catgnn::DevBuf<unsigned char>> scratch;
+
+  template <typename T>
+  T* scratch_buf(const std::string& name, size_t count) {
+    auto& b = scratch[name];
+    b.reserve(count * sizeof(T));
+    return reinterpret_cast<T*>(b.p);
+  }
+  cudaEvent_t take_event();
+  // Bracket a kernel for timing; returns an index to close with end_timed.
+  int begin_timed(int kind);
+  void end_timed(int idx);
+  void drain_timing();
+  ~catgnn_ctx_s();
+};

@@ -1,0 +1,97 @@
+// Device-resident shard: the B200 restatement of gnnpart::Shard
+// (proj/include/gnnpart/train.hpp:84-91) plus the aggregation work plan.
+//
+// HBM layout (all row-major, 16-byte aligned rows):
+//   row_ptr  int64[rows+1]      CSR offsets (LocalAdjacency.offsets, widened to
+//                               64 bit: train.hpp:19 is u32 and overflows past
+//                               4.29e9 nnz at papers100M scale)
+//   col      int32[nnz]         neighbours, per-row order = build_adjacency's
+//                               cursor order (train.cpp:41-45)
+//   x        f32[rows][ld]      input features, ld = round_up(dim, 4)
+//   xprop    f32[rows][ld]      SGC-propagated features (sgc_propagate output)
+//   dinv     f32[rows]          (1+deg)^-1/2  (GCN normalisation)
+//   inv_deg  f32[rows]          1/deg, 0 for deg 0 (SAGE mean)
+//   units    int4[n_units]      aggregation work units (see aggregate.cu)
+//   heavy    int4[n_heavy]      split rows: {row, first partial slot, chunks, 0}
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.hpp"
+
+struct catgnn_shard_s {
+  catgnn_ctx ctx = nullptr;
+  uint64_t rows = 0;
+  uint64_t nnz = 0;
+  uint64_t num_edges = 0;
+  catgnn::DevBuf<int64_t> row_ptr;
+  catgnn::DevBuf<int32_t> col;
+  catgnn::DevBuf<float> dinv, inv_deg;
+  // aggregation plan (built once per shard, reused by every pass)
+  catgnn::DevBuf<int4> units;
+  catgnn::DevBuf<int4> heavy;
+  uint64_t n_units = 0, n_heavy = 0, n_chunks = 0;
+  uint32_t unit_cost = 0;
+  // features
+  uint32_t dim = 0, ld = 0;
+  catgnn::DevBuf<float> x, xprop;
+  catgnn::DevBuf<float> xT;  // transposed input [ld][rows_pad] for the layer-1 dW GEMM
+  uint32_t xT_ld = 0;
+  bool xT_valid = false;
+  // labels / roles (host copies + device copies)
+  std::vector<int32_t> h_labels;
+  std::vector<uint32_t> h_train, h_val, h_test;
+  catgnn::DevBuf<int32_t> labels;
+  catgnn::DevBuf<uint32_t> d_train, d_val, d_test;
+  uint32_t classes = 1;
+  // replica map (only for shards created from a partition)
+  std::vector<uint64_t> ext_ids;
+  std::vector<uint8_t> owner, role;
+};
+
+namespace catgnn {
+
+// Post-scale of the aggregated sum, computed from the local CSR degree.
+enum AggNorm : int {
+  kNormNone = 0,  // 1
+  kNormSgc = 1,   // 1/(1+deg)          (train.cpp:60)
+  kNormGcn = 2,   // (1+deg)^-1/2
+  kNormMean = 3,  // deg>0 ? 1/deg : 0  (SAGE mean)
+};
+
+struct AggArgs {
+  const float* in = nullptr;  // rows x in_ld, columns [in_col, in_col+width)
+  uint32_t in_ld = 0, in_col = 0;
+  float* out = nullptr;  // rows x out_ld, columns [out_col, out_col+width)
+  uint32_t out_ld = 0, out_col = 0;
+  uint32_t width = 0;              // multiple of 4
+  const float* pre = nullptr;      // per-source-row scale (applied to self term too)
+  int self = 0;                    // add the row's own (pre-scaled) input
+  int norm = kNormNone;            // post scale
+  const float* bias = nullptr;     // [width]
+  const float* residual = nullptr; // rows x res_ld at res_col
+  uint32_t res_ld = 0, res_col = 0;
+  int relu = 0;
+  const float* mask = nullptr;     // ReLU backward: keep where mask[r][c] > 0
+  uint32_t mask_ld = 0, mask_col = 0;
+};
+
+// K1: CSR builder (stable radix sort by source row, bit-exact with
+// build_adjacency) + aggregation plan + degree scales.  pairs are device
+// local-id pairs in edge order.
+void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges);
+// Device mapping of external-id edges to local rows by binary search over the
+// ascending node table (load_training_data's local[] map, train.cpp:258-271).
+void map_ext_edges(catgnn_ctx ctx, const uint64_t* d_ext_ids, uint64_t rows,
+                   const uint64_t* d_edges_ext, uint64_t num_edges, uint32_t* d_pairs);
+// K2: neighbourhood aggregation over the shard CSR.
+void aggregate(catgnn_shard_s* s, const AggArgs& a);
+// Copy rows x width between strided buffers (hops = 0 propagate).
+void copy_rows(catgnn_ctx ctx, const float* in, uint32_t in_ld, float* out, uint32_t out_ld,
+               uint64_t rows, uint32_t width);
+// Tiled transpose: out[c][r] = in[r][c], out_ld >= rows.
+void transpose(catgnn_ctx ctx, const float* in, uint32_t in_ld, uint64_t rows, uint32_t cols,
+               float* out, uint32_t out_ld);
+
+}  // namespace catgnn

@@ -1,0 +1,442 @@
+"""Host-side mirror of the reference training API (namespace ``gnnpart``).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/gnnpart/train.hpp, backed by the B200 kernels in
+libcatgnn.so through the C ABI (include/catgnn.h).  Parameters are float32
+NumPy arrays (the device computes in float32 / TF32); shards live on the GPU.
+
+    reference (train.hpp)               this module
+    ---------------------               -----------
+    build_adjacency        :26-27       build_adjacency(rows, edges) -> LocalAdjacency
+    sgc_propagate          :31-32       sgc_propagate(shard, hops)   (shard holds adj + x)
+    zero_params            :40          zero_params(dim, classes)
+    softmax_loss           :50-51       softmax_loss(params, shard, rows)
+    softmax_gradient       :53-55       softmax_gradient(params, shard, rows)
+    train_epochs           :61-64       train_epochs(params, shard, cfg, begin, end, seed)
+    train_local            :66-67       train_local(shard, cfg)
+    sync_weights           :71          sync_weights(counts)
+    model_average          :73-74       model_average(params_list, counts)
+    evaluate_micro_f1      :78-81       evaluate_micro_f1(params, shard, mask_rows)
+    load_training_data     :100-103     load_training_data(artifact_dir, input=, features=)
+    distributed_train      :123-124     distributed_train(data, workers, sync_interval, cfg)
+    replication_factor     metrics.hpp:46  replication_factor(artifact)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from ._lib import (ArtifactInfo, ConfigError, DataError, DistResult, InternalError, ShardInfo,
+                   TrainConfig, check, lib)
+
+__all__ = [
+    "Context", "Artifact", "Shard", "LocalAdjacency", "ModelParams", "TrainConfig", "TrainingData",
+    "SyncPoint", "DistTrainResult", "ConfigError", "DataError", "InternalError", "build_adjacency",
+    "sgc_propagate", "zero_params", "softmax_loss", "softmax_gradient", "train_epochs", "train_local",
+    "sync_weights", "model_average", "evaluate_micro_f1", "load_training_data", "distributed_train",
+    "replication_factor", "default_context",
+]
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Context:
+    """A device + CUDA stream (catgnn_ctx)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        h = C.c_void_p()
+        check(lib.catgnn_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def synchronize(self):
+        check(lib.catgnn_ctx_synchronize(self.handle))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.catgnn_ctx_launch_count(self.handle))
+
+    def set_kernel_timing(self, enable: bool):
+        check(lib.catgnn_ctx_set_kernel_timing(self.handle, int(enable)))
+
+    def kernel_time(self):
+        a = C.c_double(); an = C.c_uint64(); g = C.c_double(); gn = C.c_uint64()
+        check(lib.catgnn_ctx_kernel_time(self.handle, C.byref(a), C.byref(an), C.byref(g), C.byref(gn)))
+        return dict(agg_ms=a.value, agg_launches=an.value, gemm_ms=g.value, gemm_launches=gn.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.catgnn_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class Artifact:
+    """Host view of a stored partition artifact (read_partitions, store.cpp:269-333)."""
+
+    def __init__(self, directory: str):
+        h = C.c_void_p()
+        check(lib.catgnn_artifact_open(str(directory).encode(), C.byref(h)))
+        self.handle = h
+        self.directory = str(directory)
+        info = ArtifactInfo()
+        check(lib.catgnn_artifact_get_info(h, C.byref(info)))
+        self.info = info
+        self.num_partitions = info.num_partitions
+
+    def part_counts(self, part: int):
+        n = C.c_uint64(); o = C.c_uint64(); e = C.c_uint64()
+        check(lib.catgnn_artifact_part_counts(self.handle, part, C.byref(n), C.byref(o), C.byref(e)))
+        return n.value, o.value, e.value
+
+    def replica_map(self, part: int):
+        """(ext_ids u64, owner u8, role u8, home u32) in local row order."""
+        n, _, _ = self.part_counts(part)
+        ext = np.zeros(n, np.uint64); own = np.zeros(n, np.uint8)
+        role = np.zeros(n, np.uint8); home = np.zeros(n, np.uint32)
+        check(lib.catgnn_artifact_replica_map(self.handle, part, _ptr(ext), _ptr(own), _ptr(role), _ptr(home)))
+        return ext, own, role, home
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.catgnn_artifact_close(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def replication_factor(artifact: Artifact) -> float:
+    """metrics.cpp:9-12: sum of node records / |V| (f64)."""
+    return artifact.info.replication_factor
+
+
+@dataclass
+class LocalAdjacency:
+    """train.hpp:18-24 (offsets widened to u64)."""
+    offsets: np.ndarray
+    neighbors: np.ndarray
+
+    def rows(self) -> int:
+        return 0 if self.offsets.size == 0 else self.offsets.size - 1
+
+
+class Shard:
+    """Device-resident gnnpart::Shard (train.hpp:84-91)."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+        self._info = None
+
+    # -- constructors ---------------------------------------------------
+    @classmethod
+    def from_edges(cls, rows: int, edges, features: Optional[np.ndarray] = None,
+                   ctx: Optional[Context] = None) -> "Shard":
+        ctx = ctx or default_context()
+        pairs = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+        feats = None
+        dim = 0
+        if features is not None:
+            feats = np.ascontiguousarray(features, dtype=np.float32)
+            dim = feats.shape[1]
+        h = C.c_void_p()
+        check(lib.catgnn_shard_create(ctx.handle, rows, _ptr(pairs), pairs.shape[0], _ptr(feats), dim,
+                                      C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_artifact(cls, artifact: Artifact, part: int, input: str = "", features: str = "",
+                      ctx: Optional[Context] = None) -> "Shard":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib.catgnn_shard_load(ctx.handle, artifact.handle, part, (input or "").encode(),
+                                    (features or "").encode(), C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_part(cls, ext_ids, owner, role, labels, edges_ext, features, ctx=None) -> "Shard":
+        ctx = ctx or default_context()
+        ext = np.ascontiguousarray(ext_ids, np.uint64)
+        own = np.ascontiguousarray(owner, np.uint8)
+        rl = np.ascontiguousarray(role, np.uint8)
+        lab = np.ascontiguousarray(labels, np.int32)
+        ed = np.ascontiguousarray(np.asarray(edges_ext, np.uint64).reshape(-1, 2))
+        feats = np.ascontiguousarray(features, np.float32) if features is not None else None
+        dim = 0 if feats is None else feats.shape[1]
+        h = C.c_void_p()
+        check(lib.catgnn_shard_create_from_part(ctx.handle, ext.size, _ptr(ext), _ptr(own), _ptr(rl), _ptr(lab),
+                                                _ptr(ed), ed.shape[0], _ptr(feats), dim, C.byref(h)))
+        return cls(h, ctx)
+
+    # -- accessors -------------------------------------------------------
+    @property
+    def info(self) -> ShardInfo:
+        inf = ShardInfo()
+        check(lib.catgnn_shard_get_info(self.handle, C.byref(inf)))
+        return inf
+
+    @property
+    def rows(self) -> int:
+        return int(self.info.rows)
+
+    @property
+    def dim(self) -> int:
+        return int(self.info.dim)
+
+    def adjacency(self) -> LocalAdjacency:
+        inf = self.info
+        off = np.zeros(inf.rows + 1, np.uint64)
+        nb = np.zeros(max(inf.nnz, 1), np.uint32)
+        check(lib.catgnn_csr_export(self.handle, _ptr(off), _ptr(nb)))
+        return LocalAdjacency(off, nb[: inf.nnz])
+
+    def set_labels(self, labels, train_rows=(), val_rows=(), test_rows=()):
+        lab = np.ascontiguousarray(labels, np.int32)
+        tr = np.ascontiguousarray(train_rows, np.uint32)
+        va = np.ascontiguousarray(val_rows, np.uint32)
+        te = np.ascontiguousarray(test_rows, np.uint32)
+        check(lib.catgnn_shard_set_labels(self.handle, _ptr(lab), _ptr(tr), tr.size, _ptr(va), va.size,
+                                          _ptr(te), te.size))
+
+    def upload_features(self, features: np.ndarray):
+        f = np.ascontiguousarray(features, np.float32)
+        check(lib.catgnn_shard_upload_features(self.handle, _ptr(f), f.shape[1]))
+
+    def role_rows(self, role: int) -> np.ndarray:
+        inf = self.info
+        n = {1: inf.n_train, 2: inf.n_val, 3: inf.n_test}[role]
+        out = np.zeros(max(n, 1), np.uint32)
+        check(lib.catgnn_shard_role_rows(self.handle, role, _ptr(out)))
+        return out[:n]
+
+    @property
+    def train_rows(self):
+        return self.role_rows(1)
+
+    @property
+    def val_rows(self):
+        return self.role_rows(2)
+
+    @property
+    def test_rows(self):
+        return self.role_rows(3)
+
+    @property
+    def labels(self) -> np.ndarray:
+        out = np.zeros(max(self.rows, 1), np.int32)
+        check(lib.catgnn_shard_labels(self.handle, _ptr(out)))
+        return out[: self.rows]
+
+    def features(self, propagated: bool = False) -> np.ndarray:
+        out = np.zeros((self.rows, self.dim), np.float32)
+        check(lib.catgnn_shard_export_features(self.handle, 1 if propagated else 0, _ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.catgnn_shard_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_adjacency(rows: int, edges, ctx: Optional[Context] = None) -> LocalAdjacency:
+    """train.cpp:30-47 on the device; bit-exact offsets/neighbors."""
+    s = Shard.from_edges(rows, edges, None, ctx)
+    try:
+        return s.adjacency()
+    finally:
+        s.close()
+
+
+def sgc_propagate(shard: Shard, hops: int) -> np.ndarray:
+    """train.cpp:49-65: hops rounds of (x_i + sum_j x_j) / (1 + deg_i)."""
+    check(lib.catgnn_sgc_propagate(shard.handle, hops))
+    return shard.features(propagated=True)
+
+
+@dataclass
+class ModelParams:
+    """train.hpp:34-38 (float32)."""
+    weight: np.ndarray  # dim x classes
+    bias: np.ndarray    # classes
+    epochs_trained: int = 0
+
+    def copy(self) -> "ModelParams":
+        return ModelParams(self.weight.copy(), self.bias.copy(), self.epochs_trained)
+
+
+def zero_params(dim: int, classes: int) -> ModelParams:
+    """train.cpp:67-72."""
+    return ModelParams(np.zeros((dim, classes), np.float32), np.zeros(classes, np.float32))
+
+
+def _wb(p: ModelParams):
+    p.weight = np.ascontiguousarray(p.weight, np.float32)
+    p.bias = np.ascontiguousarray(p.bias, np.float32)
+    return p.weight, p.bias
+
+
+def softmax_loss(params: ModelParams, shard: Shard, rows) -> float:
+    """train.cpp:74-84 over the given rows of the propagated features."""
+    W, b = _wb(params)
+    r = np.ascontiguousarray(rows, np.uint32)
+    out = C.c_double()
+    check(lib.catgnn_softmax_loss(shard.handle, _ptr(W), _ptr(b), W.shape[1], _ptr(r), r.size, C.byref(out)))
+    return out.value
+
+
+def softmax_gradient(params: ModelParams, shard: Shard, rows):
+    """train.cpp:86-94 -> (grad_weight, grad_bias)."""
+    W, b = _wb(params)
+    r = np.ascontiguousarray(rows, np.uint32)
+    gW = np.zeros_like(W); gb = np.zeros_like(b)
+    check(lib.catgnn_softmax_gradient(shard.handle, _ptr(W), _ptr(b), W.shape[1], _ptr(r), r.size, _ptr(gW),
+                                      _ptr(gb)))
+    return gW, gb
+
+
+def train_epochs(params, shards, cfg: TrainConfig, epoch_begin: int, epoch_end: int, seeds):
+    """train.cpp:96-128.  params/shards/seeds may be lists: replicas train in one launch."""
+    single = isinstance(params, ModelParams)
+    plist = [params] if single else list(params)
+    slist = [shards] if single else list(shards)
+    seeds = [seeds] if single else list(seeds)
+    if not plist:
+        return params
+    ws = [_wb(p)[0] for p in plist]
+    bs = [p.bias for p in plist]
+    n = len(plist)
+    Wp = (C.c_void_p * n)(*[w.ctypes.data for w in ws])
+    bp = (C.c_void_p * n)(*[b.ctypes.data for b in bs])
+    sh = (C.c_void_p * n)(*[s.handle.value for s in slist])
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    check(lib.catgnn_train_epochs(n, sh, Wp, bp, ws[0].shape[1], cfg.lr, cfg.batch, epoch_begin, epoch_end,
+                                  _ptr(sd)))
+    for p in plist:
+        p.epochs_trained = epoch_end
+    return params
+
+
+def train_local(shard: Shard, cfg: TrainConfig) -> ModelParams:
+    """train.cpp:130-137 (expects propagated features)."""
+    classes = max(int(shard.labels.max(initial=0)) + 1, 1)
+    p = zero_params(shard.dim, classes)
+    train_epochs(p, shard, cfg, 0, cfg.epochs, cfg.seed)
+    return p
+
+
+def sync_weights(counts) -> np.ndarray:
+    """train.cpp:139-152."""
+    c = np.ascontiguousarray(counts, np.uint64)
+    a = np.zeros(c.size, np.float64)
+    check(lib.catgnn_sync_weights(_ptr(c), c.size, _ptr(a)))
+    return a
+
+
+def model_average(params: List[ModelParams], counts, ctx: Optional[Context] = None) -> ModelParams:
+    """train.cpp:154-172 (computed on the device)."""
+    ctx = ctx or default_context()
+    if not params or len(params) != len(counts):
+        raise DataError("model averaging needs one training count per replica")
+    shapes = {(p.weight.shape, p.bias.shape) for p in params}
+    if len(shapes) != 1:
+        raise DataError("model shapes differ across replicas")
+    flat = [np.concatenate([np.asarray(p.weight, np.float32).ravel(), np.asarray(p.bias, np.float32)])
+            for p in params]
+    n = len(flat)
+    ptrs = (C.c_void_p * n)(*[f.ctypes.data for f in flat])
+    c = np.ascontiguousarray(counts, np.uint64)
+    out = np.zeros_like(flat[0])
+    check(lib.catgnn_model_average_host(ctx.handle, n, ptrs, out.size, _ptr(c), _ptr(out)))
+    W = params[0].weight
+    return ModelParams(out[: W.size].reshape(W.shape).copy(), out[W.size:].copy(), params[0].epochs_trained)
+
+
+def evaluate_micro_f1(params: ModelParams, shard: Shard, mask_rows) -> float:
+    """train.cpp:174-198 on the propagated features."""
+    W, b = _wb(params)
+    m = np.ascontiguousarray(mask_rows, np.uint32)
+    out = C.c_double()
+    check(lib.catgnn_evaluate_micro_f1(shard.handle, _ptr(W), _ptr(b), W.shape[1], _ptr(m), m.size, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class TrainingData:
+    """train.hpp:93-96."""
+    shards: List[Shard]
+    global_: Shard
+    artifact: Optional[Artifact] = None
+
+
+def load_training_data(artifact_dir: str, input: str = "", features: str = "",
+                       ctx: Optional[Context] = None, with_global: bool = True) -> TrainingData:
+    """train.cpp:216-287: one device shard per partition plus the global shard."""
+    ctx = ctx or default_context()
+    art = Artifact(artifact_dir)
+    g = Shard.from_artifact(art, -1, input, features, ctx) if with_global else None
+    shards = [Shard.from_artifact(art, s, input, features, ctx) for s in range(art.num_partitions)]
+    return TrainingData(shards, g, art)
+
+
+@dataclass
+class SyncPoint:
+    epoch: int
+    syncs: int
+    val_f1: float
+    test_f1: float
+
+
+@dataclass
+class DistTrainResult:
+    params: ModelParams
+    history: List[SyncPoint] = field(default_factory=list)
+    averaging_ops: int = 0
+
+
+def distributed_train(data: TrainingData, workers: int, sync_interval: int, cfg: TrainConfig) -> DistTrainResult:
+    """train.cpp:289-340 on one device (workers are logical; p % q == 0)."""
+    g = data.global_
+    gi = g.info
+    p = len(data.shards)
+    W = np.zeros((gi.dim, gi.classes), np.float32)
+    b = np.zeros(gi.classes, np.float32)
+    cap = (cfg.epochs + max(sync_interval, 1) - 1) // max(sync_interval, 1) + 1
+    he = np.zeros(cap, np.uint64); hs = np.zeros(cap, np.uint64)
+    hv = np.zeros(cap, np.float64); ht = np.zeros(cap, np.float64)
+    res = DistResult(W.ctypes.data, b.ctypes.data, 0, 0, he.ctypes.data, hs.ctypes.data, hv.ctypes.data,
+                     ht.ctypes.data, cap, 0, 0)
+    sh = (C.c_void_p * max(p, 1))(*[s.handle.value for s in data.shards])
+    check(lib.catgnn_distributed_train(p, sh, g.handle, workers, sync_interval, C.byref(cfg), C.byref(res)))
+    n = min(res.n_hist, cap)
+    hist = [SyncPoint(int(he[i]), int(hs[i]), float(hv[i]), float(ht[i])) for i in range(n)]
+    return DistTrainResult(ModelParams(W, b, cfg.epochs), hist, int(res.averaging_ops))

@@ -1,0 +1,247 @@
+"""GPU parity of the reference's own hot path (the SGC training simulator,
+proj/src/train.cpp) — every call goes through the C ABI into the sm_100a
+kernels and is compared with the oracle (the unmodified reference compiled
+with the Eigen shim) on identical inputs and seeds.
+
+Tolerances: CSR / replica map / RF bit-exact; float32 device results vs the
+f64 reference within 2e-3 relative (north star), tighter where the math is a
+plain sum; final accuracy within 0.5 pt at config-1 scale."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import make_artifact, make_dataset, rel_err
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_small.npz")
+
+
+@pytest.fixture(scope="module")
+def gp():
+    from paper_2404_02300_b200 import gnnpart
+    return gnnpart
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+# --------------------------------------------------------------- K1 CSR
+@pytest.mark.parametrize("rows,edges,seed", [(1, 0, 0), (5, 0, 1), (10, 40, 2), (300, 5000, 3),
+                                             (2000, 100, 4), (4096, 60000, 5)])
+def test_csr_bit_exact_random(gp, rows, edges, seed):
+    rng = np.random.default_rng(seed)
+    pairs = rng.integers(0, rows, size=(edges, 2)).astype(np.uint32)
+    if edges:
+        pairs[::7, 1] = pairs[::7, 0]          # self-loops
+        pairs[1::11] = pairs[0]                # duplicates
+    adj = gp.build_adjacency(rows, pairs)
+    off, nb = ref.build_adjacency(rows, pairs)
+    assert np.array_equal(adj.offsets, off.astype(np.uint64))
+    assert np.array_equal(adj.neighbors, nb)
+
+
+def test_csr_rejects_out_of_range(gp):
+    with pytest.raises(gp.DataError, match="outside the row space"):
+        gp.build_adjacency(3, np.array([[0, 3]], np.uint32))
+
+
+def test_csr_hub_rows_split(gp):
+    # a hub far above the split threshold keeps bit-exact CSR and exact sums
+    rows = 5000
+    hub = np.stack([np.zeros(4000, np.uint32), np.arange(1, 4001, dtype=np.uint32)], 1)
+    rng = np.random.default_rng(9)
+    rest = rng.integers(0, rows, size=(3000, 2)).astype(np.uint32)
+    pairs = np.concatenate([hub, rest])
+    s = gp.Shard.from_edges(rows, pairs, rng.normal(size=(rows, 12)).astype(np.float32))
+    assert s.info.heavy_rows >= 1
+    off, nb = ref.build_adjacency(rows, pairs)
+    adj = s.adjacency()
+    assert np.array_equal(adj.offsets, off.astype(np.uint64)) and np.array_equal(adj.neighbors, nb)
+    y = gp.sgc_propagate(s, 2)
+    yr = ref.sgc_propagate(off, nb, s.features().astype(np.float64), 2)
+    assert rel_err(y, yr) < 1e-5
+
+
+def test_golden_shards_csr_and_replica_map(gp, golden):
+    g = golden
+    n = int(g["num_nodes"])
+    for s in range(int(g["config"][5])):
+        sh = gp.Shard.from_part(g[f"p{s}_ext"], g[f"p{s}_owner"], g[f"p{s}_role"], g[f"s{s}_labels"],
+                                g[f"p{s}_edges"], g["X"][g[f"p{s}_ext"].astype(np.int64)])
+        adj = sh.adjacency()
+        assert np.array_equal(adj.offsets, g[f"s{s}_offsets"].astype(np.uint64))
+        assert np.array_equal(adj.neighbors, g[f"s{s}_neighbors"])
+        assert np.array_equal(sh.train_rows, g[f"s{s}_train"])
+    gs = gp.Shard.from_edges(n, g["edges"].astype(np.uint32), g["X"])
+    adj = gs.adjacency()
+    assert np.array_equal(adj.offsets, g["g_offsets"].astype(np.uint64))
+    assert np.array_equal(adj.neighbors, g["g_neighbors"])
+
+
+def test_load_training_data_matches_reference(gp, small_artifact):
+    data = gp.load_training_data(small_artifact)
+    td = ref.TrainingData(small_artifact)
+    for s in [-1] + list(range(len(data.shards))):
+        mine = data.global_ if s < 0 else data.shards[s]
+        theirs = td.shard(s)
+        adj = mine.adjacency()
+        assert np.array_equal(adj.offsets, theirs.offsets.astype(np.uint64))
+        assert np.array_equal(adj.neighbors, theirs.neighbors)
+        assert np.array_equal(mine.labels, theirs.labels)
+        assert np.array_equal(mine.train_rows, theirs.train_rows)
+        assert np.array_equal(mine.val_rows, theirs.val_rows)
+        assert np.array_equal(mine.test_rows, theirs.test_rows)
+        assert np.array_equal(mine.features().astype(np.float64), theirs.features)
+
+
+def test_load_without_split_features(gp, small_ds):
+    # has_features = false: rows gathered from the global matrix (train.cpp:277-283)
+    art = make_artifact(small_ds, p=2, with_features=False, tag="nofeat")
+    data = gp.load_training_data(art, with_global=False)
+    td = ref.TrainingData(art)
+    for s, sh in enumerate(data.shards):
+        assert np.array_equal(sh.features().astype(np.float64), td.shard(s).features)
+
+
+# --------------------------------------------------------------- K2 SGC
+def test_sgc_propagate_star_kat(gp):
+    s = gp.Shard.from_edges(3, [[0, 1], [0, 2]], np.array([[0.0], [3.0], [3.0]], np.float32))
+    y = gp.sgc_propagate(s, 1).ravel()
+    np.testing.assert_allclose(y, [2.0, 1.5, 1.5], rtol=1e-6)
+    np.testing.assert_array_equal(gp.sgc_propagate(s, 0).ravel(), [0.0, 3.0, 3.0])
+
+
+@pytest.mark.parametrize("dim", [1, 4, 8, 12, 48, 64, 100, 256, 602, 1433])
+def test_sgc_propagate_widths(gp, dim):
+    rng = np.random.default_rng(dim)
+    rows = 700
+    pairs = rng.integers(0, rows, size=(6000, 2)).astype(np.uint32)
+    x = rng.normal(size=(rows, dim)).astype(np.float32)
+    s = gp.Shard.from_edges(rows, pairs, x)
+    off, nb = ref.build_adjacency(rows, pairs)
+    y = gp.sgc_propagate(s, 2)
+    yr = ref.sgc_propagate(off, nb, x.astype(np.float64), 2)
+    assert rel_err(y, yr) < 1e-5
+    ones = gp.Shard.from_edges(rows, pairs, np.ones((rows, dim), np.float32))
+    np.testing.assert_allclose(gp.sgc_propagate(ones, 3), 1.0, rtol=2e-6)
+
+
+def test_sgc_propagate_golden(gp, golden):
+    g = golden
+    hops = int(g["config"][6])
+    for s in range(int(g["config"][5])):
+        sh = gp.Shard.from_part(g[f"p{s}_ext"], g[f"p{s}_owner"], g[f"p{s}_role"], g[f"s{s}_labels"],
+                                g[f"p{s}_edges"], g["X"][g[f"p{s}_ext"].astype(np.int64)])
+        assert rel_err(gp.sgc_propagate(sh, hops), g[f"s{s}_prop"]) < 1e-5
+
+
+# ------------------------------------------------------ softmax / SGD / F1
+def golden_shard0(gp, g):
+    sh = gp.Shard.from_part(g["p0_ext"], g["p0_owner"], g["p0_role"], g["s0_labels"], g["p0_edges"],
+                            g["X"][g["p0_ext"].astype(np.int64)])
+    gp.sgc_propagate(sh, int(g["config"][6]))
+    return sh
+
+
+def test_softmax_gradient_and_loss_golden(gp, golden):
+    g = golden
+    sh = golden_shard0(gp, g)
+    P = gp.ModelParams(g["W0"].astype(np.float32), g["b0"].astype(np.float32))
+    gW, gb = gp.softmax_gradient(P, sh, g["grad_rows"])
+    assert rel_err(gW, g["gW"]) < 1e-4 and rel_err(gb, g["gb"]) < 1e-4
+    assert abs(gp.softmax_loss(P, sh, g["grad_rows"]) - float(g["loss"])) < 1e-5 * abs(float(g["loss"]))
+
+
+def test_train_epochs_golden(gp, golden):
+    g = golden
+    sh = golden_shard0(gp, g)
+    P = gp.zero_params(sh.dim, int(g["config"][3]))
+    cfg = gp.TrainConfig(lr=float(g["lr"]), batch=int(g["config"][9]))
+    gp.train_epochs(P, sh, cfg, 0, 3, 11)
+    assert rel_err(P.weight, g["te_W"]) < 1e-4 and rel_err(P.bias, g["te_b"]) < 1e-4
+
+
+def test_train_epochs_lr0_determinism_and_errors(gp, golden):
+    g = golden
+    sh = golden_shard0(gp, g)
+    W0 = gp.ModelParams(g["W0"].astype(np.float32), g["b0"].astype(np.float32))
+    P = W0.copy()
+    gp.train_epochs(P, sh, gp.TrainConfig(lr=0.0, batch=16), 0, 3, 5)
+    assert np.array_equal(P.weight, W0.weight)
+    A = W0.copy(); B = W0.copy()
+    cfg = gp.TrainConfig(lr=0.1, batch=16)
+    gp.train_epochs(A, sh, cfg, 0, 3, 5)
+    gp.train_epochs(B, sh, cfg, 0, 3, 5)
+    assert np.array_equal(A.weight, B.weight)
+    with pytest.raises(gp.ConfigError, match="batch size"):
+        gp.train_epochs(W0.copy(), sh, gp.TrainConfig(batch=0), 0, 1, 5)
+
+
+def test_model_average_kats(gp):
+    a = gp.ModelParams(np.array([[2.0]], np.float32), np.zeros(1, np.float32))
+    b = gp.ModelParams(np.array([[4.0]], np.float32), np.zeros(1, np.float32))
+    assert gp.model_average([a, b], [1, 3]).weight[0, 0] == 3.5
+    assert gp.model_average([a, b], [5, 0]).weight[0, 0] == 2.0
+    with pytest.raises(gp.DataError):
+        gp.model_average([a, b], [0, 0])
+
+
+def test_evaluate_micro_f1_kats(gp):
+    x = np.eye(4, dtype=np.float32)
+    s = gp.Shard.from_edges(4, np.zeros((0, 2), np.uint32), x)
+    s.set_labels(np.arange(4))
+    gp.sgc_propagate(s, 0)
+    assert gp.evaluate_micro_f1(gp.ModelParams(np.eye(4, dtype=np.float32) * 5, np.zeros(4, np.float32)),
+                                s, np.arange(4)) == 1.0
+    const = gp.ModelParams(np.zeros((4, 4), np.float32), np.array([0, 0, 1, 0], np.float32))
+    assert gp.evaluate_micro_f1(const, s, np.arange(4)) == 0.25
+    with pytest.raises(gp.DataError, match="mask is empty"):
+        gp.evaluate_micro_f1(const, s, np.array([], np.uint32))
+
+
+def test_distributed_train_golden(gp, golden):
+    g = golden
+    scale, edges, dim, classes, seed, p, hops, epochs, sync, batch = g["config"].tolist()
+    shards = []
+    for s in range(p):
+        shards.append(gp.Shard.from_part(g[f"p{s}_ext"], g[f"p{s}_owner"], g[f"p{s}_role"],
+                                         g[f"s{s}_labels"], g[f"p{s}_edges"],
+                                         g["X"][g[f"p{s}_ext"].astype(np.int64)]))
+    gs = gp.Shard.from_edges(int(g["num_nodes"]), g["edges"].astype(np.uint32), g["X"])
+    gs.set_labels(g["g_labels"], g["g_train"], g["g_val"], g["g_test"])
+    data = gp.TrainingData(shards, gs)
+    res = gp.distributed_train(data, 1, sync, gp.TrainConfig(epochs=epochs, lr=float(g["lr"]), batch=batch,
+                                                             prop_hops=hops, seed=seed))
+    assert res.averaging_ops == int(g["dt_ops"])
+    assert rel_err(res.params.weight, g["dt_W"]) < 1e-4
+    hist = np.array([[h.epoch, h.syncs, h.val_f1, h.test_f1] for h in res.history])
+    assert np.array_equal(hist[:, :2], g["dt_hist"][:, :2])
+    nv = max(len(g["g_val"]), 1)
+    assert np.abs(hist[:, 2:] - g["dt_hist"][:, 2:]).max() <= 1.0 / nv + 1e-12
+
+
+def test_distributed_train_config_errors(gp, small_artifact):
+    data = gp.load_training_data(small_artifact)
+    with pytest.raises(gp.ConfigError, match="multiple of the worker count"):
+        gp.distributed_train(data, 3, 1, gp.TrainConfig(epochs=1))
+    with pytest.raises(gp.ConfigError, match="sync interval"):
+        gp.distributed_train(data, 1, 0, gp.TrainConfig(epochs=1))
+
+
+@pytest.mark.slow
+def test_config1_distributed_parity(gp, tmp_path_factory):
+    """Config 1 (RMAT 2^16, 524,288 edges, d=64, C=8, SPRING p=2): GPU vs reference."""
+    d = make_dataset(tmp_path_factory.mktemp("cfg1"), scale=16, edges=524288, dim=64, classes=8, seed=1)
+    art = make_artifact(d, p=2)
+    td = ref.TrainingData(art)
+    ep = 10
+    want = td.distributed_train(1, 1, epochs=ep, lr=0.01, batch=512, prop_hops=2, seed=0)
+    data = gp.load_training_data(art)
+    got = gp.distributed_train(data, 1, 1, gp.TrainConfig(epochs=ep, lr=0.01, batch=512, prop_hops=2, seed=0))
+    assert rel_err(got.params.weight, want["W"]) < 1e-3
+    for h, w in zip(got.history, want["history"]):
+        assert abs(h.val_f1 - w[2]) <= 0.005 and abs(h.test_f1 - w[3]) <= 0.005
