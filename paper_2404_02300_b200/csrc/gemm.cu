@@ -1,0 +1,403 @@
+// K3 — dense layer transform on the 5th-generation tensor cores.
+//
+//   C[M x N] = A[M x K] . B[N x K]^T        (A, B K-major fp32 in HBM, TF32 MMA,
+//                                            fp32 accumulation in TMEM)
+//
+// One CTA computes a 128 x BN tile (BN <= 256, multiple of 16) over a K range:
+//   warp 0      TMA producer: 128x32 and BNx32 fp32 boxes (128-byte rows,
+//               SWIZZLE_128B) into an S-stage shared-memory ring, completion on
+//               per-stage mbarriers (cp.async.bulk.tensor ... complete_tx)
+//   warp 1      TMEM allocation + one elected thread issuing tcgen05.mma
+//               .cta_group::1.kind::tf32 (M=128, N=BN, K=8 per instruction,
+//               4 per 32-float k-block); tcgen05.commit frees each stage and
+//               finally signals the accumulator
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
+//               32*(w%4)..+31 = tile rows), fused row-scale / bias / ReLU /
+//               ReLU-backward mask, 128-bit stores — or raw split-K partials
+//               that gemm_reduce_kernel sums in split order (deterministic).
+// Tail rows/columns and K past the tensor extent are zero-filled by TMA.
+#include <cuda.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "gemm.hpp"
+
+namespace catgnn {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;              // fp32 elements per k-block row = 128 bytes
+constexpr int A_STAGE = BM * BK * 4;  // 16 KB
+constexpr int kThreads = 192;
+
+struct GemmArgs {
+  uint32_t M, N, K;
+  uint32_t BN;
+  uint32_t stages;
+  uint32_t kb_per_split;
+  uint32_t tmem_cols;
+  uint32_t idesc;
+  GemmEpi epi;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+// Parity wait with a watchdog: a pipeline bug traps (kernel error) instead of
+// hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  uint64_t t0 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    if (done) return;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 2000000000ull) __trap();  // 2 s
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: rows of 128 bytes,
+// 8-row core groups 1024 bytes apart (SBO), LBO unused (1), version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
+  if (e.rowscale && col >= e.scale_col_begin) v *= __ldg(e.rowscale + row);
+  if (e.bias) v += __ldg(e.bias + col);
+  if (e.relu) v = fmaxf(v, 0.f);
+  if (e.mask && !(__ldg(e.mask + (size_t)row * e.mask_ld + e.mask_col + col) > 0.f)) v = 0.f;
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t BN = args.BN;
+  const uint32_t B_STAGE = BN * BK * 4;
+  const uint32_t S = args.stages;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)S * A_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)S * B_STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* accum = bars + 2 * S;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const uint32_t nkb_total = (args.K + BK - 1) / BK;
+  const uint32_t kb0 = blockIdx.z * args.kb_per_split;
+  const uint32_t kb1 = min(nkb_total, kb0 + args.kb_per_split);
+  const uint32_t nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < S; ++i) {
+      mbar_init(smem_u32(full + i), 1);
+      mbar_init(smem_u32(empty + i), 1);
+    }
+    mbar_init(smem_u32(accum), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(args.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = A_STAGE + B_STAGE;
+      for (uint32_t i = 0; i < nkb; ++i) {
+        const uint32_t s = i % S, ph = (i / S) & 1;
+        mbar_wait(smem_u32(empty + s), ph ^ 1);
+        mbar_expect_tx(smem_u32(full + s), bytes);
+        const int kx = (int)((kb0 + i) * BK);
+        tma_load_2d(smem_u32(sA + (size_t)s * A_STAGE), &tmA, kx, (int)m0, smem_u32(full + s));
+        tma_load_2d(smem_u32(sB + (size_t)s * B_STAGE), &tmB, kx, (int)n0, smem_u32(full + s));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (uint32_t i = 0; i < nkb; ++i) {
+        const uint32_t s = i % S, ph = (i / S) & 1;
+        mbar_wait(smem_u32(full + s), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
+        const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
+          mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
+                   (i > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(smem_u32(empty + s));
+      }
+      if (nkb) mma_commit(smem_u32(accum));
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const uint32_t q = warp & 3;
+    const uint32_t row = m0 + q * 32 + lane;
+    if (nkb) {
+      mbar_wait(smem_u32(accum), 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    const GemmEpi& e = args.epi;
+    for (uint32_t c = 0; c < BN; c += 32) {
+      float v[32];
+      if (nkb) {
+        tmem_ld32(tmem + ((q * 32u) << 16) + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (row >= args.M) continue;
+      const uint32_t col0 = n0 + c;
+      if (e.partial) {
+        float* dst = e.partial + ((size_t)blockIdx.z * args.M + row) * args.N;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < args.N) dst[col0 + i] = v[i];
+        continue;
+      }
+      float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
+      if (col0 + 32 <= args.N) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 o = make_float4(apply_epi(e, row, col0 + i, v[i]), apply_epi(e, row, col0 + i + 1, v[i + 1]),
+                                 apply_epi(e, row, col0 + i + 2, v[i + 2]),
+                                 apply_epi(e, row, col0 + i + 3, v[i + 3]));
+          *reinterpret_cast<float4*>(dst + i) = o;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < args.N) dst[i] = apply_epi(e, row, col0 + i, v[i]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(args.tmem_cols));
+  }
+}
+
+__global__ void gemm_reduce_kernel(const float* __restrict__ partial, uint32_t splits, uint32_t M,
+                                   uint32_t N, GemmEpi e) {
+  const uint64_t total = (uint64_t)M * N;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (uint32_t z = 0; z < splits; ++z) acc += partial[(uint64_t)z * total + i];
+    const uint32_t row = (uint32_t)(i / N), col = (uint32_t)(i % N);
+    e.out[(size_t)row * e.ld_out + e.out_col + col] = apply_epi(e, row, col, acc);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) throw InternalError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(const float* ptr, uint64_t rows, uint64_t K, uint32_t ld, uint32_t box_rows) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16)
+    throw ConfigError("GEMM operand must be 16-byte aligned with a row stride multiple of 4 floats");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw InternalError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+uint32_t pow2_cols(uint32_t n) {
+  uint32_t c = 32;
+  while (c < n) c <<= 1;
+  return c;
+}
+
+}  // namespace
+
+void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
+             uint32_t N, uint32_t K, const GemmEpi& epi_in, uint32_t split_k) {
+  if (M == 0 || N == 0) return;
+  GemmEpi epi = epi_in;
+  if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
+  if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  const uint32_t BN = N >= 256 ? 256 : round_up(N, 16);
+  const uint32_t nkb = (K + BK - 1) / BK;
+  const uint32_t mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
+  uint32_t splits = 1;
+  if (split_k == 0) {
+    // fill the SMs when the tile grid is small and K is long
+    const uint32_t tiles = mt * nt;
+    if (tiles < (uint32_t)ctx->num_sms && nkb >= 8)
+      splits = std::min<uint32_t>(std::max<uint32_t>(1, (uint32_t)ctx->num_sms / tiles), nkb / 4);
+  } else {
+    splits = std::min<uint32_t>(split_k, std::max<uint32_t>(1, nkb));
+  }
+  splits = std::max<uint32_t>(1, splits);
+  const uint32_t kbps = std::max<uint32_t>(1, (nkb + splits - 1) / splits);
+  splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
+
+  const uint32_t b_stage = BN * BK * 4;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  uint32_t stages = (uint32_t)std::min<size_t>(6, budget / (A_STAGE + b_stage));
+  if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
+  const size_t smem = 1024 + (size_t)stages * (A_STAGE + b_stage) + (2 * stages + 2) * 8;
+
+  GemmArgs args{};
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.BN = BN;
+  args.stages = stages;
+  args.kb_per_split = kbps;
+  args.tmem_cols = pow2_cols(BN);
+  // instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
+  args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  float* partial = nullptr;
+  if (splits > 1) {
+    partial = ctx->scratch_buf<float>("gemm_partial", (size_t)splits * M * N);
+    args.epi = epi;
+    args.epi.partial = partial;
+  } else {
+    args.epi = epi;
+    args.epi.partial = nullptr;
+  }
+  CUtensorMap ta = make_map(A, M, K, lda, BM);
+  CUtensorMap tb = make_map(B, N, K, ldb, BN);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CG_CUDA(cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
+  int t = ctx->begin_timed(1);
+  gemm_tf32_kernel<<<dim3(mt, nt, splits), kThreads, smem, ctx->stream>>>(ta, tb, args);
+  CG_CHECK_LAUNCH();
+  ctx->launches++;
+  if (splits > 1) {
+    const uint64_t total = (uint64_t)M * N;
+    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
+    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(partial, splits, M, N, epi);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  ctx->end_timed(t);
+}
+
+}  // namespace catgnn
+
+extern "C" int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
+                              const float* B, float* Cout, uint32_t split_k) {
+  using namespace catgnn;
+  return guarded([&] {
+    if (!ctx) throw ConfigError("null context");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    const uint32_t lda = round_up(std::max(K, 1u), 4), ldc = round_up(N, 4);
+    float* dA = ctx->scratch_buf<float>("gt_A", (size_t)std::max(M, 1u) * lda);
+    float* dB = ctx->scratch_buf<float>("gt_B", (size_t)std::max(N, 1u) * lda);
+    float* dC = ctx->scratch_buf<float>("gt_C", (size_t)std::max(M, 1u) * ldc);
+    cudaStream_t st = ctx->stream;
+    CG_CUDA(cudaMemsetAsync(dA, 0, (size_t)std::max(M, 1u) * lda * 4, st));
+    CG_CUDA(cudaMemsetAsync(dB, 0, (size_t)std::max(N, 1u) * lda * 4, st));
+    if (K) {
+      CG_CUDA(cudaMemcpy2DAsync(dA, lda * 4, A, K * 4, K * 4, M, cudaMemcpyHostToDevice, st));
+      CG_CUDA(cudaMemcpy2DAsync(dB, lda * 4, B, K * 4, K * 4, N, cudaMemcpyHostToDevice, st));
+    }
+    GemmEpi e{};
+    e.out = dC;
+    e.ld_out = ldc;
+    gemm_tn(ctx, dA, lda, dB, lda, M, N, K, e, split_k);
+    CG_CUDA(cudaMemcpy2DAsync(Cout, N * 4, dC, ldc * 4, N * 4, M, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+  });
+}

@@ -1,0 +1,28 @@
+#pragma once
+
+#include "common.hpp"
+
+namespace catgnn {
+
+// Fused epilogue of K3, applied per output element (row, col):
+//   v = acc; v *= rowscale[row] (cols >= scale_col_begin); v += bias[col];
+//   v = relu(v); v = mask[row][mask_col+col] > 0 ? v : 0;  out[row][out_col+col] = v
+struct GemmEpi {
+  float* out = nullptr;
+  uint32_t ld_out = 0, out_col = 0;
+  const float* rowscale = nullptr;
+  uint32_t scale_col_begin = 0;
+  const float* bias = nullptr;
+  int relu = 0;
+  const float* mask = nullptr;
+  uint32_t mask_ld = 0, mask_col = 0;
+  float* partial = nullptr;  // internal (split-K workspace)
+};
+
+// C[M x N] = A[M x K] . B[N x K]^T with A (row stride lda) and B (row stride
+// ldb) K-major fp32 device matrices.  split_k = 0 picks a split automatically
+// (deterministic reduction in split order).
+void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
+             uint32_t N, uint32_t K, const GemmEpi& epi, uint32_t split_k = 1);
+
+}  // namespace catgnn

@@ -21,5 +21,4 @@ int catgnn_comm_create(catgnn_ctx, int, int, const char*, catgnn_comm*) PENDING
 int catgnn_comm_destroy(catgnn_comm) PENDING
 int catgnn_model_scale(catgnn_model, double) PENDING
 int catgnn_model_allreduce(catgnn_model, catgnn_comm) PENDING
-int catgnn_gemm_tn(catgnn_ctx, uint32_t, uint32_t, uint32_t, const float*, const float*, float*, uint32_t) PENDING
 }

@@ -1,0 +1,42 @@
+"""K3 tcgen05 TF32 GEMM vs a float64 NumPy product (TF32 inputs, fp32 accumulate:
+normwise relative error well inside the north star's 2e-3)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2404_02300_b200 import gnnpart as gp
+    return gp.Context(0)
+
+
+def gemm(ctx, A, B, split=1):
+    from paper_2404_02300_b200._lib import check, lib
+    A = np.ascontiguousarray(A, np.float32); B = np.ascontiguousarray(B, np.float32)
+    M, K = A.shape; N = B.shape[0]
+    out = np.zeros((M, N), np.float32)
+    check(lib.catgnn_gemm_tn(ctx.handle, M, N, K, A.ctypes.data_as(C.c_void_p), B.ctypes.data_as(C.c_void_p),
+                             out.ctypes.data_as(C.c_void_p), split))
+    return out
+
+
+@pytest.mark.parametrize("M,N,K,split", [(128, 16, 32, 1), (1, 16, 8, 1), (200, 48, 256, 1), (1000, 256, 602, 1),
+                                         (300, 602, 256, 1), (48, 256, 5000, 0), (256, 602, 20000, 0),
+                                         (513, 41, 100, 1), (130, 128, 64, 3)])
+def test_gemm_tn(ctx, M, N, K, split):
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    got = gemm(ctx, A, B, split)
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 1e-3, err
+
+
+def test_gemm_k_zero(ctx):
+    A = np.zeros((5, 0), np.float32); B = np.zeros((16, 0), np.float32)
+    assert np.all(gemm(ctx, A, B) == 0)

@@ -101,8 +101,11 @@ def test_load_training_data_matches_reference(gp, small_artifact):
 def test_load_without_split_features(gp, small_ds):
     # has_features = false: rows gathered from the global matrix (train.cpp:277-283)
     art = make_artifact(small_ds, p=2, with_features=False, tag="nofeat")
-    data = gp.load_training_data(art, with_global=False)
-    td = ref.TrainingData(art)
+    with pytest.raises(gp.ConfigError, match="features not recorded"):
+        gp.load_training_data(art, with_global=False)
+    data = gp.load_training_data(art, input=small_ds["edge_file"], features=small_ds["feat_file"],
+                                 with_global=False)
+    td = ref.TrainingData(art, small_ds["edge_file"], small_ds["feat_file"])
     for s, sh in enumerate(data.shards):
         assert np.array_equal(sh.features().astype(np.float64), td.shard(s).features)
 
