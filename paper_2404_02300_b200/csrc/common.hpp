@@ -112,6 +112,8 @@ struct catgnn_ctx_s {
   uint64_t agg_n = 0, gemm_n = 0;
   // named grow-only scratch buffers
   std::map<std::string, catgnn::DevBuf<unsigned char>> scratch;
+  // last (rows, row stride) each named activation buffer was used with
+  std::map<std::string, std::pair<uint64_t, uint32_t>> act_shape;
 
   template <typename T>
   T* scratch_buf(const std::string& name, size_t count) {

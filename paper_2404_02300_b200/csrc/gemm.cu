@@ -312,6 +312,14 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   GemmEpi epi = epi_in;
   if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
   if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  if (K == 0) {  // empty contraction: the epilogue of a zero accumulator
+    const uint64_t total = (uint64_t)M * N;
+    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
+    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(nullptr, 0, M, N, epi);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+    return;
+  }
   const uint32_t BN = N >= 256 ? 256 : round_up(N, 16);
   const uint32_t nkb = (K + BK - 1) / BK;
   const uint32_t mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;

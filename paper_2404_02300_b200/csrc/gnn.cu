@@ -1,0 +1,852 @@
+// GNN models of the north star (GCN-norm / SAGE-mean / GIN-sum), full-batch
+// per partition: forward, loss, backward, optimizer, model averaging and the
+// NCCL all-reduce of the averaged parameters.
+//
+// The reference trains SGC (propagation once, then a linear softmax model;
+// proj/src/train.cpp) and has no GCN/SAGE/GIN; these layers follow its
+// conventions: local CSR degrees, local rows in
+// node-table order, loss = mean cross-entropy over owned train rows, alpha-
+// weighted averaging of every parameter tensor (train.cpp:154-172), one "local
+// iteration" = one full-batch step.  Parity is against the NumPy restatement in
+// oracle/gnn_oracle.py (unpinned by the reference: it has no such models).
+//
+// Per layer, the aggregation runs at min(d_in, d_out):
+//   GCN  transform-first: T = dinv*(H W^T)  [K3 epi: row scale]
+//                         Z = dinv*(T_self + sum T_nbr) + b, H = relu(Z)   [K2]
+//   GCN  aggregate-first: A = dinv*(dinv*H_self + sum dinv*H_nbr)          [K2 pre+post]
+//                         Z = A W^T + b, H = relu(Z)                       [K3 epi]
+//   SAGE aggregate-first: cat = [H | mean_N(H)] ; Z = cat [W_s|W_n]^T + b
+//   SAGE transform-first: P = H [W_s;W_n]^T ; Z = P_s + mean_N(P_n) + b
+//   GIN  (eps = 0): as GCN with plain sums (no normalisation)
+// Backward uses the same CSR (A is symmetric, train.cpp:41-45 inserts both
+// directions) with the source-row scale applied as K2's `pre`, and the
+// weight gradients as split-K K3 GEMMs over transposed activations.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "artifact.hpp"
+#include "gemm.hpp"
+#include "sgc.hpp"
+#include "shard.hpp"
+
+using namespace catgnn;
+
+namespace catgnn {
+
+namespace {
+
+struct Layer {
+  uint32_t d_in = 0, d_out = 0;
+  uint32_t K_in = 0;    // round4(d_in): activation row stride of the input
+  uint32_t D_out = 0;   // round4(d_out)
+  bool agg_first = false;
+  // internal weight matrix (GEMM B operand): w_rows x w_cols
+  uint32_t w_rows = 0, w_cols = 0;
+  uint64_t off_w = 0, off_b = 0;
+  // logical (exported) weight shape
+  uint32_t lw_rows = 0, lw_cols = 0;
+  uint32_t gemm_n = 0;   // forward GEMM N (transform-first SAGE: D_out + d_out)
+};
+
+__device__ __forceinline__ float wsum(float v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+__device__ __forceinline__ float wmax(float v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
+}
+
+// K4: softmax cross-entropy over the train rows.  dZ[r] = (softmax(z_r) - onehot)
+// / n_train (rows not listed keep the caller's zeros); per-row loss for a
+// deterministic reduction.  Warp per row, lanes over classes.
+__global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uint32_t C,
+                                  const int32_t* __restrict__ labels, const uint32_t* __restrict__ rows,
+                                  uint64_t n, float* __restrict__ dZ, uint32_t lddz,
+                                  double* __restrict__ row_loss) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const float inv_n = 1.0f / (float)n;
+  for (uint64_t i = wid; i < n; i += nw) {
+    const uint32_t r = rows[i];
+    const float* z = Z + (size_t)r * ldz;
+    const int y = labels[r];
+    float m = -INFINITY;
+    for (uint32_t c = lane; c < C; c += 32) m = fmaxf(m, z[c]);
+    m = wmax(m);
+    float s = 0.f, zy = 0.f;
+    for (uint32_t c = lane; c < C; c += 32) {
+      s += expf(z[c] - m);
+      if ((int)c == y) zy = z[c];
+    }
+    s = wsum(s);
+    zy = wsum(zy);
+    for (uint32_t c = lane; c < C; c += 32) {
+      float p = expf(z[c] - m) / s;
+      if ((int)c == y) p -= 1.0f;
+      dZ[(size_t)r * lddz + c] = p * inv_n;
+    }
+    if (lane == 0) row_loss[i] = (double)m + log((double)s) - (double)zy;
+  }
+}
+
+// Deterministic sum of n doubles (single block, fixed order per thread, tree).
+__global__ void sum_doubles_kernel(const double* __restrict__ v, uint64_t n, double* out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) acc += v[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// Per-row argmax (first maximum) over role rows -> correct count.
+__global__ void argmax_correct_kernel(const float* __restrict__ Z, uint32_t ldz, uint32_t C,
+                                      const int32_t* __restrict__ labels, const uint32_t* __restrict__ rows,
+                                      uint64_t n, unsigned long long* correct) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = wid; i < n; i += nw) {
+    const uint32_t r = rows[i];
+    const float* z = Z + (size_t)r * ldz;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (uint32_t c = lane; c < C; c += 32)
+      if (z[c] > best) { best = z[c]; bi = (int)c; }
+#pragma unroll
+    for (int m = 16; m; m >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, best, m);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0 && bi == labels[r]) atomicAdd(correct, 1ull);
+  }
+}
+
+// Column sums of rows x width (ld): per-block partials, then fixed-order reduce.
+__global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, uint64_t rows,
+                                      uint32_t width, float* __restrict__ partial) {
+  const uint64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const uint64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  for (uint32_t c = threadIdx.x; c < width; c += blockDim.x) {
+    float acc = 0.f;
+    for (uint64_t r = r0; r < r1; ++r) acc += X[r * ld + c];
+    partial[(size_t)blockIdx.x * width + c] = acc;
+  }
+}
+__global__ void colsum_reduce_kernel(const float* __restrict__ partial, uint32_t blocks, uint32_t width,
+                                     float* __restrict__ out) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (uint32_t b = 0; b < blocks; ++b) acc += partial[(size_t)b * width + c];
+    out[c] = acc;
+  }
+}
+
+// K5: fused optimizer over the flat parameter vector.
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, uint64_t n, float lr, float b1, float b2, float eps,
+                            float bc1, float bc2) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+}
+__global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, uint64_t n, float lr) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] -= lr * g[i];
+}
+__global__ void scale_kernel(float* __restrict__ p, uint64_t n, double a) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = (float)((double)p[i] * a);
+}
+
+unsigned grid1d(uint64_t n) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16));
+}
+
+double unit_uniform(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+}  // namespace
+}  // namespace catgnn
+
+struct catgnn_model_s {
+  catgnn_ctx ctx = nullptr;
+  catgnn_model_config cfg{};
+  std::vector<Layer> layers;
+  uint64_t n_params = 0;
+  DevBuf<float> params, grads, m, v;
+  std::vector<DevBuf<float>> wT;  // per-layer W^T (w_cols x w_rows, ld round4(w_rows))
+  bool wT_valid = false;
+  uint64_t step = 0;
+  uint64_t last_rows = 0;
+  catgnn_shard last_shard = nullptr;
+  double last_loss = 0.0;
+};
+
+namespace catgnn {
+namespace {
+
+void check_model(catgnn_model m) {
+  if (!m) throw ConfigError("null model");
+  CG_CUDA(cudaSetDevice(m->ctx->device));
+}
+
+// Named activation buffer; zero-filled whenever its shape changes so padding
+// columns (never written by narrower producers) are exactly zero.
+float* act(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld, bool zero) {
+  float* p = ctx->scratch_buf<float>(name, std::max<uint64_t>(1, rows) * ld);
+  auto sig = std::make_pair(rows, ld);
+  auto it = ctx->act_shape.find(name);
+  if (zero || it == ctx->act_shape.end() || it->second != sig) {
+    CG_CUDA(cudaMemsetAsync(p, 0, std::max<uint64_t>(1, rows) * ld * 4, ctx->stream));
+    ctx->act_shape[name] = sig;
+  }
+  return p;
+}
+
+void plan_layers(catgnn_model_s* M) {
+  const auto& c = M->cfg;
+  M->layers.clear();
+  uint64_t off = 0;
+  for (uint32_t l = 0; l < c.layers; ++l) {
+    Layer L;
+    L.d_in = l == 0 ? c.in_dim : c.hidden;
+    L.d_out = l + 1 == c.layers ? c.classes : c.hidden;
+    L.K_in = round_up(L.d_in, 4);
+    L.D_out = round_up(L.d_out, 4);
+    if (c.kind == CATGNN_MODEL_SAGE) {
+      L.agg_first = L.d_in <= L.d_out;
+      if (L.agg_first) {
+        L.w_rows = L.d_out; L.w_cols = 2 * L.K_in;
+        L.lw_rows = L.d_out; L.lw_cols = 2 * L.d_in;
+        L.gemm_n = L.d_out;
+      } else {
+        L.w_rows = L.D_out + L.d_out; L.w_cols = L.K_in;
+        L.lw_rows = 2 * L.d_out; L.lw_cols = L.d_in;
+        L.gemm_n = L.D_out + L.d_out;
+      }
+    } else {
+      L.agg_first = L.d_in < L.d_out;
+      L.w_rows = L.d_out; L.w_cols = L.K_in;
+      L.lw_rows = L.d_out; L.lw_cols = L.d_in;
+      L.gemm_n = L.d_out;
+    }
+    L.off_w = off;
+    off += (uint64_t)L.w_rows * L.w_cols;
+    L.off_b = off;
+    off += L.D_out;
+    M->layers.push_back(L);
+  }
+  M->n_params = off;
+}
+
+// logical (row, col) of layer L -> internal index
+uint64_t internal_w_index(const catgnn_model_s* M, const Layer& L, uint32_t r, uint32_t c) {
+  uint32_t ir = r, ic = c;
+  if (M->cfg.kind == CATGNN_MODEL_SAGE) {
+    if (L.agg_first) ic = c < L.d_in ? c : L.K_in + (c - L.d_in);
+    else ir = r < L.d_out ? r : L.D_out + (r - L.d_out);
+  }
+  return L.off_w + (uint64_t)ir * L.w_cols + ic;
+}
+
+uint64_t logical_count(const catgnn_model_s* M) {
+  uint64_t n = 0;
+  for (const auto& L : M->layers) n += (uint64_t)L.lw_rows * L.lw_cols + L.d_out;
+  return n;
+}
+
+// logical flat <-> internal flat (host)
+void logical_to_internal(const catgnn_model_s* M, const float* in, std::vector<float>& out) {
+  out.assign(M->n_params, 0.f);
+  uint64_t k = 0;
+  for (const auto& L : M->layers) {
+    for (uint32_t r = 0; r < L.lw_rows; ++r)
+      for (uint32_t c = 0; c < L.lw_cols; ++c) out[internal_w_index(M, L, r, c)] = in[k++];
+    for (uint32_t j = 0; j < L.d_out; ++j) out[L.off_b + j] = in[k++];
+  }
+}
+void internal_to_logical(const catgnn_model_s* M, const std::vector<float>& in, float* out) {
+  uint64_t k = 0;
+  for (const auto& L : M->layers) {
+    for (uint32_t r = 0; r < L.lw_rows; ++r)
+      for (uint32_t c = 0; c < L.lw_cols; ++c) out[k++] = in[internal_w_index(M, L, r, c)];
+    for (uint32_t j = 0; j < L.d_out; ++j) out[k++] = in[L.off_b + j];
+  }
+}
+
+void refresh_wT(catgnn_model_s* M) {
+  if (M->wT_valid) return;
+  for (size_t l = 0; l < M->layers.size(); ++l) {
+    const Layer& L = M->layers[l];
+    transpose(M->ctx, M->params.p + L.off_w, L.w_cols, L.w_rows, L.w_cols, M->wT[l].p, round_up(L.w_rows, 4));
+  }
+  M->wT_valid = true;
+}
+
+void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t width, float* out) {
+  const uint32_t blocks = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (rows + 1023) / 1024), 592);
+  float* part = ctx->scratch_buf<float>("colsum_part", (size_t)blocks * width);
+  colsum_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part);
+  CG_CHECK_LAUNCH();
+  colsum_reduce_kernel<<<(width + 255) / 256, 256, 0, ctx->stream>>>(part, blocks, width, out);
+  CG_CHECK_LAUNCH();
+  ctx->launches += 2;
+}
+
+int agg_norm(const catgnn_model_s* M) {
+  return M->cfg.kind == CATGNN_MODEL_GCN ? kNormGcn : kNormNone;
+}
+
+struct Bufs {
+  const float* in;  // H_{l-1}
+  uint32_t in_ld;
+  float* mid;       // T / A / cat / P
+  uint32_t mid_ld;
+  float* out;       // H_l
+  uint32_t out_ld;
+};
+
+std::string nm(const char* base, size_t l) { return std::string(base) + std::to_string(l); }
+
+// Forward over the shard; returns the logits buffer (rows x D_out of the last layer).
+std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
+  catgnn_ctx ctx = M->ctx;
+  const uint64_t rows = S->rows;
+  const bool gcn = M->cfg.kind == CATGNN_MODEL_GCN;
+  const bool sage = M->cfg.kind == CATGNN_MODEL_SAGE;
+  std::vector<Bufs> B(M->layers.size());
+  const float* in = S->x.p;
+  uint32_t in_ld = S->ld;
+  const bool fresh = M->last_rows != rows;
+  for (size_t l = 0; l < M->layers.size(); ++l) {
+    const Layer& L = M->layers[l];
+    const bool last = l + 1 == M->layers.size();
+    Bufs& b = B[l];
+    b.in = in;
+    b.in_ld = in_ld;
+    b.out_ld = L.D_out;
+    b.out = act(ctx, nm("H", l), rows, b.out_ld, fresh);
+    const float* bias = M->params.p + L.off_b;
+    if (sage && L.agg_first) {
+      b.mid_ld = 2 * L.K_in;
+      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
+      copy_rows(ctx, in, in_ld, b.mid, b.mid_ld, rows, L.K_in);
+      AggArgs a;
+      a.in = in; a.in_ld = in_ld; a.out = b.mid; a.out_ld = b.mid_ld; a.out_col = L.K_in;
+      a.width = L.K_in; a.norm = kNormMean;
+      aggregate(S, a);
+      GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
+      gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.w_cols, e, 1);
+    } else if (sage) {
+      b.mid_ld = round_up(L.gemm_n, 4);
+      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
+      GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld;
+      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.gemm_n, L.K_in, e, 1);
+      AggArgs a;
+      a.in = b.mid; a.in_ld = b.mid_ld; a.in_col = L.D_out;
+      a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out; a.norm = kNormMean;
+      a.residual = b.mid; a.res_ld = b.mid_ld; a.res_col = 0;
+      a.bias = bias; a.relu = !last;
+      aggregate(S, a);
+    } else if (L.agg_first) {  // GCN / GIN aggregate-first
+      b.mid_ld = L.K_in;
+      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
+      AggArgs a;
+      a.in = in; a.in_ld = in_ld; a.out = b.mid; a.out_ld = b.mid_ld; a.width = L.K_in;
+      a.self = 1; a.norm = agg_norm(M); a.pre = gcn ? S->dinv.p : nullptr;
+      aggregate(S, a);
+      GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
+      gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1);
+    } else {  // GCN / GIN transform-first
+      b.mid_ld = L.D_out;
+      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
+      GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld; e.rowscale = gcn ? S->dinv.p : nullptr;
+      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1);
+      AggArgs a;
+      a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
+      a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
+      aggregate(S, a);
+    }
+    in = b.out;
+    in_ld = b.out_ld;
+  }
+  M->last_rows = rows;
+  return B;
+}
+
+// Loss + backward; fills M->grads.  Returns the loss when want_loss.
+double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B, bool want_loss) {
+  catgnn_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  const uint64_t rows = S->rows;
+  const uint32_t R4 = round_up((uint32_t)std::max<uint64_t>(rows, 1), 4);
+  const bool gcn = M->cfg.kind == CATGNN_MODEL_GCN;
+  const bool sage = M->cfg.kind == CATGNN_MODEL_SAGE;
+  const size_t nl = M->layers.size();
+  refresh_wT(M);
+  // K4: dZ of the last layer
+  const Layer& LL = M->layers[nl - 1];
+  float* dZ = act(ctx, nm("dZ", nl - 1), rows, LL.D_out, false);
+  CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.D_out * 4, st));
+  const uint64_t ntr = S->h_train.size();
+  double loss = 0.0;
+  double* row_loss = ctx->scratch_buf<double>("row_loss", std::max<uint64_t>(1, ntr));
+  double* loss_dev = ctx->scratch_buf<double>("loss_dev", 1);
+  if (ntr) {
+    softmax_ce_kernel<<<grid1d(ntr * 32), 256, 0, st>>>(B[nl - 1].out, B[nl - 1].out_ld, LL.d_out,
+                                                      S->labels.p, S->d_train.p, ntr, dZ, LL.D_out, row_loss);
+    CG_CHECK_LAUNCH();
+    sum_doubles_kernel<<<1, 256, 0, st>>>(row_loss, ntr, loss_dev);
+    CG_CHECK_LAUNCH();
+    ctx->launches += 2;
+  }
+  uint32_t dZ_ld = LL.D_out;
+  for (size_t li = nl; li-- > 0;) {
+    const Layer& L = M->layers[li];
+    const Bufs& b = B[li];
+    float* gW = M->grads.p + L.off_w;
+    colsum(ctx, dZ, dZ_ld, rows, L.d_out, M->grads.p + L.off_b);
+    const bool need_dx = li > 0;
+    const float* hprev = b.in;  // ReLU mask source for the previous layer
+    float* dZprev = need_dx ? act(ctx, nm("dZ", li - 1), rows, L.K_in, false) : nullptr;
+    if (sage && L.agg_first) {
+      // dW = dZ^T cat
+      float* dZt = act(ctx, "dZt", L.d_out, R4, false);
+      float* catT = act(ctx, "midT", b.mid_ld, R4, false);
+      transpose(ctx, dZ, dZ_ld, rows, L.d_out, dZt, R4);
+      transpose(ctx, b.mid, b.mid_ld, rows, b.mid_ld, catT, R4);
+      GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
+      gemm_tn(ctx, dZt, R4, catT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      if (need_dx) {
+        float* dcat = act(ctx, "dmid", rows, b.mid_ld, false);
+        GemmEpi e2; e2.out = dcat; e2.ld_out = b.mid_ld;
+        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
+        AggArgs a;
+        a.in = dcat; a.in_ld = b.mid_ld; a.in_col = L.K_in; a.pre = S->inv_deg.p;
+        a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in; a.norm = kNormNone;
+        a.residual = dcat; a.res_ld = b.mid_ld; a.res_col = 0;
+        a.mask = hprev; a.mask_ld = b.in_ld;
+        aggregate(S, a);
+      }
+    } else if (sage) {
+      // dP = [dZ | sum_{i in N(j)} dZ_i / deg_i]
+      float* dP = act(ctx, "dmid", rows, b.mid_ld, false);
+      copy_rows(ctx, dZ, dZ_ld, dP, b.mid_ld, rows, L.D_out);
+      AggArgs a;
+      a.in = dZ; a.in_ld = dZ_ld; a.pre = S->inv_deg.p;
+      a.out = dP; a.out_ld = b.mid_ld; a.out_col = L.D_out; a.width = L.D_out; a.norm = kNormNone;
+      aggregate(S, a);
+      float* dPt = act(ctx, "dZt", L.gemm_n, R4, false);
+      transpose(ctx, dP, b.mid_ld, rows, L.gemm_n, dPt, R4);
+      const float* hT = nullptr;
+      if (li == 0) {
+        if (!S->xT_valid || S->xT_ld != R4) {
+          S->xT.reserve((size_t)S->ld * R4);
+          transpose(ctx, S->x.p, S->ld, rows, S->ld, S->xT.p, R4);
+          S->xT_ld = R4;
+          S->xT_valid = true;
+        }
+        hT = S->xT.p;
+      } else {
+        float* t = act(ctx, "midT", b.in_ld, R4, false);
+        transpose(ctx, b.in, b.in_ld, rows, b.in_ld, t, R4);
+        hT = t;
+      }
+      GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
+      gemm_tn(ctx, dPt, R4, hT, R4, L.gemm_n, L.w_cols, (uint32_t)rows, e, 0);
+      if (need_dx) {
+        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
+        gemm_tn(ctx, dP, b.mid_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1);
+      }
+    } else if (L.agg_first) {  // GCN / GIN
+      float* dZt = act(ctx, "dZt", L.d_out, R4, false);
+      float* aT = act(ctx, "midT", b.mid_ld, R4, false);
+      transpose(ctx, dZ, dZ_ld, rows, L.d_out, dZt, R4);
+      transpose(ctx, b.mid, b.mid_ld, rows, b.mid_ld, aT, R4);
+      GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
+      gemm_tn(ctx, dZt, R4, aT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      if (need_dx) {
+        float* dA = act(ctx, "dmid", rows, L.K_in, false);
+        GemmEpi e2; e2.out = dA; e2.ld_out = L.K_in;
+        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
+        AggArgs a;
+        a.in = dA; a.in_ld = L.K_in; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
+        a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in;
+        a.mask = hprev; a.mask_ld = b.in_ld;
+        aggregate(S, a);
+      }
+    } else {  // GCN / GIN transform-first
+      float* dT = act(ctx, "dmid", rows, L.D_out, false);
+      AggArgs a;
+      a.in = dZ; a.in_ld = dZ_ld; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
+      a.out = dT; a.out_ld = L.D_out; a.width = L.D_out;
+      aggregate(S, a);
+      float* dTt = act(ctx, "dZt", L.d_out, R4, false);
+      transpose(ctx, dT, L.D_out, rows, L.d_out, dTt, R4);
+      const float* hT = nullptr;
+      if (li == 0) {
+        if (!S->xT_valid || S->xT_ld != R4) {
+          S->xT.reserve((size_t)S->ld * R4);
+          transpose(ctx, S->x.p, S->ld, rows, S->ld, S->xT.p, R4);
+          S->xT_ld = R4;
+          S->xT_valid = true;
+        }
+        hT = S->xT.p;
+      } else {
+        float* t = act(ctx, "midT", b.in_ld, R4, false);
+        transpose(ctx, b.in, b.in_ld, rows, b.in_ld, t, R4);
+        hT = t;
+      }
+      GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
+      gemm_tn(ctx, dTt, R4, hT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      if (need_dx) {
+        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
+        gemm_tn(ctx, dT, L.D_out, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
+      }
+    }
+    dZ = dZprev;
+    dZ_ld = L.K_in;
+  }
+  if (want_loss && ntr) {
+    CG_CUDA(cudaMemcpyAsync(&loss, loss_dev, 8, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    loss /= (double)ntr;
+  }
+  return loss;
+}
+
+void optimizer_step(catgnn_model_s* M) {
+  catgnn_ctx ctx = M->ctx;
+  M->step++;
+  const auto& c = M->cfg;
+  if (c.optimizer == CATGNN_OPT_ADAM) {
+    const float bc1 = (float)(1.0 - std::pow(c.beta1, (double)M->step));
+    const float bc2 = (float)(1.0 - std::pow(c.beta2, (double)M->step));
+    adam_kernel<<<grid1d(M->n_params), 256, 0, ctx->stream>>>(M->params.p, M->grads.p, M->m.p, M->v.p,
+                                                             M->n_params, (float)c.lr, (float)c.beta1,
+                                                             (float)c.beta2, (float)c.eps, bc1, bc2);
+  } else {
+    sgd_kernel<<<grid1d(M->n_params), 256, 0, ctx->stream>>>(M->params.p, M->grads.p, M->n_params, (float)c.lr);
+  }
+  CG_CHECK_LAUNCH();
+  ctx->launches++;
+  M->wT_valid = false;
+}
+
+void check_pair(catgnn_model m, catgnn_shard s) {
+  check_model(m);
+  if (!s) throw ConfigError("null shard");
+  if (s->ctx != m->ctx) throw ConfigError("model and shard must share one context");
+  if (s->dim != m->cfg.in_dim) throw DataError("shard feature width differs from the model input width");
+}
+
+}  // namespace
+}  // namespace catgnn
+
+struct catgnn_comm_s {
+  ncclComm_t comm = nullptr;
+  catgnn_ctx ctx = nullptr;
+};
+
+extern "C" {
+
+int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_model* out) {
+  return guarded([&] {
+    if (!ctx || !cfg || !out) throw ConfigError("null argument");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    if (cfg->kind != CATGNN_MODEL_GCN && cfg->kind != CATGNN_MODEL_SAGE && cfg->kind != CATGNN_MODEL_GIN)
+      throw ConfigError("unknown model kind");
+    if (cfg->layers < 1 || cfg->in_dim < 1 || cfg->classes < 1 || (cfg->layers > 1 && cfg->hidden < 1))
+      throw ConfigError("model needs >= 1 layer and positive widths");
+    if (cfg->optimizer != CATGNN_OPT_SGD && cfg->optimizer != CATGNN_OPT_ADAM)
+      throw ConfigError("unknown optimizer");
+    auto M = std::make_unique<catgnn_model_s>();
+    M->ctx = ctx;
+    M->cfg = *cfg;
+    plan_layers(M.get());
+    M->params.alloc(M->n_params);
+    M->grads.alloc(M->n_params);
+    M->m.alloc(M->n_params);
+    M->v.alloc(M->n_params);
+    CG_CUDA(cudaMemsetAsync(M->grads.p, 0, M->n_params * 4, ctx->stream));
+    CG_CUDA(cudaMemsetAsync(M->m.p, 0, M->n_params * 4, ctx->stream));
+    CG_CUDA(cudaMemsetAsync(M->v.p, 0, M->n_params * 4, ctx->stream));
+    for (const auto& L : M->layers) {
+      DevBuf<float> t;
+      t.alloc((size_t)L.w_cols * round_up(L.w_rows, 4));
+      CG_CUDA(cudaMemsetAsync(t.p, 0, t.bytes(), ctx->stream));
+      M->wT.push_back(std::move(t));
+    }
+    // Glorot-uniform init: W[i] = (2u-1)*sqrt(6/(d_in+d_out)), u from
+    // splitmix64(seed_for(seed, layer) + i) over the logical row-major index;
+    // biases zero.  (The reference's SGC model is zero-initialised,
+    // train.cpp:67-72; multi-layer nets need a seeded init shared with the oracle.)
+    std::vector<float> logical(logical_count(M.get()), 0.f);
+    uint64_t k = 0;
+    for (size_t l = 0; l < M->layers.size(); ++l) {
+      const Layer& L = M->layers[l];
+      const double a = std::sqrt(6.0 / (double)(L.d_in + L.d_out));
+      const uint64_t base = seed_for(cfg->seed, l);
+      const uint64_t nw = (uint64_t)L.lw_rows * L.lw_cols;
+      for (uint64_t i = 0; i < nw; ++i)
+        logical[k++] = (float)((2.0 * unit_uniform(mix64(base + i)) - 1.0) * a);
+      k += L.d_out;
+    }
+    std::vector<float> internal;
+    logical_to_internal(M.get(), logical.data(), internal);
+    CG_CUDA(cudaMemcpyAsync(M->params.p, internal.data(), M->n_params * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = M.release();
+  });
+}
+
+int catgnn_model_destroy(catgnn_model m) {
+  return guarded([&] {
+    if (!m) return;
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream);
+    delete m;
+  });
+}
+
+uint64_t catgnn_model_num_params(catgnn_model m) { return m ? logical_count(m) : 0; }
+
+int catgnn_model_layer_shape(catgnn_model m, uint32_t layer, uint32_t* w_rows, uint32_t* w_cols,
+                             uint64_t* offset_w, uint64_t* offset_b) {
+  return guarded([&] {
+    check_model(m);
+    if (layer >= m->layers.size()) throw ConfigError("layer index out of range");
+    uint64_t off = 0;
+    for (uint32_t l = 0; l < layer; ++l)
+      off += (uint64_t)m->layers[l].lw_rows * m->layers[l].lw_cols + m->layers[l].d_out;
+    const Layer& L = m->layers[layer];
+    if (w_rows) *w_rows = L.lw_rows;
+    if (w_cols) *w_cols = L.lw_cols;
+    if (offset_w) *offset_w = off;
+    if (offset_b) *offset_b = off + (uint64_t)L.lw_rows * L.lw_cols;
+  });
+}
+
+static void export_flat(catgnn_model m, const float* dev, float* out) {
+  std::vector<float> h(m->n_params);
+  CG_CUDA(cudaMemcpyAsync(h.data(), dev, m->n_params * 4, cudaMemcpyDeviceToHost, m->ctx->stream));
+  CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  internal_to_logical(m, h, out);
+}
+
+int catgnn_model_get_params(catgnn_model m, float* out) {
+  return guarded([&] {
+    check_model(m);
+    export_flat(m, m->params.p, out);
+  });
+}
+
+int catgnn_model_get_grads(catgnn_model m, float* out) {
+  return guarded([&] {
+    check_model(m);
+    export_flat(m, m->grads.p, out);
+  });
+}
+
+int catgnn_model_set_params(catgnn_model m, const float* in) {
+  return guarded([&] {
+    check_model(m);
+    std::vector<float> internal;
+    logical_to_internal(m, in, internal);
+    CG_CUDA(cudaMemcpyAsync(m->params.p, internal.data(), m->n_params * 4, cudaMemcpyHostToDevice, m->ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    m->wT_valid = false;
+  });
+}
+
+int catgnn_model_copy_params(catgnn_model dst, catgnn_model src) {
+  return guarded([&] {
+    check_model(dst);
+    check_model(src);
+    if (dst->n_params != src->n_params) throw DataError("model shapes differ across replicas");
+    CG_CUDA(cudaMemcpyAsync(dst->params.p, src->params.p, dst->n_params * 4, cudaMemcpyDeviceToDevice,
+                            dst->ctx->stream));
+    dst->wT_valid = false;
+  });
+}
+
+int catgnn_model_forward_backward(catgnn_model m, catgnn_shard s, double* loss) {
+  return guarded([&] {
+    check_pair(m, s);
+    auto B = forward(m, s);
+    double l = backward(m, s, B, loss != nullptr);
+    if (loss) *loss = l;
+    m->last_shard = s;
+  });
+}
+
+int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss) {
+  return guarded([&] {
+    check_pair(m, s);
+    auto B = forward(m, s);
+    double l = backward(m, s, B, loss != nullptr);
+    optimizer_step(m);
+    if (loss) *loss = l;
+    m->last_shard = s;
+  });
+}
+
+int catgnn_model_forward(catgnn_model m, catgnn_shard s, float* logits, int role, double* f1) {
+  return guarded([&] {
+    check_pair(m, s);
+    auto B = forward(m, s);
+    m->last_shard = s;
+    catgnn_ctx ctx = m->ctx;
+    const Layer& LL = m->layers.back();
+    if (logits && s->rows)
+      CG_CUDA(cudaMemcpy2DAsync(logits, LL.d_out * 4, B.back().out, B.back().out_ld * 4, LL.d_out * 4, s->rows,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    if (f1) {
+      const uint32_t* rows = role == 1 ? s->d_train.p : role == 2 ? s->d_val.p : s->d_test.p;
+      const uint64_t n = role == 1 ? s->h_train.size() : role == 2 ? s->h_val.size() : s->h_test.size();
+      if (role < 1 || role > 3) throw ConfigError("role must be 1, 2 or 3");
+      if (n == 0) throw DataError("evaluation mask is empty");
+      auto* cnt = ctx->scratch_buf<unsigned long long>("eval_cnt", 1);
+      CG_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
+      argmax_correct_kernel<<<grid1d(n * 32), 256, 0, ctx->stream>>>(B.back().out, B.back().out_ld, LL.d_out,
+                                                                     s->labels.p, rows, n, cnt);
+      CG_CHECK_LAUNCH();
+      ctx->launches++;
+      unsigned long long h = 0;
+      CG_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      CG_CUDA(cudaStreamSynchronize(ctx->stream));
+      // micro-F1 from pooled counts (train.cpp:189-197) == accuracy
+      const double tp = (double)h, miss = (double)(n - h);
+      *f1 = (2 * tp + 2 * miss) == 0 ? 0.0 : 2 * tp / (2 * tp + 2 * miss);
+    }
+    CG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, uint32_t* width) {
+  return guarded([&] {
+    check_model(m);
+    if (layer >= m->layers.size()) throw ConfigError("layer index out of range");
+    catgnn_shard s = m->last_shard;
+    if (!s) throw ConfigError("no forward pass has run");
+    const Layer& L = m->layers[layer];
+    const float* src = nullptr;
+    uint32_t ld = 0, w = L.d_out;
+    if (what == 0) { src = m->ctx->scratch_buf<float>(nm("H", layer), 1); ld = L.D_out; }
+    else if (what == 2) { src = m->ctx->scratch_buf<float>(nm("dZ", layer), 1); ld = L.D_out; }
+    else throw ConfigError("export: what must be 0 (H) or 2 (dZ)");
+    if (width) *width = w;
+    if (out && s->rows)
+      CG_CUDA(cudaMemcpy2DAsync(out, w * 4, src, ld * 4, w * 4, s->rows, cudaMemcpyDeviceToHost, m->ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  });
+}
+
+int catgnn_model_average(uint32_t n, const catgnn_model* src, const uint64_t* train_counts, catgnn_model dst) {
+  return guarded([&] {
+    check_model(dst);
+    if (n == 0) throw DataError("model averaging needs one training count per replica");
+    std::vector<double> alpha(n);
+    {
+      uint64_t total = 0;
+      for (uint32_t i = 0; i < n; ++i) total += train_counts[i];
+      if (total == 0) throw DataError("model averaging requires a nonzero training-node count");
+      double partial = 0;
+      for (uint32_t i = 0; i + 1 < n; ++i) {
+        alpha[i] = (double)train_counts[i] / (double)total;
+        partial += alpha[i];
+      }
+      alpha[n - 1] = 1.0 - partial;
+    }
+    std::vector<const float*> ptrs(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      check_model(src[i]);
+      if (src[i]->n_params != dst->n_params || src[i]->ctx != dst->ctx)
+        throw DataError("model shapes differ across replicas");
+      ptrs[i] = src[i]->params.p;
+    }
+    float* tmp = dst->ctx->scratch_buf<float>("avg_tmp", dst->n_params);
+    average_params(dst->ctx, ptrs, alpha, dst->n_params, tmp);
+    CG_CUDA(cudaMemcpyAsync(dst->params.p, tmp, dst->n_params * 4, cudaMemcpyDeviceToDevice, dst->ctx->stream));
+    dst->wT_valid = false;
+  });
+}
+
+int catgnn_model_scale(catgnn_model m, double alpha) {
+  return guarded([&] {
+    check_model(m);
+    scale_kernel<<<grid1d(m->n_params), 256, 0, m->ctx->stream>>>(m->params.p, m->n_params, alpha);
+    CG_CHECK_LAUNCH();
+    m->ctx->launches++;
+    m->wT_valid = false;
+  });
+}
+
+int catgnn_comm_unique_id(char id[128]) {
+  return guarded([&] {
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) throw InternalError("ncclGetUniqueId failed");
+    static_assert(sizeof(u) == 128, "NCCL unique id size");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+int catgnn_comm_create(catgnn_ctx ctx, int nranks, int rank, const char id[128], catgnn_comm* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw ConfigError("null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw ConfigError("bad rank / world size");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    auto c = std::make_unique<catgnn_comm_s>();
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) throw InternalError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    c->ctx = ctx;
+    *out = c.release();
+  });
+}
+
+int catgnn_comm_destroy(catgnn_comm c) {
+  return guarded([&] {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+  });
+}
+
+// C1: sum over ranks of the (alpha-prescaled) parameters, in place, on the
+// context stream (NCCL over NVLink / NVSwitch).
+int catgnn_model_allreduce(catgnn_model m, catgnn_comm c) {
+  return guarded([&] {
+    check_model(m);
+    if (!c) throw ConfigError("null communicator");
+    ncclResult_t r = ncclAllReduce(m->params.p, m->params.p, m->n_params, ncclFloat32, ncclSum, c->comm,
+                                   m->ctx->stream);
+    if (r != ncclSuccess) throw InternalError(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    m->wT_valid = false;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+"""GPU parity of the north-star GNN layers (tcgen05 GEMM + aggregation +
+softmax-CE + optimizer) against the float64 restatement in oracle/gnn_oracle.py.
+
+North-star tolerances: single-step layer outputs and gradients within 2e-3
+relative (normwise; TF32 inputs, fp32 accumulation), loss over the first 10
+epochs within 1e-3 relative, final accuracy within 0.5 pt."""
+import numpy as np
+import pytest
+
+from conftest import make_artifact, make_dataset, rel_err
+from oracle import gnn_oracle as go
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # kind, in_dim, hidden, classes, layers  (covers aggregate-first and transform-first)
+    ("gcn", 602, 64, 41, 2),   # transform-first both layers, unaligned widths
+    ("gcn", 8, 32, 5, 2),      # aggregate-first layer 0
+    ("sage", 64, 256, 8, 2),   # config-1 shape: aggregate-first then transform-first
+    ("sage", 100, 32, 47, 3),  # transform-first, 3 layers, odd class count
+    ("gin", 12, 48, 6, 2),
+]
+
+
+@pytest.fixture(scope="module")
+def graph():
+    from paper_2404_02300_b200 import gnnpart as gp, synth
+    rng = np.random.default_rng(0)
+    e, n, _ = synth.rmat_edges(11, 12000, seed=4)
+    hub = np.stack([np.zeros(1500, np.uint64), np.arange(1, 1501, dtype=np.uint64) % n], 1)
+    pairs = np.concatenate([e, hub[hub[:, 1] != 0]]).astype(np.uint32)
+    off, nb = ref.build_adjacency(n, pairs)
+    return dict(n=n, pairs=pairs, off=off, nb=nb, G=go.Graph.from_csr(off, nb, n), rng=rng)
+
+
+def make(gp, graph, in_dim, classes, seed=1):
+    rng = np.random.default_rng(seed)
+    n = graph["n"]
+    X = rng.normal(size=(n, in_dim)).astype(np.float32)
+    labels = rng.integers(0, classes, n).astype(np.int32)
+    train = np.sort(rng.choice(n, size=n // 2, replace=False)).astype(np.uint32)
+    s = gp.Shard.from_edges(n, graph["pairs"], X)
+    s.set_labels(labels, train)
+    o = go.OracleShard(graph["G"], X.astype(np.float64), labels, train.astype(np.int64))
+    return s, o
+
+
+@pytest.mark.parametrize("kind,in_dim,hidden,classes,layers", CASES)
+def test_single_step_outputs_and_grads(graph, kind, in_dim, hidden, classes, layers):
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    s, o = make(gp, graph, in_dim, classes)
+    m = GNNModel(kind, layers, in_dim, hidden, classes, seed=5)
+    k = {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[kind]
+    # the seeded init is shared with the oracle
+    init = go.init_params(k, layers, in_dim, hidden, classes, seed=5)
+    p_gpu = m.get_params()
+    np.testing.assert_allclose(p_gpu, go.flatten(init).astype(np.float32), rtol=1e-7, atol=0)
+    loss = m.forward_backward(s)
+    rep = go.Replica(k, go.unflatten(p_gpu.astype(np.float64), init))
+    loss_ref, H, Zs, grads = rep.forward_backward(o)
+    assert abs(loss - loss_ref) <= 1e-3 * abs(loss_ref)
+    for l in range(layers):
+        h = m.export(l, 0, s.rows)
+        assert rel_err(h, H[l + 1]) < 2e-3, (l, rel_err(h, H[l + 1]))
+    g = m.unflatten(m.get_grads())
+    for l, ((gW, gb), (rW, rb)) in enumerate(zip(g, grads)):
+        assert rel_err(gW, rW) < 2e-3, (l, "W", rel_err(gW, rW))
+        assert rel_err(gb, rb) < 2e-3, (l, "b", rel_err(gb, rb))
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage", "gin"])
+def test_ten_epoch_loss_two_partitions(kind, tmp_path_factory):
+    """p=2 SPRING shards, s=1, Adam lr 0.01: per-epoch loss within 1e-3 of the oracle."""
+    from paper_2404_02300_b200 import gnnpart as gp, gnn
+    ds = make_dataset(tmp_path_factory.mktemp(f"ten_{kind}"), scale=11, edges=12000, dim=24, classes=6, seed=2)
+    art = make_artifact(ds, p=2)
+    data = gp.load_training_data(art)
+    td = ref.TrainingData(art)
+    counts = [int(s.info.n_train) for s in data.shards]
+    res = gnn.distributed_train(kind, data.shards, counts, 1, 10, 2, 32, 6, seed=9, global_shard=data.global_)
+    k = {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[kind]
+    osh = []
+    for i in range(2):
+        r = td.shard(i)
+        osh.append(go.OracleShard(go.Graph.from_csr(r.offsets, r.neighbors, r.labels.size), r.features,
+                                  r.labels, r.train_rows.astype(np.int64)))
+    rg = td.shard(-1)
+    og = go.OracleShard(go.Graph.from_csr(rg.offsets, rg.neighbors, rg.labels.size), rg.features, rg.labels,
+                        rg.train_rows, rg.val_rows, rg.test_rows)
+    want = go.distributed_train(k, osh, 1, 10, 2, 32, 6, seed=9, global_shard=og)
+    for a, b in zip(res.losses, want["losses"]):
+        assert abs(a - b) <= 1e-3 * abs(b), (res.losses, want["losses"])
+    assert res.averaging_ops == want["averaging_ops"]
+    for (e1, s1, v1, t1), (e2, s2, v2, t2) in zip(res.history, want["history"]):
+        assert (e1, s1) == (e2, s2)
+        assert abs(t1 - t2) <= max(0.005, 2.0 / max(len(rg.test_rows), 1))
+
+
+@pytest.mark.slow
+def test_config1_sage_accuracy(tmp_path_factory):
+    """Config 1: 2-layer GraphSAGE-mean, RMAT 2^16 (524,288 edges), 64-d, 8 classes, SPRING p=2."""
+    from paper_2404_02300_b200 import gnnpart as gp, gnn
+    ds = make_dataset(tmp_path_factory.mktemp("cfg1g"), scale=16, edges=524288, dim=64, classes=8, seed=1)
+    art = make_artifact(ds, p=2)
+    data = gp.load_training_data(art)
+    counts = [int(s.info.n_train) for s in data.shards]
+    ep = 30
+    res = gnn.distributed_train("sage", data.shards, counts, 1, ep, 2, 256, 8, seed=0, global_shard=data.global_)
+    td = ref.TrainingData(art)
+    osh = []
+    for i in range(2):
+        r = td.shard(i)
+        osh.append(go.OracleShard(go.Graph.from_csr(r.offsets, r.neighbors, r.labels.size), r.features,
+                                  r.labels, r.train_rows.astype(np.int64)))
+    rg = td.shard(-1)
+    og = go.OracleShard(go.Graph.from_csr(rg.offsets, rg.neighbors, rg.labels.size), rg.features, rg.labels,
+                        rg.train_rows, rg.val_rows, rg.test_rows)
+    want = go.distributed_train(go.SAGE, osh, 1, ep, 2, 256, 8, seed=0, global_shard=og)
+    for a, b in zip(res.losses[:10], want["losses"][:10]):
+        assert abs(a - b) <= 1e-3 * abs(b)
+    assert abs(res.history[-1][3] - want["history"][-1][3]) <= 0.005
