@@ -235,9 +235,10 @@ int catgnn_model_allreduce(catgnn_model m, catgnn_comm c);
 
 /* ------------------------------------------------------------- utilities */
 /* Tensor-core GEMM test hook: C[M x N] = A[M x K] . B[N x K]^T (all host,
- * row-major float32), computed by the tcgen05 TF32 kernel. */
+ * row-major float32), computed by the tcgen05 kernel; precision 1 = TF32,
+ * 3 = 3xTF32 (split operands, ~fp32 accuracy); split_k 0 = automatic. */
 int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
-                   const float* B, float* C, uint32_t split_k);
+                   const float* B, float* C, uint32_t split_k, int precision);
 
 #ifdef __cplusplus
 }

@@ -89,7 +89,7 @@ def _load():
         "catgnn_comm_destroy": (C.c_int, [vp]),
         "catgnn_model_scale": (C.c_int, [vp, f64]),
         "catgnn_model_allreduce": (C.c_int, [vp, vp]),
-        "catgnn_gemm_tn": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, u32]),
+        "catgnn_gemm_tn": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, u32, C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

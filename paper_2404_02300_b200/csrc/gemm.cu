@@ -39,6 +39,7 @@ struct GemmArgs {
   uint32_t kb_per_split;
   uint32_t tmem_cols;
   uint32_t idesc;
+  uint32_t split3;  // 1: 3xTF32 (hi*hi + hi*lo + lo*hi), 0: plain TF32
   GemmEpi epi;
 };
 
@@ -122,6 +123,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ float tf32_residual(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+__device__ __forceinline__ float4 tf32_residual4(float4 v) {
+  return make_float4(tf32_residual(v.x), tf32_residual(v.y), tf32_residual(v.z), tf32_residual(v.w));
+}
+
 __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
   if (e.rowscale && col >= e.scale_col_begin) v *= __ldg(e.rowscale + row);
   if (e.bias) v += __ldg(e.bias + col);
@@ -138,13 +146,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t BN = args.BN;
   const uint32_t B_STAGE = BN * BK * 4;
   const uint32_t S = args.stages;
+  const bool split3 = args.split3 != 0;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)S * A_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)S * B_STAGE);
+  // 3xTF32: residual ("lo") tiles with the same swizzled layout
+  uint8_t* sAl = sB + (size_t)S * B_STAGE;
+  uint8_t* sBl = sAl + (split3 ? (size_t)S * A_STAGE : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (split3 ? (size_t)S * B_STAGE : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* accum = bars + 2 * S;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+  uint64_t* conv = bars + 2 * S;
+  uint64_t* accum = bars + 3 * S;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -157,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t i = 0; i < S; ++i) {
       mbar_init(smem_u32(full + i), 1);
       mbar_init(smem_u32(empty + i), 1);
+      mbar_init(smem_u32(conv + i), 4);  // one arrive per converter warp
     }
     mbar_init(smem_u32(accum), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -189,14 +203,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       for (uint32_t i = 0; i < nkb; ++i) {
         const uint32_t s = i % S, ph = (i / S) & 1;
-        mbar_wait(smem_u32(full + s), ph);
+        mbar_wait(smem_u32(split3 ? conv + s : full + s), ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
         const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
+        if (split3) {
+          const uint32_t al = smem_u32(sAl + (size_t)s * A_STAGE);
+          const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
 #pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
-          mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
-                   (i > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first
+            mma_tf32(tmem, umma_desc(al + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
+                     (i > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(bl + ks * 32), args.idesc, 1u);
+            mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc, 1u);
+          }
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
+            mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
+                     (i > 0 || ks > 0) ? 1u : 0u);
+        }
         mma_commit(smem_u32(empty + s));
       }
       if (nkb) mma_commit(smem_u32(accum));
@@ -206,6 +232,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue warps 2..5: TMEM lane quarter = warp % 4
     const uint32_t q = warp & 3;
     const uint32_t row = m0 + q * 32 + lane;
+    if (split3) {
+      // lo = x - tf32_trunc(x) for every element of the A and B tiles of each
+      // stage (element-wise, so the swizzled layout carries over)
+      const uint32_t t = threadIdx.x - 64;
+      const uint32_t a4 = A_STAGE / 16, b4 = B_STAGE / 16;
+      for (uint32_t i = 0; i < nkb; ++i) {
+        const uint32_t s = i % S, ph = (i / S) & 1;
+        mbar_wait(smem_u32(full + s), ph);
+        const float4* ah = reinterpret_cast<const float4*>(sA + (size_t)s * A_STAGE);
+        float4* alo = reinterpret_cast<float4*>(sAl + (size_t)s * A_STAGE);
+        const float4* bh = reinterpret_cast<const float4*>(sB + (size_t)s * B_STAGE);
+        float4* blo = reinterpret_cast<float4*>(sBl + (size_t)s * B_STAGE);
+        for (uint32_t k = t; k < a4; k += 128) alo[k] = tf32_residual4(ah[k]);
+        for (uint32_t k = t; k < b4; k += 128) blo[k] = tf32_residual4(bh[k]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(conv + s)) : "memory");
+      }
+    }
     if (nkb) {
       mbar_wait(smem_u32(accum), 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -307,7 +352,7 @@ uint32_t pow2_cols(uint32_t n) {
 }  // namespace
 
 void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
-             uint32_t N, uint32_t K, const GemmEpi& epi_in, uint32_t split_k) {
+             uint32_t N, uint32_t K, const GemmEpi& epi_in, uint32_t split_k, int precision) {
   if (M == 0 || N == 0) return;
   GemmEpi epi = epi_in;
   if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
@@ -337,10 +382,12 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
 
   const uint32_t b_stage = BN * BK * 4;
-  const size_t budget = 227 * 1024 - 1024 - 256;
-  uint32_t stages = (uint32_t)std::min<size_t>(6, budget / (A_STAGE + b_stage));
+  const bool split3 = precision == 3;
+  const size_t stage_bytes = (size_t)(A_STAGE + b_stage) * (split3 ? 2 : 1);
+  const size_t budget = 227 * 1024 - 1024 - 512;
+  uint32_t stages = (uint32_t)std::min<size_t>(6, budget / stage_bytes);
   if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
-  const size_t smem = 1024 + (size_t)stages * (A_STAGE + b_stage) + (2 * stages + 2) * 8;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (3 * stages + 2) * 8;
 
   GemmArgs args{};
   args.M = M;
@@ -350,6 +397,7 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   args.stages = stages;
   args.kb_per_split = kbps;
   args.tmem_cols = pow2_cols(BN);
+  args.split3 = split3 ? 1u : 0u;
   // instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
   args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   float* partial = nullptr;
@@ -385,7 +433,7 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
 }  // namespace catgnn
 
 extern "C" int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
-                              const float* B, float* Cout, uint32_t split_k) {
+                              const float* B, float* Cout, uint32_t split_k, int precision) {
   using namespace catgnn;
   return guarded([&] {
     if (!ctx) throw ConfigError("null context");
@@ -404,7 +452,8 @@ extern "C" int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K
     GemmEpi e{};
     e.out = dC;
     e.ld_out = ldc;
-    gemm_tn(ctx, dA, lda, dB, lda, M, N, K, e, split_k);
+    if (precision != 1 && precision != 3) throw ConfigError("precision must be 1 (TF32) or 3 (3xTF32)");
+    gemm_tn(ctx, dA, lda, dB, lda, M, N, K, e, split_k, precision);
     CG_CUDA(cudaMemcpy2DAsync(Cout, N * 4, dC, ldc * 4, N * 4, M, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
   });

@@ -21,8 +21,9 @@ struct GemmEpi {
 
 // C[M x N] = A[M x K] . B[N x K]^T with A (row stride lda) and B (row stride
 // ldb) K-major fp32 device matrices.  split_k = 0 picks a split automatically
-// (deterministic reduction in split order).
+// (deterministic reduction in split order).  precision 1 = TF32 (inputs
+// truncated to 10 mantissa bits), 3 = 3xTF32 (hi*hi + hi*lo + lo*hi, ~fp32).
 void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
-             uint32_t N, uint32_t K, const GemmEpi& epi, uint32_t split_k = 1);
+             uint32_t N, uint32_t K, const GemmEpi& epi, uint32_t split_k = 1, int precision = 1);
 
 }  // namespace catgnn

@@ -181,6 +181,10 @@ __global__ void scale_kernel(float* __restrict__ p, uint64_t n, double a) {
     p[i] = (float)((double)p[i] * a);
 }
 
+// Backward GEMMs (weight gradients reduce over all rows with heavy
+// cancellation) run 3xTF32; forward GEMMs plain TF32 (north-star tolerance).
+constexpr int kBwdPrecision = 3;
+
 unsigned grid1d(uint64_t n) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16));
 }
@@ -438,11 +442,11 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       transpose(ctx, dZ, dZ_ld, rows, L.d_out, dZt, R4);
       transpose(ctx, b.mid, b.mid_ld, rows, b.mid_ld, catT, R4);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dZt, R4, catT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      gemm_tn(ctx, dZt, R4, catT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         float* dcat = act(ctx, "dmid", rows, b.mid_ld, false);
         GemmEpi e2; e2.out = dcat; e2.ld_out = b.mid_ld;
-        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
+        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
         AggArgs a;
         a.in = dcat; a.in_ld = b.mid_ld; a.in_col = L.K_in; a.pre = S->inv_deg.p;
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in; a.norm = kNormNone;
@@ -475,10 +479,10 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         hT = t;
       }
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dPt, R4, hT, R4, L.gemm_n, L.w_cols, (uint32_t)rows, e, 0);
+      gemm_tn(ctx, dPt, R4, hT, R4, L.gemm_n, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
-        gemm_tn(ctx, dP, b.mid_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1);
+        gemm_tn(ctx, dP, b.mid_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1, kBwdPrecision);
       }
     } else if (L.agg_first) {  // GCN / GIN
       float* dZt = act(ctx, "dZt", L.d_out, R4, false);
@@ -486,11 +490,11 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       transpose(ctx, dZ, dZ_ld, rows, L.d_out, dZt, R4);
       transpose(ctx, b.mid, b.mid_ld, rows, b.mid_ld, aT, R4);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dZt, R4, aT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      gemm_tn(ctx, dZt, R4, aT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         float* dA = act(ctx, "dmid", rows, L.K_in, false);
         GemmEpi e2; e2.out = dA; e2.ld_out = L.K_in;
-        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
+        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
         AggArgs a;
         a.in = dA; a.in_ld = L.K_in; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in;
@@ -520,10 +524,10 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         hT = t;
       }
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dTt, R4, hT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      gemm_tn(ctx, dTt, R4, hT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
-        gemm_tn(ctx, dT, L.D_out, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
+        gemm_tn(ctx, dT, L.D_out, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
       }
     }
     dZ = dZprev;

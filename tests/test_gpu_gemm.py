@@ -14,13 +14,13 @@ def ctx():
     return gp.Context(0)
 
 
-def gemm(ctx, A, B, split=1):
+def gemm(ctx, A, B, split=1, precision=1):
     from paper_2404_02300_b200._lib import check, lib
     A = np.ascontiguousarray(A, np.float32); B = np.ascontiguousarray(B, np.float32)
     M, K = A.shape; N = B.shape[0]
     out = np.zeros((M, N), np.float32)
     check(lib.catgnn_gemm_tn(ctx.handle, M, N, K, A.ctypes.data_as(C.c_void_p), B.ctypes.data_as(C.c_void_p),
-                             out.ctypes.data_as(C.c_void_p), split))
+                             out.ctypes.data_as(C.c_void_p), split, precision))
     return out
 
 
@@ -31,10 +31,25 @@ def test_gemm_tn(ctx, M, N, K, split):
     rng = np.random.default_rng(M * 7 + N + K)
     A = rng.standard_normal((M, K)).astype(np.float32)
     B = rng.standard_normal((N, K)).astype(np.float32)
-    got = gemm(ctx, A, B, split)
     want = A.astype(np.float64) @ B.astype(np.float64).T
+    got = gemm(ctx, A, B, split)
     err = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert err < 1e-3, err
+    got3 = gemm(ctx, A, B, split, precision=3)
+    err3 = np.linalg.norm(got3 - want) / np.linalg.norm(want)
+    assert err3 < 5e-6, err3
+
+
+def test_gemm_cancellation_needs_3xtf32(ctx):
+    # weight-gradient shape: long K with heavy cancellation (result << terms)
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((64, 20000)).astype(np.float32)
+    B = rng.standard_normal((96, 20000)).astype(np.float32)
+    B[:, 10000:] = -B[:, :10000] * np.float32(0.999)
+    A[:, 10000:] = A[:, :10000]
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    err3 = np.linalg.norm(gemm(ctx, A, B, 0, 3) - want) / np.linalg.norm(want)
+    assert err3 < 1e-4, err3
 
 
 def test_gemm_k_zero(ctx):
