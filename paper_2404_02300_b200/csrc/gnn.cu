@@ -24,6 +24,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -183,7 +184,12 @@ __global__ void scale_kernel(float* __restrict__ p, uint64_t n, double a) {
 
 // Backward GEMMs (weight gradients reduce over all rows with heavy
 // cancellation) run 3xTF32; forward GEMMs plain TF32 (north-star tolerance).
-constexpr int kBwdPrecision = 3;
+int env_precision(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && (v[0] == '1' || v[0] == '3')) ? v[0] - '0' : dflt;
+}
+const int kBwdPrecision = env_precision("CATGNN_BWD_PRECISION", 3);
+const int kFwdPrecision = env_precision("CATGNN_FWD_PRECISION", 1);
 
 unsigned grid1d(uint64_t n) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16));
@@ -362,12 +368,12 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       a.width = L.K_in; a.norm = kNormMean;
       aggregate(S, a);
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
-      gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.w_cols, e, 1);
+      gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.w_cols, e, 1, kFwdPrecision);
     } else if (sage) {
       b.mid_ld = round_up(L.gemm_n, 4);
       b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
       GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld;
-      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.gemm_n, L.K_in, e, 1);
+      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.gemm_n, L.K_in, e, 1, kFwdPrecision);
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.in_col = L.D_out;
       a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out; a.norm = kNormMean;
@@ -382,12 +388,12 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       a.self = 1; a.norm = agg_norm(M); a.pre = gcn ? S->dinv.p : nullptr;
       aggregate(S, a);
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
-      gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1);
+      gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN transform-first
       b.mid_ld = L.D_out;
       b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
       GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld; e.rowscale = gcn ? S->dinv.p : nullptr;
-      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1);
+      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
       a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
