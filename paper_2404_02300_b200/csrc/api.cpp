@@ -120,6 +120,7 @@ void set_labels(catgnn_shard_s* s, const int32_t* labels, const uint32_t* tr, ui
 std::unique_ptr<catgnn_shard_s> new_shard(catgnn_ctx ctx, uint64_t rows) {
   auto s = std::make_unique<catgnn_shard_s>();
   s->ctx = ctx;
+  ctx_retain(ctx);
   s->rows = rows;
   return s;
 }
@@ -245,7 +246,7 @@ int catgnn_ctx_destroy(catgnn_ctx ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    delete ctx;
+    ctx_release(ctx);
   });
 }
 
@@ -469,9 +470,11 @@ int catgnn_shard_create_from_part(catgnn_ctx ctx, uint64_t rows, const uint64_t*
 int catgnn_shard_destroy(catgnn_shard s) {
   return guarded([&] {
     if (!s) return;
-    cudaSetDevice(s->ctx->device);
-    cudaStreamSynchronize(s->ctx->stream);
+    catgnn_ctx c = s->ctx;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
     delete s;
+    ctx_release(c);
   });
 }
 

@@ -96,6 +96,7 @@ inline uint64_t round_up64(uint64_t x, uint64_t m) { return (x + m - 1) / m * m;
 // optional per-kernel event timing for the roofline measurement.
 struct catgnn_ctx_s {
   int device = 0;
+  int refs = 1;  // the owner handle + every shard / model / comm created on it
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int num_sms = 148;
@@ -128,3 +129,11 @@ struct catgnn_ctx_s {
   void drain_timing();
   ~catgnn_ctx_s();
 };
+
+namespace catgnn {
+inline void ctx_retain(catgnn_ctx c) { c->refs++; }
+// Drops one reference; the context is freed with its last user.
+inline void ctx_release(catgnn_ctx c) {
+  if (c && --c->refs == 0) delete c;
+}
+}  // namespace catgnn

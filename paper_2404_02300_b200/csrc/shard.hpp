@@ -21,7 +21,7 @@
 #include "common.hpp"
 
 struct catgnn_shard_s {
-  catgnn_ctx ctx = nullptr;
+  catgnn_ctx ctx = nullptr;  // retained (ctx_retain) for the shard's lifetime
   uint64_t rows = 0;
   uint64_t nnz = 0;
   uint64_t num_edges = 0;
