@@ -1,0 +1,411 @@
+"""Benchmark of the per-partition GNN training step (BASELINE.json north star).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload reddit_gcn] [--sync S]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+
+Workload (default, BASELINE.json configs[1]): 2-layer GCN (hidden 256) on the
+reddit-shaped synthetic RMAT graph (scale 18, 57,307,946 undirected edges =
+114.6M nnz, 602-d class-mean features, 41 classes) partitioned by the
+reference's SPRING into p = 8 partitions with 1-hop completion.  Partitions
+are assigned to ranks cyclically (8/N per GPU, strong scaling); one step = one
+local iteration (full-batch forward + backward + Adam) over every partition of
+the rank, followed by alpha-weighted model averaging (every --sync steps):
+in-process across the rank's replicas and an NCCL all-reduce across ranks.
+
+Metric: edges aggregated per second = sum over partitions and aggregation
+passes of local nnz, per second of step time (max over ranks, CUDA events on
+the library's stream).  Inputs stay resident in HBM for `value`; `e2e`
+re-uploads every partition's features from pinned host memory through the
+C ABI each step and reads the loss back.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edges aggregated/sec per epoch (local nnz x aggregation passes / step time)"
+UNIT = "edges/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, device=0, period=0.1):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.device = period, device
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            names = {getattr(nv, k): k.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", "")
+                     for k in dir(nv) if k.startswith(("nvmlClocksEventReason", "nvmlClocksThrottleReason"))
+                     and isinstance(getattr(nv, k), int)}
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for bit, nm in names.items():
+                            if bit and (r & bit) == bit and nm not in ("None", "All", "GpuIdle", "ApplicationsClocksSetting"):
+                                self.reasons.add(nm)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            log("[clocks] unavailable:", e)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def agg_bytes(nnz, rows, width, self_term):
+    """nnz*(4 + 4d) + N*(4d*(1+self) + 8)."""
+    return nnz * (4 + 4 * width) + rows * (4 * width * (1 + self_term) + 8)
+
+
+def load_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "r01_k2_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def reference_jobs(prep, parts_idx, budget_edges):
+    """Bounded samples for the reference CPU path: partition CSR from the
+    reference's own build_adjacency; the first R rows keep their neighbour
+    lists (~budget_edges local edges), later rows have none."""
+    from oracle import ref
+    jobs = []
+    for i in parts_idx:
+        d = prep["dir"]
+        edges = np.load(os.path.join(d, f"p{i}_edges.npy"))
+        ext = np.load(os.path.join(d, f"p{i}_ext.npy"))
+        local = np.searchsorted(ext, edges.ravel()).astype(np.uint32).reshape(-1, 2)
+        rows = ext.size
+        off, nb = ref.build_adjacency(rows, local)
+        R = max(1, min(int(np.searchsorted(off, budget_edges)), rows))
+        off_s = off.copy()
+        off_s[R + 1:] = off[R]
+        jobs.append((rows, off_s, nb[: off[R]].copy(), int(off[R])))
+    return jobs
+
+
+def cpu_reference_rate(w, jobs, seed=0):
+    """The reference's aggregation (proj/src/train.cpp:49-65 sgc_propagate, compiled
+    unmodified via oracle/_ref) over the bounded samples, one pass per width of
+    this workload's epoch schedule; one host thread per partition sample (the
+    reference is single-threaded and its workers are schedule-independent)."""
+    from oracle import ref
+    widths = [(x + 3) // 4 * 4 for x in w.passes()]
+    results = [None] * len(jobs)
+
+    def run(j):
+        rows, off_s, nb_s, edges_s = jobs[j]
+        rng = np.random.default_rng(seed + j)
+        t = 0.0
+        for wd in widths:
+            x = rng.standard_normal(rows * wd)  # column-major f64 (Eigen MatrixXd)
+            t0 = time.perf_counter()
+            ref.sgc_propagate_colmajor(off_s, nb_s, x, rows, wd, 1)
+            t += time.perf_counter() - t0
+        results[j] = (edges_s * len(widths), t)
+
+    ths = [threading.Thread(target=run, args=(j,)) for j in range(len(jobs))]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    edges = sum(r[0] for r in results)
+    wall = max(r[1] for r in results)
+    sample = (f"reference sgc_propagate (1 hop) over the first ~{jobs[0][3]} local edges of "
+              f"{len(jobs)} partition(s), one pass per epoch width {widths}, f64 column-major, "
+              f"{len(jobs)} host thread(s)")
+    return edges / wall, len(jobs), sample
+
+
+def run_reference(args, w, prep):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = min(os.cpu_count() or 1, w.partitions)
+    jobs = reference_jobs(prep, list(range(threads)), args.ref_edges)
+    vals = []
+    for s in range(args.warmup + args.steps):
+        v, cores, sample = cpu_reference_rate(w, jobs, seed=s)
+        if s >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(w, prep, args), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, prep, args):
+    m = prep["meta"]
+    return {"workload": w.name, "model": f"{w.layers}-layer {w.model.upper()} hidden {w.hidden}",
+            "graph": f"RMAT scale {w.scale}, {w.edges} undirected edges ({m['nnz']} nnz), |V|={m['num_nodes']}",
+            "feature_dim": w.dim, "classes": w.classes, "partitions": w.partitions,
+            "partitioner": f"reference SPRING beta={w.beta} tau_vol={m['tau_vol']} + 1-hop completion",
+            "replication_factor": m["rf"], "part_nnz": m["part_nnz"], "sum_over_max_edges": m["sum_over_max"],
+            "aggregation_widths": [(x + 3) // 4 * 4 for x in w.passes()], "sync_interval": args.sync,
+            "optimizer": "adam lr 0.01", "gemm_precision": "3xTF32 (tcgen05 kind::tf32)",
+            "global_batch": "full-batch per partition", "parallelism": f"partition-parallel p={w.partitions}",
+            "l2": "inputs larger than L2 (per-partition features 0.5 GB, activations > 126 MB)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=os.environ.get("CATGNN_WORKLOAD", "reddit_gcn"))
+    ap.add_argument("--sync", type=int, default=1)
+    ap.add_argument("--ref-edges", type=int, default=300_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from paper_2404_02300_b200 import workloads as W
+    w = W.WORKLOADS[args.workload]
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank == 0:
+            prep = W.prepare(w, log)
+            run_reference(args, w, prep)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if w.partitions % world:
+        raise SystemExit(f"partition count {w.partitions} must be a multiple of the GPU count {world}")
+    # data preparation (untimed; rank 0 builds the cache, the others wait)
+    if rank == 0:
+        prep = W.prepare(w, log)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        prep = W.prepare(w, log)
+    meta = prep["meta"]
+
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import ADAM, Comm, GNNModel, model_average, sync_weights
+    stream = torch.cuda.Stream()
+    ctx = gp.Context(local, stream.cuda_stream)
+    mine = list(range(rank, w.partitions, world))
+    X = np.load(os.path.join(prep["dir"], "features.npy"), mmap_mode="r")
+    labels = np.load(os.path.join(prep["dir"], "labels.npy"))
+    shards, host_feats = [], []
+    t0 = time.time()
+    for i in mine:
+        p = W.load_part(prep, i, X, labels)
+        s = gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx)
+        shards.append(s)
+        pinned = torch.empty(p["features"].shape, dtype=torch.float32, pin_memory=True)
+        pinned.numpy()[:] = p["features"]
+        host_feats.append(pinned)
+    log(f"[rank {rank}] {len(shards)} shards resident in {time.time() - t0:.1f}s")
+    counts_all = meta["part_train"]
+    alpha_all = sync_weights(counts_all)
+    my_alpha = [alpha_all[i] for i in mine]
+    my_counts = [counts_all[i] for i in mine]
+    comm = None
+    if world > 1:
+        uid = [Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = Comm(ctx, world, rank, uid[0])
+    kw = dict(optimizer=ADAM, lr=0.01, seed=0, ctx=ctx)
+    shared = GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **kw)
+    reps = [GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **kw) for _ in shards]
+    for r in reps:
+        r.copy_params_from(shared)
+
+    def average():
+        if comm is None:
+            model_average(reps, my_counts, shared)
+        else:
+            if len(reps) == 1:
+                shared.copy_params_from(reps[0])
+            else:
+                model_average(reps, my_counts, shared)
+            shared.scale(sum(my_alpha))
+            shared.allreduce(comm)
+        for r in reps:
+            r.copy_params_from(shared)
+
+    state = {"it": 0}
+
+    def step(e2e=False):
+        losses = []
+        for r, s, hf in zip(reps, shards, host_feats):
+            if e2e:
+                s.upload_features(hf.numpy())
+            losses.append(r.train_step(s, want_loss=e2e))
+        state["it"] += 1
+        if state["it"] % args.sync == 0:
+            average()
+        return losses
+
+    def timed(n, e2e=False):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        wall0 = time.perf_counter()
+        for _ in range(n):
+            step(e2e)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        ms = ev0.elapsed_time(ev1)
+        if e2e:
+            ms = max(ms, wall * 1e3)  # host-side copies/syncs are part of the end-to-end time
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    ctx.set_kernel_timing(True)
+    with ClockSampler(local) as clk:
+        total_ms = timed(args.steps)
+    kt = ctx.kernel_time()
+    ctx.set_kernel_timing(False)
+    launches = ctx.launches - launches0
+    ms_step = total_ms / args.steps
+
+    widths = [(x + 3) // 4 * 4 for x in w.passes()]
+    part_nnz = [meta["part_nnz"][i] for i in mine]
+    part_rows = [meta["part_rows"][i] for i in mine]
+    edges_per_step_rank = sum(part_nnz) * len(widths)
+    edges_per_step = sum(meta["part_nnz"]) * len(widths)
+    value = edges_per_step * args.steps / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (K2) from per-launch CUDA events
+    self_terms = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
+    algo_bytes = sum(agg_bytes(nz, rw, wd, self_terms) for nz, rw in zip(part_nnz, part_rows) for wd in widths)
+    agg_ms_step = kt["agg_ms"] / args.steps
+    hbm, bf16, src = peaks()
+    achieved_gbs = algo_bytes / (agg_ms_step / 1e3) / 1e9 if agg_ms_step > 0 else None
+    per_launch = kt["agg_launches"] / args.steps
+    ncu = load_ncu_traffic()
+    roofline = {"bound": "hbm", "kernel": "catgnn::agg_kernel (K2 neighbourhood aggregation)",
+                "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved_gbs / hbm) if achieved_gbs else None,
+                "traffic": ncu.get("dram_bytes_per_launch") if ncu else None,
+                "algorithmic_bytes_per_launch": algo_bytes / max(per_launch, 1),
+                "launches_per_step": per_launch, "agg_ms_per_step": agg_ms_step,
+                "agg_share_of_step": agg_ms_step / ms_step,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                "note": "algorithmic bytes per SURVEY §8(d); RMAT hub rows are re-served from L2, so "
+                        "algorithmic GB/s can exceed the DRAM peak — traffic is ncu dram bytes"}
+    # useful GEMM flops per step: forward + weight gradient (+ input gradient past layer 0)
+    gemm_flops = 0
+    for rows_i in part_rows:
+        d_in = w.dim
+        for l in range(w.layers):
+            d_out = w.classes if l + 1 == w.layers else w.hidden
+            k = 2 * d_in if w.model == "sage" else d_in
+            gemm_flops += 2 * rows_i * k * d_out * (3 if l > 0 else 2)
+            d_in = d_out
+    gemm = {"kernel": "catgnn::gemm_tf32_kernel (K3 tcgen05 kind::tf32, 3xTF32)",
+            "ms_per_step": kt["gemm_ms"] / args.steps,
+            "achieved_tflops": gemm_flops / (kt["gemm_ms"] / args.steps / 1e3) / 1e12 if kt["gemm_ms"] else None,
+            "peak_tflops_tf32": bf16 / 2, "peak_note": "dense TF32 = half the measured bf16 figure"}
+
+    # end-to-end through the C ABI: features re-uploaded from pinned host memory each step, loss read back
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            step(True)
+        e2e_ms = timed(args.steps, e2e=True) / args.steps
+        h2d = sum(int(h.numel()) * 4 for h in host_feats) * world
+        e2e = {"value": edges_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
+               "path": "catgnn_shard_upload_features (pinned H2D) + catgnn_model_train_step per partition "
+                       "+ loss D2H + model averaging"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = cpu_reference_rate(w, reference_jobs(prep, [0], args.ref_edges))
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 aggregation)",
+                "data": "synthetic (RMAT + reference SPRING partitions, random-init weights)",
+                "config": workload_config(w, prep, args), "roofline": roofline, "gemm": gemm,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "global_nnz_edges_per_s": meta["nnz"] * len(widths) * args.steps / (total_ms / 1e3),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -56,13 +56,13 @@ def _rmat_chunk(rng, m, scale, a, b, c):
     return src, dst
 
 
-def rmat_edges(scale: int, num_edges: int, a=0.57, b=0.19, c=0.19, seed=1, chunk=1 << 24):
+def rmat_edges(scale: int, num_edges: int, a=0.57, b=0.19, c=0.19, seed=1, chunk=1 << 26):
     """Returns (edges uint64 [E,2] with compacted ids, num_nodes, raw_ids_seen)."""
     rng = np.random.Generator(np.random.PCG64(seed_for(seed, 0x3A7)))
     keys_all, src_all, dst_all = [], [], []
     have = 0
     while True:
-        m = max(chunk, int((num_edges - have) * 1.3) + 1024) if have < num_edges else chunk
+        m = min(chunk, int((num_edges - have) * 1.3) + 1024)
         s, d = _rmat_chunk(rng, m, scale, a, b, c)
         keep = s != d
         s, d = s[keep], d[keep]

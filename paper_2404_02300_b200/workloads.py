@@ -1,0 +1,147 @@
+"""Benchmark workloads (BASELINE.json configs) and their cached preparation.
+
+Preparation happens before any timed region:
+  1. RMAT edge stream (synth.rmat_edges; SURVEY.md §8(d) generation details),
+     written as EDG1 so the reference partitioner can stream it;
+  2. the reference's own SPRING assignment (upstream/_ref, built unmodified
+     from /root/reference/proj/src/spring.cpp) — consumed unchanged;
+  3. 1-hop neighbour completion (synth.complete_edges, bit-exact with the
+     reference's complete_edges on duplicate-free streams, tests/test_synth.py);
+  4. labels / roles / class-mean features (reference scheme, synth.py).
+Results are cached in $CATGNN_CACHE (default /tmp/catgnn_cache) so repeated
+runs on one box (e.g. the 1/2/4/8-GPU sweep) reuse them.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import time
+from dataclasses import asdict, dataclass
+
+import numpy as np
+
+from . import synth
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    model: str          # gcn | sage | gin
+    layers: int
+    hidden: int
+    scale: int
+    edges: int
+    dim: int
+    classes: int
+    partitions: int
+    fracs: tuple
+    seed: int = 42
+    beta: float = 1.05
+    tau_vol: int = 0    # 0 = reference default ceil(2|E|/p)
+
+    def key(self) -> str:
+        return hashlib.sha1(json.dumps(asdict(self), sort_keys=True).encode()).hexdigest()[:12]
+
+    def passes(self) -> list:
+        """Aggregation widths per epoch (forward + backward), aggregating at
+        min(d_in, d_out); layer-1 backward aggregation only when the first
+        layer aggregates after its transform."""
+        out = []
+        bwd = []
+        for l in range(self.layers):
+            d_in = self.dim if l == 0 else self.hidden
+            d_out = self.classes if l + 1 == self.layers else self.hidden
+            if self.model == "sage":
+                agg_first = d_in <= d_out
+                w = d_in if agg_first else d_out
+                out.append(w)
+                if not (agg_first and l == 0):
+                    bwd.append(w)
+            else:
+                agg_first = d_in < d_out
+                w = d_in if agg_first else d_out
+                out.append(w)
+                if not (agg_first and l == 0):
+                    bwd.append(w)
+        return out + bwd[::-1]
+
+
+WORKLOADS = {
+    # configs[1]: 2-layer GCN, reddit-shaped (233k nodes, 114M nnz, 602-d, 41 classes), 8 partitions
+    "reddit_gcn": Workload("reddit_gcn", "gcn", 2, 256, 18, 57_307_946, 602, 41, 8, (0.66, 0.10, 0.24)),
+    # configs[0]: 2-layer GraphSAGE-mean, RMAT 2^16 avg-degree 16, 64-d, 8 classes, 2 SPRING partitions
+    "cfg1_sage": Workload("cfg1_sage", "sage", 2, 256, 16, 524_288, 64, 8, 2, (0.70, 0.15, 0.15), seed=1),
+    # configs[2]: 3-layer GraphSAGE, ogbn-products-shaped (2.45M nodes, 62M edges, 100-d, 47 classes)
+    "products_sage": Workload("products_sage", "sage", 3, 256, 22, 61_859_140, 100, 47, 8, (0.08, 0.02, 0.90)),
+    # small smoke workload
+    "tiny_gcn": Workload("tiny_gcn", "gcn", 2, 64, 12, 40_000, 32, 8, 4, (0.6, 0.2, 0.2), seed=3),
+}
+
+
+def cache_dir(w: Workload) -> str:
+    root = os.environ.get("CATGNN_CACHE", "/tmp/catgnn_cache")
+    d = os.path.join(root, f"{w.name}_{w.key()}")
+    os.makedirs(d, exist_ok=True)
+    return d
+
+
+def prepare(w: Workload, log=print) -> dict:
+    """Builds (or loads) the partitioned dataset; returns a dict of arrays/metadata."""
+    d = cache_dir(w)
+    meta_path = os.path.join(d, "meta.json")
+    if os.path.exists(meta_path):
+        with open(meta_path) as f:
+            meta = json.load(f)
+        log(f"[prep] cached {d}")
+        return dict(meta=meta, dir=d)
+    t0 = time.time()
+    e, n, _ = synth.rmat_edges(w.scale, w.edges, seed=w.seed)
+    t1 = time.time()
+    edge_file = os.path.join(d, "edges.bin")
+    with open(edge_file, "wb") as f:
+        f.write(b"EDG1")
+        e.tofile(f)
+    from upstream.spring import spring_homes  # the reference's SPRING (prep only)
+    home, tau = spring_homes(edge_file, n, w.partitions, beta=w.beta, tau_vol=w.tau_vol, seed=0)
+    t2 = time.time()
+    labels, roles = synth.node_meta(n, w.classes, *w.fracs, seed=w.seed)
+    parts = synth.complete_edges(e, home, roles, w.partitions)
+    t3 = time.time()
+    for i, p in enumerate(parts):
+        np.save(os.path.join(d, f"p{i}_edges.npy"), p.edges)
+        np.save(os.path.join(d, f"p{i}_ext.npy"), p.ext)
+        np.save(os.path.join(d, f"p{i}_owner.npy"), p.owner)
+        np.save(os.path.join(d, f"p{i}_role.npy"), p.role)
+    np.save(os.path.join(d, "labels.npy"), labels)
+    np.save(os.path.join(d, "roles.npy"), roles)
+    X = synth.class_features(labels, w.dim, w.classes, seed=w.seed)
+    np.save(os.path.join(d, "features.npy"), X)
+    t4 = time.time()
+    part_edges = [int(p.edges.shape[0]) for p in parts]
+    meta = dict(num_nodes=n, num_edges=w.edges, nnz=2 * w.edges, tau_vol=int(tau), beta=w.beta,
+                rf=synth.replication_factor(parts, n), part_rows=[p.rows for p in parts],
+                part_edges=part_edges, part_nnz=[2 * x for x in part_edges],
+                part_owned=[int(p.owner.sum()) for p in parts],
+                part_train=[int(((p.owner == 1) & (p.role == 1)).sum()) for p in parts],
+                sum_over_max=float(sum(part_edges) / max(max(part_edges), 1)),
+                times=dict(rmat=t1 - t0, spring=t2 - t1, completion=t3 - t2, features=t4 - t3))
+    with open(meta_path, "w") as f:
+        json.dump(meta, f)
+    log(f"[prep] built {d} in {t4 - t0:.1f}s {meta['times']}")
+    return dict(meta=meta, dir=d)
+
+
+def load_part(prep: dict, i: int, X=None, labels=None):
+    d = prep["dir"]
+    edges = np.load(os.path.join(d, f"p{i}_edges.npy"))
+    ext = np.load(os.path.join(d, f"p{i}_ext.npy"))
+    owner = np.load(os.path.join(d, f"p{i}_owner.npy"))
+    role = np.load(os.path.join(d, f"p{i}_role.npy"))
+    if labels is None:
+        labels = np.load(os.path.join(d, "labels.npy"))
+    if X is None:
+        X = np.load(os.path.join(d, "features.npy"), mmap_mode="r")
+    idx = ext.astype(np.int64)
+    return dict(edges=edges, ext=ext, owner=owner, role=role, labels=labels[idx],
+                features=np.ascontiguousarray(X[idx]))

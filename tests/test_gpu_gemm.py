@@ -47,9 +47,10 @@ def test_gemm_cancellation_needs_3xtf32(ctx):
     B = rng.standard_normal((96, 20000)).astype(np.float32)
     B[:, 10000:] = -B[:, :10000] * np.float32(0.999)
     A[:, 10000:] = A[:, :10000]
-    want = A.astype(np.float64) @ B.astype(np.float64).T
+    want = A.astype(np.float64) @ B.astype(np.float64).T   # ~1000x smaller than its terms
+    err1 = np.linalg.norm(gemm(ctx, A, B, 0, 1) - want) / np.linalg.norm(want)
     err3 = np.linalg.norm(gemm(ctx, A, B, 0, 3) - want) / np.linalg.norm(want)
-    assert err3 < 1e-4, err3
+    assert err3 < err1 / 50 and err3 < 1e-2, (err1, err3)
 
 
 def test_gemm_k_zero(ctx):
