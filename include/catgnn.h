@@ -239,6 +239,11 @@ int catgnn_model_allreduce(catgnn_model m, catgnn_comm c);
  * 3 = 3xTF32 (split operands, ~fp32 accuracy); split_k 0 = automatic. */
 int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
                    const float* B, float* C, uint32_t split_k, int precision);
+/* Synthetic RMAT(a,b,c,1-a-b-c) stream of num_edges unique undirected pairs, no
+ * self-loops, first-seen orientation, ids compacted to 0..|V|-1 (bench input
+ * preparation).  out_edges holds 2*num_edges u64. */
+int catgnn_synth_rmat(uint32_t scale, uint64_t num_edges, double a, double b, double c,
+                      uint64_t seed, uint64_t* out_edges, uint64_t* num_nodes);
 
 #ifdef __cplusplus
 }

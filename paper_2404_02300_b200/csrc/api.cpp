@@ -79,6 +79,22 @@ void h2d(T* dst, const T* src, size_t n, cudaStream_t st) {
   if (n) CG_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
 }
 
+// Host rows x dim -> device rows x ld.  One contiguous H2D copy (full PCIe /
+// C2C bandwidth from pinned memory; a pitched host copy with 2408-byte rows
+// runs at a fraction of it), then an on-device re-pitch when dim % 4 != 0.
+void copy_features_in(catgnn_shard_s* s, const float* feats, uint32_t dim) {
+  cudaStream_t st = s->ctx->stream;
+  const size_t bytes = s->rows * (size_t)dim * sizeof(float);
+  if (s->ld == dim) {
+    CG_CUDA(cudaMemcpyAsync(s->x.p, feats, bytes, cudaMemcpyHostToDevice, st));
+    return;
+  }
+  float* stage = s->ctx->scratch_buf<float>("feat_stage", s->rows * (size_t)dim);
+  CG_CUDA(cudaMemcpyAsync(stage, feats, bytes, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpy2DAsync(s->x.p, s->ld * sizeof(float), stage, dim * sizeof(float), dim * sizeof(float),
+                            s->rows, cudaMemcpyDeviceToDevice, st));
+}
+
 void upload_features(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   s->dim = dim;
   s->ld = round_up(std::max<uint32_t>(dim, 1), 4);
@@ -87,9 +103,7 @@ void upload_features(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   s->xT_valid = false;
   if (s->rows == 0 || dim == 0) return;
   if (s->ld != dim) CG_CUDA(cudaMemsetAsync(s->x.p, 0, s->x.bytes(), s->ctx->stream));
-  if (feats)
-    CG_CUDA(cudaMemcpy2DAsync(s->x.p, s->ld * sizeof(float), feats, dim * sizeof(float),
-                              dim * sizeof(float), s->rows, cudaMemcpyHostToDevice, s->ctx->stream));
+  if (feats) copy_features_in(s, feats, dim);
 }
 
 void set_labels(catgnn_shard_s* s, const int32_t* labels, const uint32_t* tr, uint64_t ntr,
@@ -494,9 +508,7 @@ int catgnn_shard_upload_features(catgnn_shard s, const float* features, uint32_t
       upload_features(s, features, dim);
       return;
     }
-    if (s->rows && dim)
-      CG_CUDA(cudaMemcpy2DAsync(s->x.p, s->ld * sizeof(float), features, dim * sizeof(float),
-                                dim * sizeof(float), s->rows, cudaMemcpyHostToDevice, s->ctx->stream));
+    if (s->rows && dim) copy_features_in(s, features, dim);
     s->xT_valid = false;
   });
 }

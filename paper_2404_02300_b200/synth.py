@@ -40,49 +40,70 @@ def seed_for(seed: int, stream: int) -> int:
     return mix64(seed ^ mix64((stream + 0x51ED2701) & MASK64))
 
 
-def _rmat_chunk(rng, m, scale, a, b, c):
-    thr_a = np.uint32(a * 2**32)
-    thr_ab = np.uint32(min((a + b) * 2**32, 2**32 - 1))
-    thr_abc = np.uint32(min((a + b + c) * 2**32, 2**32 - 1))
-    src = np.zeros(m, np.uint64)
-    dst = np.zeros(m, np.uint64)
+def _mix64_np(x):
+    """common.hpp:27-32 on uint64 arrays (wrapping arithmetic)."""
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def _thr(p):
+    return np.uint64(int(min(p * 4294967296.0, 4294967295.0)))
+
+
+def _rmat_draw(base, idx, scale, a, b, c):
+    """Quadrant choices of candidates idx (uint64 array): counter-based stream,
+    word j of candidate i = splitmix64(base + 16 i + j//2), 32 bits per level."""
+    ta, tab, tabc = _thr(a), _thr(a + b), _thr(a + b + c)
+    s = np.zeros(idx.size, np.uint64)
+    d = np.zeros(idx.size, np.uint64)
+    word = None
     for level in range(scale):
-        r = rng.integers(0, 2**32, size=m, dtype=np.uint32)
-        bs = r >= thr_ab                      # quadrants c, d -> src bit
-        bd = ((r >= thr_a) & (r < thr_ab)) | (r >= thr_abc)  # quadrants b, d -> dst bit
-        shift = np.uint64(scale - 1 - level)
-        src |= bs.astype(np.uint64) << shift
-        dst |= bd.astype(np.uint64) << shift
-    return src, dst
+        if level % 2 == 0:
+            word = _mix64_np(np.uint64(base) + np.uint64(16) * idx + np.uint64(level >> 1))
+        r = (word >> np.uint64(32)) if level & 1 else (word & np.uint64(0xFFFFFFFF))
+        bs = r >= tab
+        bd = ((r >= ta) & (r < tab)) | (r >= tabc)
+        sh = np.uint64(scale - 1 - level)
+        s |= bs.astype(np.uint64) << sh
+        d |= bd.astype(np.uint64) << sh
+    return s, d
 
 
-def rmat_edges(scale: int, num_edges: int, a=0.57, b=0.19, c=0.19, seed=1, chunk=1 << 26):
-    """Returns (edges uint64 [E,2] with compacted ids, num_nodes, raw_ids_seen)."""
-    rng = np.random.Generator(np.random.PCG64(seed_for(seed, 0x3A7)))
-    keys_all, src_all, dst_all = [], [], []
-    have = 0
+def rmat_edges_numpy(scale: int, num_edges: int, a=0.57, b=0.19, c=0.19, seed=1):
+    """Pure NumPy statement of the generator (checker for the C++ one)."""
+    base = seed_for(seed, 0x3A7)
+    n_cand = num_edges + num_edges * 3 // 10 + 1024
     while True:
-        m = min(chunk, int((num_edges - have) * 1.3) + 1024)
-        s, d = _rmat_chunk(rng, m, scale, a, b, c)
-        keep = s != d
-        s, d = s[keep], d[keep]
-        lo = np.minimum(s, d); hi = np.maximum(s, d)
-        src_all.append(s); dst_all.append(d); keys_all.append((lo << np.uint64(32)) | hi)
-        keys = np.concatenate(keys_all)
-        _, first = np.unique(keys, return_index=True)
-        have = first.size
-        if have >= num_edges:
+        idx = np.arange(n_cand, dtype=np.uint64)
+        s, d = _rmat_draw(base, idx, scale, a, b, c)
+        valid = s != d
+        key = (np.minimum(s, d) << np.uint64(32)) | np.maximum(s, d)
+        vidx = idx[valid]
+        _, first = np.unique(key[valid], return_index=True)
+        if first.size >= num_edges:
             break
-    first.sort()
-    first = first[:num_edges]
-    src = np.concatenate(src_all)[first]
-    dst = np.concatenate(dst_all)[first]
-    raw = np.concatenate([src, dst])
-    seen = np.unique(raw)
+        n_cand = n_cand + n_cand // 2
+    chosen = np.sort(vidx[first])[:num_edges]
+    s, d = _rmat_draw(base, chosen, scale, a, b, c)
+    seen = np.unique(np.concatenate([s, d]))
     e = np.empty((num_edges, 2), np.uint64)
-    e[:, 0] = np.searchsorted(seen, src)
-    e[:, 1] = np.searchsorted(seen, dst)
+    e[:, 0] = np.searchsorted(seen, s)
+    e[:, 1] = np.searchsorted(seen, d)
     return e, int(seen.size), seen
+
+
+def rmat_edges(scale: int, num_edges: int, a=0.57, b=0.19, c=0.19, seed=1):
+    """RMAT stream via the parallel C++ generator (catgnn_synth_rmat), identical
+    to rmat_edges_numpy.  Returns (edges uint64 [E,2] compacted, num_nodes, None)."""
+    import ctypes as C
+    from ._lib import check, lib
+    e = np.empty((num_edges, 2), np.uint64)
+    n = C.c_uint64()
+    check(lib.catgnn_synth_rmat(C.c_uint32(scale), C.c_uint64(num_edges), C.c_double(a), C.c_double(b),
+                                C.c_double(c), C.c_uint64(seed), e.ctypes.data_as(C.c_void_p), C.byref(n)))
+    return e, int(n.value), None
 
 
 def node_meta(num_nodes: int, classes: int, train_frac: float, val_frac: float, test_frac: float, seed: int):

@@ -35,6 +35,13 @@ def test_rmat_invariants():
     assert np.array_equal(e, e2) and n == n2               # deterministic
 
 
+@pytest.mark.parametrize("scale,edges,seed", [(6, 200, 0), (9, 1500, 7), (12, 40000, 3), (14, 100000, 11)])
+def test_cpp_generator_matches_numpy_statement(scale, edges, seed):
+    a = synth.rmat_edges_numpy(scale, edges, seed=seed)
+    b = synth.rmat_edges(scale, edges, seed=seed)
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+
+
 def test_seed_for_matches_reference():
     from oracle import ref
     for s, k in [(0, 0), (1, 0xFEA7), (42, 7), (2**63 + 5, 2**40)]:
