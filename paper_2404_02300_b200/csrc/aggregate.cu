@@ -18,6 +18,7 @@
 // more than U neighbours are chunked; chunk partials are combined in chunk
 // order by agg_fixup_kernel, so results are deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 
 #include "shard.hpp"
@@ -225,10 +226,25 @@ AggFn pick_pre(bool pre) {
 // Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
 constexpr uint32_t kMaxSlab4 = 256;
 
+int narrow_mode() {
+  static int m = [] {
+    const char* s = std::getenv("CATGNN_NARROW");
+    return s ? std::atoi(s) : 0;
+  }();
+  return m;
+}
+
 AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
   if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre); }
   if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre); }
-  if (w4 <= 16) { *lpn_out = 16; return pick_pre<1, 16>(pre); }
+  if (w4 <= 16) {
+    // narrow rows: lanes per neighbour x float4 per lane
+    switch (narrow_mode()) {
+      case 1: *lpn_out = 8; return pick_pre<2, 8>(pre);
+      case 2: *lpn_out = 4; return pick_pre<4, 4>(pre);
+      default: *lpn_out = 16; return pick_pre<1, 16>(pre);
+    }
+  }
   *lpn_out = 32;
   switch ((w4 + 31) / 32) {
     case 1: return pick_pre<1, 32>(pre);

@@ -30,7 +30,7 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;              // fp32 elements per k-block row = 128 bytes
 constexpr int A_STAGE = BM * BK * 4;  // 16 KB
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 10 warps: TMA, MMA, 4 converters, 4 epilogue
 
 struct GemmArgs {
   uint32_t M, N, K;
@@ -40,6 +40,7 @@ struct GemmArgs {
   uint32_t tmem_cols;
   uint32_t idesc;
   uint32_t split3;  // 1: 3xTF32 (hi*hi + hi*lo + lo*hi), 0: plain TF32
+  uint32_t mt, nt, splits, tiles;
   GemmEpi epi;
 };
 
@@ -138,6 +139,29 @@ __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint3
   return v;
 }
 
+__device__ __forceinline__ void tile_coords(const GemmArgs& a, uint32_t t, uint32_t& m0, uint32_t& n0,
+                                            uint32_t& kb0, uint32_t& nkb) {
+  // n fastest: CTAs working on the same M block at the same time share A in L2
+  const uint32_t n = t % a.nt, m = (t / a.nt) % a.mt, z = t / (a.nt * a.mt);
+  m0 = m * BM;
+  n0 = n * a.BN;
+  const uint32_t nkb_total = (a.K + BK - 1) / BK;
+  kb0 = z * a.kb_per_split;
+  const uint32_t kb1 = min(nkb_total, kb0 + a.kb_per_split);
+  nkb = kb1 > kb0 ? kb1 - kb0 : 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Persistent warp-specialised kernel (one CTA per SM):
+//   warp 0     TMA producer over every tile's k-blocks (S-stage ring)
+//   warp 1     TMEM allocator + MMA issuer; accumulators double-buffered in
+//              TMEM (2 x acc_cols columns) so tile i's epilogue overlaps tile
+//              i+1's MMAs
+//   warps 2-5  3xTF32 converters (lo = x - tf32(x) tiles), idle otherwise
+//   warps 6-9  epilogue: tcgen05.ld -> fused epilogue -> 128-bit stores
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs args) {
@@ -149,30 +173,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool split3 = args.split3 != 0;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)S * A_STAGE;
-  // 3xTF32: residual ("lo") tiles with the same swizzled layout
-  uint8_t* sAl = sB + (size_t)S * B_STAGE;
+  uint8_t* sAl = sB + (size_t)S * B_STAGE;  // 3xTF32 residual tiles (same swizzled layout)
   uint8_t* sBl = sAl + (split3 ? (size_t)S * A_STAGE : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (split3 ? (size_t)S * B_STAGE : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* conv = bars + 2 * S;
-  uint64_t* accum = bars + 3 * S;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
-
+  uint64_t* tfull = bars + 3 * S;    // [2] accumulator ready
+  uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const uint32_t nkb_total = (args.K + BK - 1) / BK;
-  const uint32_t kb0 = blockIdx.z * args.kb_per_split;
-  const uint32_t kb1 = min(nkb_total, kb0 + args.kb_per_split);
-  const uint32_t nkb = kb1 > kb0 ? kb1 - kb0 : 0;
 
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < S; ++i) {
       mbar_init(smem_u32(full + i), 1);
       mbar_init(smem_u32(empty + i), 1);
-      mbar_init(smem_u32(conv + i), 4);  // one arrive per converter warp
+      mbar_init(smem_u32(conv + i), 4);
     }
-    mbar_init(smem_u32(accum), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(tfull + b), 1);
+      mbar_init(smem_u32(tempty + b), 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -186,107 +207,156 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_holder;
+  const uint32_t acc_cols = args.tmem_cols / 2;
 
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t bytes = A_STAGE + B_STAGE;
-      for (uint32_t i = 0; i < nkb; ++i) {
-        const uint32_t s = i % S, ph = (i / S) & 1;
-        mbar_wait(smem_u32(empty + s), ph ^ 1);
-        mbar_expect_tx(smem_u32(full + s), bytes);
-        const int kx = (int)((kb0 + i) * BK);
-        tma_load_2d(smem_u32(sA + (size_t)s * A_STAGE), &tmA, kx, (int)m0, smem_u32(full + s));
-        tma_load_2d(smem_u32(sB + (size_t)s * B_STAGE), &tmB, kx, (int)n0, smem_u32(full + s));
+      uint32_t it = 0;
+      for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+        uint32_t m0, n0, kb0, nkb;
+        tile_coords(args, t, m0, n0, kb0, nkb);
+        for (uint32_t i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % S, ph = (it / S) & 1;
+          mbar_wait(smem_u32(empty + s), ph ^ 1);
+          mbar_expect_tx(smem_u32(full + s), bytes);
+          const int kx = (int)((kb0 + i) * BK);
+          tma_load_2d(smem_u32(sA + (size_t)s * A_STAGE), &tmA, kx, (int)m0, smem_u32(full + s));
+          tma_load_2d(smem_u32(sB + (size_t)s * B_STAGE), &tmB, kx, (int)n0, smem_u32(full + s));
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (uint32_t i = 0; i < nkb; ++i) {
-        const uint32_t s = i % S, ph = (i / S) & 1;
-        mbar_wait(smem_u32(split3 ? conv + s : full + s), ph);
+      uint32_t it = 0, j = 0;
+      for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++j) {
+        uint32_t m0, n0, kb0, nkb;
+        tile_coords(args, t, m0, n0, kb0, nkb);
+        const uint32_t b = j & 1;
+        mbar_wait(smem_u32(tempty + b), ((j >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
-        const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
-        if (split3) {
-          const uint32_t al = smem_u32(sAl + (size_t)s * A_STAGE);
-          const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
+        const uint32_t acc = tmem + b * acc_cols;
+        for (uint32_t i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % S, ph = (it / S) & 1;
+          mbar_wait(smem_u32(split3 ? conv + s : full + s), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
+          const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
+          if (split3) {
+            const uint32_t al = smem_u32(sAl + (size_t)s * A_STAGE);
+            const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first
-            mma_tf32(tmem, umma_desc(al + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
-                     (i > 0 || ks > 0) ? 1u : 0u);
-            mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(bl + ks * 32), args.idesc, 1u);
-            mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc, 1u);
+            for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first
+              mma_tf32(acc, umma_desc(al + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
+                       (i > 0 || ks > 0) ? 1u : 0u);
+              mma_tf32(acc, umma_desc(a0 + ks * 32), umma_desc(bl + ks * 32), args.idesc, 1u);
+              mma_tf32(acc, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
+              mma_tf32(acc, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
+                       (i > 0 || ks > 0) ? 1u : 0u);
+          }
+          mma_commit(smem_u32(empty + s));
+        }
+        if (nkb) mma_commit(smem_u32(tfull + b));
+        else mbar_arrive(smem_u32(tfull + b));  // empty K range: epilogue writes zeros
+      }
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    if (split3) {
+      const uint32_t tt = threadIdx.x - 64;
+      const uint32_t a4 = A_STAGE / 16, b4 = B_STAGE / 16;
+      uint32_t it = 0;
+      for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+        uint32_t m0, n0, kb0, nkb;
+        tile_coords(args, t, m0, n0, kb0, nkb);
+        for (uint32_t i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % S, ph = (it / S) & 1;
+          mbar_wait(smem_u32(full + s), ph);
+          const float4* ah = reinterpret_cast<const float4*>(sA + (size_t)s * A_STAGE);
+          float4* alo = reinterpret_cast<float4*>(sAl + (size_t)s * A_STAGE);
+          const float4* bh = reinterpret_cast<const float4*>(sB + (size_t)s * B_STAGE);
+          float4* blo = reinterpret_cast<float4*>(sBl + (size_t)s * B_STAGE);
+          for (uint32_t k = tt; k < a4; k += 128) alo[k] = tf32_residual4(ah[k]);
+          for (uint32_t k = tt; k < b4; k += 128) blo[k] = tf32_residual4(bh[k]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(conv + s));
+        }
+      }
+    }
+  } else {
+    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const GemmEpi& e = args.epi;
+    uint32_t j = 0;
+    for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++j) {
+      uint32_t m0, n0, kb0, nkb;
+      tile_coords(args, t, m0, n0, kb0, nkb);
+      const uint32_t b = j & 1;
+      mbar_wait(smem_u32(tfull + b), (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t row = m0 + q * 32 + lane;
+      const bool row_ok = row < args.M;
+      const float rs = (row_ok && e.rowscale) ? __ldg(e.rowscale + row) : 1.f;
+      const uint32_t z = t / (args.nt * args.mt);
+      for (uint32_t c = 0; c < BN; c += 32) {
+        float v[32];
+        if (nkb) {
+          tmem_ld32(tmem + b * acc_cols + ((q * 32u) << 16) + c, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        const uint32_t col0 = n0 + c;
+        if (!row_ok || col0 >= args.N) continue;
+        if (e.partial) {
+          float* dst = e.partial + ((size_t)z * args.M + row) * args.N + col0;
+          if (col0 + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < args.N) dst[i] = v[i];
+          }
+          continue;
+        }
+        float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
+        if (col0 + 32 <= args.N) {
+          const float* mrow = e.mask ? e.mask + (size_t)row * e.mask_ld + e.mask_col + col0 : nullptr;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            if (e.rowscale) {
+              if (col0 + i >= e.scale_col_begin) { o.x *= rs; o.y *= rs; o.z *= rs; o.w *= rs; }
+            }
+            if (e.bias) {
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + col0 + i));
+              o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+            }
+            if (e.relu) {
+              o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+            }
+            if (mrow) {
+              const float4 mm = __ldg(reinterpret_cast<const float4*>(mrow + i));
+              o.x = mm.x > 0.f ? o.x : 0.f; o.y = mm.y > 0.f ? o.y : 0.f;
+              o.z = mm.z > 0.f ? o.z : 0.f; o.w = mm.w > 0.f ? o.w : 0.f;
+            }
+            *reinterpret_cast<float4*>(dst + i) = o;
           }
         } else {
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
-            mma_tf32(tmem, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
-                     (i > 0 || ks > 0) ? 1u : 0u);
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < args.N) dst[i] = apply_epi(e, row, col0 + i, v[i]);
         }
-        mma_commit(smem_u32(empty + s));
       }
-      if (nkb) mma_commit(smem_u32(accum));
-    }
-    __syncwarp();
-  } else {
-    // epilogue warps 2..5: TMEM lane quarter = warp % 4
-    const uint32_t q = warp & 3;
-    const uint32_t row = m0 + q * 32 + lane;
-    if (split3) {
-      // lo = x - tf32_trunc(x) for every element of the A and B tiles of each
-      // stage (element-wise, so the swizzled layout carries over)
-      const uint32_t t = threadIdx.x - 64;
-      const uint32_t a4 = A_STAGE / 16, b4 = B_STAGE / 16;
-      for (uint32_t i = 0; i < nkb; ++i) {
-        const uint32_t s = i % S, ph = (i / S) & 1;
-        mbar_wait(smem_u32(full + s), ph);
-        const float4* ah = reinterpret_cast<const float4*>(sA + (size_t)s * A_STAGE);
-        float4* alo = reinterpret_cast<float4*>(sAl + (size_t)s * A_STAGE);
-        const float4* bh = reinterpret_cast<const float4*>(sB + (size_t)s * B_STAGE);
-        float4* blo = reinterpret_cast<float4*>(sBl + (size_t)s * B_STAGE);
-        for (uint32_t k = t; k < a4; k += 128) alo[k] = tf32_residual4(ah[k]);
-        for (uint32_t k = t; k < b4; k += 128) blo[k] = tf32_residual4(bh[k]);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(conv + s)) : "memory");
-      }
-    }
-    if (nkb) {
-      mbar_wait(smem_u32(accum), 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    const GemmEpi& e = args.epi;
-    for (uint32_t c = 0; c < BN; c += 32) {
-      float v[32];
-      if (nkb) {
-        tmem_ld32(tmem + ((q * 32u) << 16) + c, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      if (row >= args.M) continue;
-      const uint32_t col0 = n0 + c;
-      if (e.partial) {
-        float* dst = e.partial + ((size_t)blockIdx.z * args.M + row) * args.N;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (col0 + i < args.N) dst[col0 + i] = v[i];
-        continue;
-      }
-      float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
-      if (col0 + 32 <= args.N) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          float4 o = make_float4(apply_epi(e, row, col0 + i, v[i]), apply_epi(e, row, col0 + i + 1, v[i + 1]),
-                                 apply_epi(e, row, col0 + i + 2, v[i + 2]),
-                                 apply_epi(e, row, col0 + i + 3, v[i + 3]));
-          *reinterpret_cast<float4*>(dst + i) = o;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (col0 + i < args.N) dst[i] = apply_epi(e, row, col0 + i, v[i]);
-      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(tempty + b));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -296,7 +366,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(args.tmem_cols));
   }
 }
-
 __global__ void gemm_reduce_kernel(const float* __restrict__ partial, uint32_t splits, uint32_t M,
                                    uint32_t N, GemmEpi e) {
   const uint64_t total = (uint64_t)M * N;
@@ -365,7 +434,10 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
     ctx->launches++;
     return;
   }
-  const uint32_t BN = N >= 256 ? 256 : round_up(N, 16);
+  const bool split3 = precision == 3;
+  // 3xTF32 doubles the stage (lo tiles): 128-wide N tiles keep 3 stages in flight
+  const uint32_t bn_max = split3 ? 128 : 256;
+  const uint32_t BN = N >= bn_max ? bn_max : round_up(N, 16);
   const uint32_t nkb = (K + BK - 1) / BK;
   const uint32_t mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
   uint32_t splits = 1;
@@ -380,14 +452,15 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   splits = std::max<uint32_t>(1, splits);
   const uint32_t kbps = std::max<uint32_t>(1, (nkb + splits - 1) / splits);
   splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
+  if ((epi.mask && (epi.mask_ld % 4 || epi.mask_col % 4)) || (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15)))
+    throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
   const uint32_t b_stage = BN * BK * 4;
-  const bool split3 = precision == 3;
   const size_t stage_bytes = (size_t)(A_STAGE + b_stage) * (split3 ? 2 : 1);
   const size_t budget = 227 * 1024 - 1024 - 512;
   uint32_t stages = (uint32_t)std::min<size_t>(6, budget / stage_bytes);
   if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (3 * stages + 2) * 8;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (3 * stages + 5) * 8;
 
   GemmArgs args{};
   args.M = M;
@@ -396,8 +469,12 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   args.BN = BN;
   args.stages = stages;
   args.kb_per_split = kbps;
-  args.tmem_cols = pow2_cols(BN);
+  args.tmem_cols = pow2_cols(2 * round_up(BN, 32));  // two accumulator buffers
   args.split3 = split3 ? 1u : 0u;
+  args.mt = mt;
+  args.nt = nt;
+  args.splits = splits;
+  args.tiles = mt * nt * splits;
   // instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
   args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   float* partial = nullptr;
@@ -417,7 +494,8 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
     attr_set = true;
   }
   int t = ctx->begin_timed(1);
-  gemm_tf32_kernel<<<dim3(mt, nt, splits), kThreads, smem, ctx->stream>>>(ta, tb, args);
+  const unsigned grid = std::min<unsigned>(args.tiles, (unsigned)ctx->num_sms);  // persistent
+  gemm_tf32_kernel<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, args);
   CG_CHECK_LAUNCH();
   ctx->launches++;
   if (splits > 1) {
