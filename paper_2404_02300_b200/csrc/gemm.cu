@@ -151,6 +151,35 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, uint32_t t, uint3
   nkb = kb1 > kb0 ? kb1 - kb0 : 0;
 }
 
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// lo = x - tf32(x) over n16 16-byte words of a stage tile; 128 converter
+// threads, 8 words in flight per thread (element-wise, so the SW128 layout of
+// the source carries over to the residual tile).
+__device__ __forceinline__ void convert_tile(uint32_t src, uint32_t dst, uint32_t n16, uint32_t t) {
+  for (uint32_t k0 = t; k0 < n16; k0 += 128 * 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t k = k0 + u * 128;
+      if (k < n16) v[u] = lds4(src + k * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t k = k0 + u * 128;
+      if (k < n16) sts4(dst + k * 16, tf32_residual4(v[u]));
+    }
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -276,12 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(smem_u32(full + s), ph);
-          const float4* ah = reinterpret_cast<const float4*>(sA + (size_t)s * A_STAGE);
-          float4* alo = reinterpret_cast<float4*>(sAl + (size_t)s * A_STAGE);
-          const float4* bh = reinterpret_cast<const float4*>(sB + (size_t)s * B_STAGE);
-          float4* blo = reinterpret_cast<float4*>(sBl + (size_t)s * B_STAGE);
-          for (uint32_t k = tt; k < a4; k += 128) alo[k] = tf32_residual4(ah[k]);
-          for (uint32_t k = tt; k < b4; k += 128) blo[k] = tf32_residual4(bh[k]);
+          convert_tile(smem_u32(sA + (size_t)s * A_STAGE), smem_u32(sAl + (size_t)s * A_STAGE), a4, tt);
+          convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)s * B_STAGE), b4, tt);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(conv + s));
