@@ -239,6 +239,10 @@ int catgnn_model_allreduce(catgnn_model m, catgnn_comm c);
  * 3 = 3xTF32 (split operands, ~fp32 accuracy); split_k 0 = automatic. */
 int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
                    const float* B, float* C, uint32_t split_k, int precision);
+/* General form: A given as M x K (a_mn = 0) or K x M (a_mn = 1, read MN-major
+ * by the tensor core), B as N x K or K x N; C[M x N] = A . B^T. */
+int catgnn_gemm(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A, int a_mn,
+                const float* B, int b_mn, float* C, uint32_t split_k, int precision);
 /* Synthetic RMAT(a,b,c,1-a-b-c) stream of num_edges unique undirected pairs, no
  * self-loops, first-seen orientation, ids compacted to 0..|V|-1 (bench input
  * preparation).  out_edges holds 2*num_edges u64. */

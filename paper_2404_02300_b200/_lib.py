@@ -90,6 +90,7 @@ def _load():
         "catgnn_model_scale": (C.c_int, [vp, f64]),
         "catgnn_model_allreduce": (C.c_int, [vp, vp]),
         "catgnn_gemm_tn": (C.c_int, [vp, u32, u32, u32, vp, vp, vp, u32, C.c_int]),
+        "catgnn_gemm": (C.c_int, [vp, u32, u32, u32, vp, C.c_int, vp, C.c_int, vp, u32, C.c_int]),
         "catgnn_synth_rmat": (C.c_int, [u32, u64, f64, f64, f64, u64, vp, P(u64)]),
     }
     for name, (res, args) in sig.items():

@@ -41,6 +41,7 @@ struct GemmArgs {
   uint32_t idesc;
   uint32_t split3;  // 1: 3xTF32 (hi*hi + hi*lo + lo*hi), 0: plain TF32
   uint32_t mt, nt, splits, tiles;
+  uint32_t a_mn, b_mn;  // operand stored MN-major ([K rows][M or N cols] row-major)
   GemmEpi epi;
 };
 
@@ -91,6 +92,30 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
   return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
          (2ull << 61);
+}
+
+// MN-major SWIZZLE_128B (tf32): 32-element (128 B) atoms along M/N, 8 K-rows per
+// 1 KB swizzle atom; LBO = 4 KB between M/N atoms (one TMA box of 32 x 32 each),
+// SBO = 1 KB between K groups.  One MMA (K = 8) consumes exactly one K group.
+__device__ __forceinline__ uint64_t umma_desc_mn(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | (256ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// descriptor of k-step ks (K = 8 elements) of a stage tile in either layout
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks, bool mn) {
+  return mn ? umma_desc_mn(base + ks * 1024) : umma_desc(base + ks * 32);
+}
+
+// TMA fill of one operand stage: K-major = one {32 x rows} box; MN-major =
+// rows/32 boxes of {32 (M/N) x 32 (K)} placed 4 KB apart.
+__device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, bool mn, int k0, int r0,
+                                             uint32_t rows, uint32_t bar) {
+  if (!mn) {
+    tma_load_2d(dst, map, k0, r0, bar);
+  } else {
+    for (uint32_t a = 0; a < rows / 32; ++a) tma_load_2d(dst + a * 4096, map, r0 + (int)(32 * a), k0, bar);
+  }
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -250,8 +275,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           mbar_expect_tx(smem_u32(full + s), bytes);
           const int kx = (int)((kb0 + i) * BK);
-          tma_load_2d(smem_u32(sA + (size_t)s * A_STAGE), &tmA, kx, (int)m0, smem_u32(full + s));
-          tma_load_2d(smem_u32(sB + (size_t)s * B_STAGE), &tmB, kx, (int)n0, smem_u32(full + s));
+          load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s));
+          load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BN, smem_u32(full + s));
         }
       }
     }
@@ -265,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(smem_u32(tempty + b), ((j >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + b * acc_cols;
+        const bool amn = args.a_mn != 0, bmn = args.b_mn != 0;
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(smem_u32(split3 ? conv + s : full + s), ph);
@@ -276,16 +302,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
 #pragma unroll
             for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first
-              mma_tf32(acc, umma_desc(al + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
-                       (i > 0 || ks > 0) ? 1u : 0u);
-              mma_tf32(acc, umma_desc(a0 + ks * 32), umma_desc(bl + ks * 32), args.idesc, 1u);
-              mma_tf32(acc, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc, 1u);
+              mma_tf32(acc, op_desc(al, ks, amn), op_desc(b0, ks, bmn), args.idesc, (i > 0 || ks > 0) ? 1u : 0u);
+              mma_tf32(acc, op_desc(a0, ks, amn), op_desc(bl, ks, bmn), args.idesc, 1u);
+              mma_tf32(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, 1u);
             }
           } else {
 #pragma unroll
             for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
-              mma_tf32(acc, umma_desc(a0 + ks * 32), umma_desc(b0 + ks * 32), args.idesc,
-                       (i > 0 || ks > 0) ? 1u : 0u);
+              mma_tf32(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, (i > 0 || ks > 0) ? 1u : 0u);
           }
           mma_commit(smem_u32(empty + s));
         }
@@ -437,6 +461,23 @@ CUtensorMap make_map(const float* ptr, uint64_t rows, uint64_t K, uint32_t ld, u
   return m;
 }
 
+// MN-major operand stored row-major as [K rows][MN cols]: inner dim = MN,
+// {32 x 32} boxes (128-byte inner rows for SWIZZLE_128B); OOB zero-filled.
+CUtensorMap make_map_mn(const float* ptr, uint64_t mn, uint64_t K, uint32_t ld) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16)
+    throw ConfigError("GEMM operand must be 16-byte aligned with a row stride multiple of 4 floats");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {mn, K};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, BK};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw InternalError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
 uint32_t pow2_cols(uint32_t n) {
   uint32_t c = 32;
   while (c < n) c <<= 1;
@@ -447,6 +488,14 @@ uint32_t pow2_cols(uint32_t n) {
 
 void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
              uint32_t N, uint32_t K, const GemmEpi& epi_in, uint32_t split_k, int precision) {
+  gemm(ctx, GemmOperand{A, lda, false}, GemmOperand{B, ldb, false}, M, N, K, epi_in, split_k, precision);
+}
+
+void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, uint32_t K,
+          const GemmEpi& epi_in, uint32_t split_k, int precision) {
+  const float* A = a.ptr;
+  const float* B = b.ptr;
+  const uint32_t lda = a.ld, ldb = b.ld;
   if (M == 0 || N == 0) return;
   GemmEpi epi = epi_in;
   if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
@@ -462,7 +511,8 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   const bool split3 = precision == 3;
   // 3xTF32 doubles the stage (lo tiles): 128-wide N tiles keep 3 stages in flight
   const uint32_t bn_max = split3 ? 128 : 256;
-  const uint32_t BN = N >= bn_max ? bn_max : round_up(N, 16);
+  // MN-major B is loaded in 32-wide atoms
+  const uint32_t BN = N >= bn_max ? bn_max : round_up(N, b.mn_major ? 32 : 16);
   const uint32_t nkb = (K + BK - 1) / BK;
   const uint32_t mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
   uint32_t splits = 1;
@@ -500,8 +550,11 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
   args.nt = nt;
   args.splits = splits;
   args.tiles = mt * nt * splits;
-  // instruction descriptor: D f32, A/B tf32, both K-major, N>>3, M>>4
-  args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  args.a_mn = a.mn_major ? 1u : 0u;
+  args.b_mn = b.mn_major ? 1u : 0u;
+  // instruction descriptor: D f32, A/B tf32, A/B major (bit 15/16), N>>3, M>>4
+  args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (args.a_mn << 15) | (args.b_mn << 16) | ((BN >> 3) << 17) |
+               ((uint32_t)(BM >> 4) << 24);
   float* partial = nullptr;
   if (splits > 1) {
     partial = ctx->scratch_buf<float>("gemm_partial", (size_t)splits * M * N);
@@ -511,8 +564,8 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
     args.epi = epi;
     args.epi.partial = nullptr;
   }
-  CUtensorMap ta = make_map(A, M, K, lda, BM);
-  CUtensorMap tb = make_map(B, N, K, ldb, BN);
+  CUtensorMap ta = a.mn_major ? make_map_mn(A, M, K, lda) : make_map(A, M, K, lda, BM);
+  CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BN);
   static bool attr_set = false;
   if (!attr_set) {
     CG_CUDA(cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -534,6 +587,38 @@ void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint3
 }
 
 }  // namespace catgnn
+
+// General test hook: A is M x K (a_mn = 0) or K x M (a_mn = 1), B is N x K or
+// K x N, all host row-major; C = A . B^T in the logical (M x K).(N x K)^T sense.
+extern "C" int catgnn_gemm(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A, int a_mn,
+                           const float* B, int b_mn, float* Cout, uint32_t split_k, int precision) {
+  using namespace catgnn;
+  return guarded([&] {
+    if (!ctx) throw ConfigError("null context");
+    if (precision != 1 && precision != 3) throw ConfigError("precision must be 1 (TF32) or 3 (3xTF32)");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    auto upload = [&](const char* name, const float* h, uint32_t r, uint32_t c) {
+      const uint32_t ld = round_up(std::max(c, 1u), 4);
+      float* d = ctx->scratch_buf<float>(name, (size_t)std::max(r, 1u) * ld + 64);
+      CG_CUDA(cudaMemsetAsync(d, 0, ((size_t)std::max(r, 1u) * ld + 64) * 4, st));
+      if (r && c) CG_CUDA(cudaMemcpy2DAsync(d, ld * 4, h, c * 4, c * 4, r, cudaMemcpyHostToDevice, st));
+      return GemmOperand{d, ld, false};
+    };
+    GemmOperand ga = a_mn ? upload("g_A", A, K, M) : upload("g_A", A, M, K);
+    GemmOperand gb = b_mn ? upload("g_B", B, K, N) : upload("g_B", B, N, K);
+    ga.mn_major = a_mn != 0;
+    gb.mn_major = b_mn != 0;
+    const uint32_t ldc = round_up(N, 4);
+    float* dC = ctx->scratch_buf<float>("g_C", (size_t)std::max(M, 1u) * ldc);
+    GemmEpi e{};
+    e.out = dC;
+    e.ld_out = ldc;
+    gemm(ctx, ga, gb, M, N, K, e, split_k, precision);
+    CG_CUDA(cudaMemcpy2DAsync(Cout, N * 4, dC, ldc * 4, N * 4, M, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+  });
+}
 
 extern "C" int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
                               const float* B, float* Cout, uint32_t split_k, int precision) {

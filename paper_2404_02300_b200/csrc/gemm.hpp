@@ -23,6 +23,17 @@ struct GemmEpi {
 // ldb) K-major fp32 device matrices.  split_k = 0 picks a split automatically
 // (deterministic reduction in split order).  precision 1 = TF32 (inputs
 // truncated to 10 mantissa bits), 3 = 3xTF32 (hi*hi + hi*lo + lo*hi, ~fp32).
+// Operand of K3: row-major fp32 with row stride ld.  K-major: [M or N rows][K];
+// MN-major: [K rows][M or N] (read in place by the tensor core, no transpose).
+struct GemmOperand {
+  const float* ptr = nullptr;
+  uint32_t ld = 0;
+  bool mn_major = false;
+};
+
+void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, uint32_t K, const GemmEpi& epi,
+          uint32_t split_k = 1, int precision = 1);
+
 void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
              uint32_t N, uint32_t K, const GemmEpi& epi, uint32_t split_k = 1, int precision = 1);
 

@@ -20,7 +20,8 @@
 //   GIN  (eps = 0): as GCN with plain sums (no normalisation)
 // Backward uses the same CSR (A is symmetric, train.cpp:41-45 inserts both
 // directions) with the source-row scale applied as K2's `pre`, and the
-// weight gradients as split-K K3 GEMMs over transposed activations.
+// weight gradients as split-K K3 GEMMs that read the row-major activations as
+// MN-major tensor-core operands (no transposes).
 #include <nccl.h>
 
 #include <cmath>
@@ -445,13 +446,10 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
     const float* hprev = b.in;  // ReLU mask source for the previous layer
     float* dZprev = need_dx ? act(ctx, nm("dZ", li - 1), rows, L.K_in, false) : nullptr;
     if (sage && L.agg_first) {
-      // dW = dZ^T cat
-      float* dZt = act(ctx, "dZt", L.d_out, R4, false);
-      float* catT = act(ctx, "midT", b.mid_ld, R4, false);
-      transpose(ctx, dZ, dZ_ld, rows, L.d_out, dZt, R4);
-      transpose(ctx, b.mid, b.mid_ld, rows, b.mid_ld, catT, R4);
+      // dW = dZ^T cat (both operands read MN-major in place)
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dZt, R4, catT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
+      gemm(ctx, GemmOperand{dZ, dZ_ld, true}, GemmOperand{b.mid, b.mid_ld, true}, L.d_out, L.w_cols,
+           (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         float* dcat = act(ctx, "dmid", rows, b.mid_ld, false);
         GemmEpi e2; e2.out = dcat; e2.ld_out = b.mid_ld;
@@ -471,35 +469,18 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       a.in = dZ; a.in_ld = dZ_ld; a.pre = S->inv_deg.p;
       a.out = dP; a.out_ld = b.mid_ld; a.out_col = L.D_out; a.width = L.D_out; a.norm = kNormNone;
       aggregate(S, a);
-      float* dPt = act(ctx, "dZt", L.gemm_n, R4, false);
-      transpose(ctx, dP, b.mid_ld, rows, L.gemm_n, dPt, R4);
-      const float* hT = nullptr;
-      if (li == 0) {
-        if (!S->xT_valid || S->xT_ld != R4) {
-          S->xT.reserve((size_t)S->ld * R4);
-          transpose(ctx, S->x.p, S->ld, rows, S->ld, S->xT.p, R4);
-          S->xT_ld = R4;
-          S->xT_valid = true;
-        }
-        hT = S->xT.p;
-      } else {
-        float* t = act(ctx, "midT", b.in_ld, R4, false);
-        transpose(ctx, b.in, b.in_ld, rows, b.in_ld, t, R4);
-        hT = t;
-      }
+      // dW = dP^T H_prev (MN-major operands, no transposes)
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dPt, R4, hT, R4, L.gemm_n, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
+      gemm(ctx, GemmOperand{dP, b.mid_ld, true}, GemmOperand{b.in, b.in_ld, true}, L.gemm_n, L.w_cols,
+           (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
         gemm_tn(ctx, dP, b.mid_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1, kBwdPrecision);
       }
     } else if (L.agg_first) {  // GCN / GIN
-      float* dZt = act(ctx, "dZt", L.d_out, R4, false);
-      float* aT = act(ctx, "midT", b.mid_ld, R4, false);
-      transpose(ctx, dZ, dZ_ld, rows, L.d_out, dZt, R4);
-      transpose(ctx, b.mid, b.mid_ld, rows, b.mid_ld, aT, R4);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dZt, R4, aT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
+      gemm(ctx, GemmOperand{dZ, dZ_ld, true}, GemmOperand{b.mid, b.mid_ld, true}, L.d_out, L.w_cols,
+           (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         float* dA = act(ctx, "dmid", rows, L.K_in, false);
         GemmEpi e2; e2.out = dA; e2.ld_out = L.K_in;
@@ -516,24 +497,9 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       a.in = dZ; a.in_ld = dZ_ld; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
       a.out = dT; a.out_ld = L.D_out; a.width = L.D_out;
       aggregate(S, a);
-      float* dTt = act(ctx, "dZt", L.d_out, R4, false);
-      transpose(ctx, dT, L.D_out, rows, L.d_out, dTt, R4);
-      const float* hT = nullptr;
-      if (li == 0) {
-        if (!S->xT_valid || S->xT_ld != R4) {
-          S->xT.reserve((size_t)S->ld * R4);
-          transpose(ctx, S->x.p, S->ld, rows, S->ld, S->xT.p, R4);
-          S->xT_ld = R4;
-          S->xT_valid = true;
-        }
-        hT = S->xT.p;
-      } else {
-        float* t = act(ctx, "midT", b.in_ld, R4, false);
-        transpose(ctx, b.in, b.in_ld, rows, b.in_ld, t, R4);
-        hT = t;
-      }
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm_tn(ctx, dTt, R4, hT, R4, L.d_out, L.w_cols, (uint32_t)rows, e, 0, kBwdPrecision);
+      gemm(ctx, GemmOperand{dT, L.D_out, true}, GemmOperand{b.in, b.in_ld, true}, L.d_out, L.w_cols,
+           (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
         gemm_tn(ctx, dT, L.D_out, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);

@@ -53,6 +53,35 @@ def test_gemm_cancellation_needs_3xtf32(ctx):
     assert err3 < err1 / 50 and err3 < 1e-2, (err1, err3)
 
 
+def gemm_general(ctx, A, a_mn, B, b_mn, split=1, precision=1):
+    """A: M x K (a_mn=0) or K x M (a_mn=1); B: N x K or K x N."""
+    from paper_2404_02300_b200._lib import check, lib
+    A = np.ascontiguousarray(A, np.float32); B = np.ascontiguousarray(B, np.float32)
+    M = A.shape[1] if a_mn else A.shape[0]
+    K = A.shape[0] if a_mn else A.shape[1]
+    N = B.shape[1] if b_mn else B.shape[0]
+    out = np.zeros((M, N), np.float32)
+    check(lib.catgnn_gemm(ctx.handle, M, N, K, A.ctypes.data_as(C.c_void_p), int(a_mn),
+                          B.ctypes.data_as(C.c_void_p), int(b_mn), out.ctypes.data_as(C.c_void_p), split, precision))
+    return out
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(1, 1), (1, 0), (0, 1)])
+@pytest.mark.parametrize("M,N,K,split,prec", [(256, 604, 20000, 0, 3), (41, 256, 3000, 0, 1), (41, 256, 3000, 0, 3),
+                                              (128, 96, 64, 1, 1), (300, 33, 100, 1, 3), (16, 602, 999, 0, 1)])
+def test_gemm_mn_major(ctx, a_mn, b_mn, M, N, K, split, prec):
+    """Weight-gradient form C = X^T Y read from row-major activations (no transpose)."""
+    rng = np.random.default_rng(M + 3 * N + K)
+    A = rng.standard_normal((K, M) if a_mn else (M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N) if b_mn else (N, K)).astype(np.float32)
+    Al = A.T if a_mn else A
+    Bl = B.T if b_mn else B
+    want = Al.astype(np.float64) @ Bl.astype(np.float64).T
+    got = gemm_general(ctx, A, a_mn, B, b_mn, split, prec)
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < (2e-5 if prec == 3 else 1e-3), err
+
+
 def test_gemm_k_zero(ctx):
     A = np.zeros((5, 0), np.float32); B = np.zeros((16, 0), np.float32)
     assert np.all(gemm(ctx, A, B) == 0)
