@@ -94,12 +94,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
          (2ull << 61);
 }
 
-// MN-major SWIZZLE_128B (tf32): 32-element (128 B) atoms along M/N, 8 K-rows per
-// 1 KB swizzle atom; LBO = 4 KB between M/N atoms (one TMA box of 32 x 32 each),
-// SBO = 1 KB between K groups.  One MMA (K = 8) consumes exactly one K group.
+// MN-major tf32 operands use the SWIZZLE_128B_BASE32B layout (layout type 1:
+// 32-byte chunks swizzled within 128-byte rows, 4-row period; filled by TMA's
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 32-element (128 B) atoms along M/N,
+// LBO = 4 KB between M/N atoms (one 32 x 32 TMA box each), SBO = 512 B between
+// 4-row K groups; one MMA (K = 8) spans two K groups, so k-steps advance 1 KB.
 __device__ __forceinline__ uint64_t umma_desc_mn(uint32_t addr) {
-  return (uint64_t)((addr & 0x3FFFFu) >> 4) | (256ull << 16) | (64ull << 32) | (1ull << 46) |
-         (2ull << 61);
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | (256ull << 16) | (32ull << 32) | (1ull << 46) |
+         (1ull << 61);
 }
 
 // descriptor of k-step ks (K = 8 elements) of a stage tile in either layout
@@ -472,7 +474,7 @@ CUtensorMap make_map_mn(const float* ptr, uint64_t mn, uint64_t K, uint32_t ld) 
   cuuint32_t box[2] = {32, BK};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
-                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw InternalError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return m;
