@@ -190,6 +190,92 @@ __global__ void __launch_bounds__(256, 2) agg_kernel(const AggKernelArgs p) {
   }
 }
 
+// Narrow rows (width <= 64 floats): each group of LPN lanes owns one row of a
+// light unit (32/LPN rows in flight per warp) and walks it with its own
+// indices staged in shared memory — no cross-lane shuffles, no cross-group
+// reduction.  Chunks of split rows are shared by the groups of the warp and
+// reduced with xor shuffles as in agg_kernel.
+template <int VPL, int LPN, bool PRE>
+__global__ void __launch_bounds__(256, 3) agg_narrow_kernel(const AggKernelArgs p) {
+  constexpr int G = 32 / LPN;
+  constexpr int UNROLL = VPL >= 2 ? 4 : 8;
+  __shared__ int s_idx[8][G][32];
+  __shared__ float s_pre[8][G][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane / LPN, li = lane % LPN;
+  const unsigned gmask = (LPN == 32) ? 0xffffffffu : (((1u << LPN) - 1u) << (g * LPN));
+  int* sidx = s_idx[wib][g];
+  float* spre = s_pre[wib][g];
+  unsigned int u = 0;
+  if (lane == 0) u = atomicAdd(p.counter, 1u);
+  u = __shfl_sync(0xffffffffu, u, 0);
+  while (u < p.n_units) {
+    unsigned int next = 0;
+    if (lane == 0) next = atomicAdd(p.counter, 1u);
+    const int4 w = __ldg(p.units + u);
+    float4 acc[VPL];
+    if (w.z < 0) {
+      // light unit: rows w.x + g, w.x + g + G, ...  (group-uniform control flow)
+      for (int64_t r = w.x + g; r < w.y; r += G) {
+        const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t e = e0; e < e1; e += 32) {
+          const int n = (int)((e1 - e) < 32 ? (e1 - e) : 32);
+          for (int t = li; t < n; t += LPN) {
+            const int j = __ldg(p.col + e + t);
+            sidx[t] = j;
+            if (PRE) spre[t] = __ldg(p.pre + j);
+          }
+          __syncwarp(gmask);
+          for (int kb = 0; kb < n; kb += UNROLL) {
+            float4 v[UNROLL][VPL];
+            float s[UNROLL];
+#pragma unroll
+            for (int uu = 0; uu < UNROLL; ++uu) {
+              const int kk = kb + uu;
+              const bool ok = kk < n;
+              const int j = ok ? sidx[kk] : 0;
+              s[uu] = (PRE && ok) ? spre[kk] : 1.0f;
+              const float* src = p.in + (size_t)j * p.in_ld + p.in_col;
+#pragma unroll
+              for (int q = 0; q < VPL; ++q) {
+                const uint32_t c4 = li + LPN * q;
+                v[uu][q] = (ok && c4 < p.w4) ? ldg4(src + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
+#pragma unroll
+            for (int uu = 0; uu < UNROLL; ++uu)
+#pragma unroll
+              for (int q = 0; q < VPL; ++q) {
+                if (PRE) fma4(acc[q], s[uu], v[uu][q]);
+                else add4(acc[q], v[uu][q]);
+              }
+          }
+          __syncwarp(gmask);
+        }
+        epilogue_row<VPL, LPN>(p, r, (float)(e1 - e0), acc, li);
+      }
+    } else {
+      const int64_t r = w.x;
+      const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
+      const int64_t e0 = rb + (int64_t)w.y * p.U;
+      const int64_t e1 = (re < e0 + (int64_t)p.U) ? re : e0 + (int64_t)p.U;
+      gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
+      if (lane < LPN) {
+        float* dst = p.partials + (size_t)w.z * p.w4 * 4;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const uint32_t c4 = li + LPN * q;
+          if (c4 < p.w4) *reinterpret_cast<float4*>(dst + c4 * 4) = acc[q];
+        }
+      }
+    }
+    __syncwarp();
+    u = __shfl_sync(0xffffffffu, next, 0);
+  }
+}
+
 // One warp per split row: sum its chunk partials in chunk order, then the
 // same epilogue as a light row.
 template <int VPL>
@@ -242,6 +328,9 @@ AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
     switch (narrow_mode()) {
       case 1: *lpn_out = 8; return pick_pre<2, 8>(pre);
       case 2: *lpn_out = 4; return pick_pre<4, 4>(pre);
+      case 3: *lpn_out = 8; return pre ? agg_narrow_kernel<2, 8, true> : agg_narrow_kernel<2, 8, false>;
+      case 4: *lpn_out = 16; return pre ? agg_narrow_kernel<1, 16, true> : agg_narrow_kernel<1, 16, false>;
+      case 5: *lpn_out = 4; return pre ? agg_narrow_kernel<4, 4, true> : agg_narrow_kernel<4, 4, false>;
       default: *lpn_out = 16; return pick_pre<1, 16>(pre);
     }
   }

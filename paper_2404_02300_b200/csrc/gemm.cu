@@ -3,15 +3,19 @@
 //   C[M x N] = A[M x K] . B[N x K]^T        (A, B K-major fp32 in HBM, TF32 MMA,
 //                                            fp32 accumulation in TMEM)
 //
-// One CTA computes a 128 x BN tile (BN <= 256, multiple of 16) over a K range:
-//   warp 0      TMA producer: 128x32 and BNx32 fp32 boxes (128-byte rows,
-//               SWIZZLE_128B) into an S-stage shared-memory ring, completion on
-//               per-stage mbarriers (cp.async.bulk.tensor ... complete_tx)
+// Persistent CTAs (one per SM) walk 128 x BN output tiles (x split-K ranges):
+//   warp 0      TMA producer: operand tiles into an S-stage shared-memory ring
+//               (cp.async.bulk.tensor ... mbarrier::complete_tx).  K-major
+//               operands: one {32 x rows} SWIZZLE_128B box; MN-major operands
+//               (row-major activations read in place for weight gradients):
+//               {32 x 32} boxes in the SWIZZLE_128B_BASE32B layout
 //   warp 1      TMEM allocation + one elected thread issuing tcgen05.mma
-//               .cta_group::1.kind::tf32 (M=128, N=BN, K=8 per instruction,
-//               4 per 32-float k-block); tcgen05.commit frees each stage and
-//               finally signals the accumulator
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
+//               .cta_group::1.kind::tf32 (M=128, N=BN, K=8 per instruction)
+//               into one of two TMEM accumulators, so the epilogue of tile i
+//               overlaps the MMAs of tile i+1; tcgen05.commit frees stages
+//   warps 2..5  3xTF32 converters: lo = x - tf32(x) tiles next to each stage,
+//               MMA issues lo*hi + hi*lo + hi*hi (~fp32 accuracy)
+//   warps 6..9  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
 //               32*(w%4)..+31 = tile rows), fused row-scale / bias / ReLU /
 //               ReLU-backward mask, 128-bit stores — or raw split-K partials
 //               that gemm_reduce_kernel sums in split order (deterministic).

@@ -138,22 +138,46 @@ __global__ void argmax_correct_kernel(const float* __restrict__ Z, uint32_t ldz,
   }
 }
 
-// Column sums of rows x width (ld): per-block partials, then fixed-order reduce.
+// Column sums of rows x width (ld % 4 == 0): each block reduces a slab of rows
+// with float4 loads (tpr threads per row, 256/tpr rows in flight), partials
+// per block, then a fixed-order reduce — deterministic.
 __global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, uint64_t rows,
                                       uint32_t width, float* __restrict__ partial) {
+  __shared__ float4 red[256];
+  const uint32_t w4 = (width + 3) / 4;
   const uint64_t per = (rows + gridDim.x - 1) / gridDim.x;
   const uint64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
-  for (uint32_t c = threadIdx.x; c < width; c += blockDim.x) {
-    float acc = 0.f;
-    for (uint64_t r = r0; r < r1; ++r) acc += X[r * ld + c];
-    partial[(size_t)blockIdx.x * width + c] = acc;
+  const uint32_t tpr = min(w4, 256u), rpi = 256 / tpr;
+  const uint32_t c4 = threadIdx.x % tpr, rs = threadIdx.x / tpr;
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  const uint32_t ld4 = ld / 4;
+  for (uint32_t cb = 0; cb < w4; cb += tpr) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t c = cb + c4;
+    if (rs < rpi && c < w4)
+      for (uint64_t r = r0 + rs; r < r1; r += rpi) {
+        const float4 v = X4[r * ld4 + c];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (rs == 0 && c < w4) {
+      float4 s = red[c4];
+      for (uint32_t k = 1; k < rpi; ++k) {
+        const float4 v = red[k * tpr + c4];
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+      }
+      float* dst = partial + (size_t)blockIdx.x * w4 * 4 + c * 4;
+      dst[0] = s.x; dst[1] = s.y; dst[2] = s.z; dst[3] = s.w;
+    }
+    __syncthreads();
   }
 }
 __global__ void colsum_reduce_kernel(const float* __restrict__ partial, uint32_t blocks, uint32_t width,
-                                     float* __restrict__ out) {
+                                     uint32_t pstride, float* __restrict__ out) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
     float acc = 0.f;
-    for (uint32_t b = 0; b < blocks; ++b) acc += partial[(size_t)b * width + c];
+    for (uint32_t b = 0; b < blocks; ++b) acc += partial[(size_t)b * pstride + c];
     out[c] = acc;
   }
 }
@@ -320,11 +344,13 @@ void refresh_wT(catgnn_model_s* M) {
 }
 
 void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t width, float* out) {
-  const uint32_t blocks = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (rows + 1023) / 1024), 592);
-  float* part = ctx->scratch_buf<float>("colsum_part", (size_t)blocks * width);
+  if (ld % 4) throw ConfigError("column sum needs a row stride multiple of 4");
+  const uint32_t blocks = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (rows + 255) / 256), 592);
+  const uint32_t pstride = round_up(width, 4);
+  float* part = ctx->scratch_buf<float>("colsum_part", (size_t)blocks * pstride);
   colsum_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part);
   CG_CHECK_LAUNCH();
-  colsum_reduce_kernel<<<(width + 255) / 256, 256, 0, ctx->stream>>>(part, blocks, width, out);
+  colsum_reduce_kernel<<<(width + 255) / 256, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out);
   CG_CHECK_LAUNCH();
   ctx->launches += 2;
 }
