@@ -16,8 +16,10 @@ in-process across the rank's replicas and an NCCL all-reduce across ranks.
 Metric: edges aggregated per second = sum over partitions and aggregation
 passes of local nnz, per second of step time (max over ranks, CUDA events on
 the library's stream).  Inputs stay resident in HBM for `value`; `e2e`
-re-uploads every partition's features from pinned host memory through the
-C ABI each step and reads the loss back.
+re-uploads the global feature matrix from pinned host memory through the C
+ABI each step, gathers every partition's rows from it on the device (the
+reference's gather-from-global load path, train.cpp:277-283) and reads the
+loss back.
 """
 from __future__ import annotations
 
@@ -250,15 +252,17 @@ def main():
     mine = list(range(rank, w.partitions, world))
     X = np.load(os.path.join(prep["dir"], "features.npy"), mmap_mode="r")
     labels = np.load(os.path.join(prep["dir"], "labels.npy"))
-    shards, host_feats = [], []
+    shards = []
     t0 = time.time()
     for i in mine:
         p = W.load_part(prep, i, X, labels)
         s = gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx)
         shards.append(s)
-        pinned = torch.empty(p["features"].shape, dtype=torch.float32, pin_memory=True)
-        pinned.numpy()[:] = p["features"]
-        host_feats.append(pinned)
+    # e2e input: the global feature matrix in pinned host memory, refreshed into
+    # the device feature store every step; shards gather their rows from it
+    host_X = torch.empty(X.shape, dtype=torch.float32, pin_memory=True)
+    host_X.numpy()[:] = X
+    store = gp.FeatureStore(X.shape[0], X.shape[1], ctx) if not args.no_e2e else None
     log(f"[rank {rank}] {len(shards)} shards resident in {time.time() - t0:.1f}s")
     counts_all = meta["part_train"]
     alpha_all = sync_weights(counts_all)
@@ -292,9 +296,11 @@ def main():
 
     def step(e2e=False):
         losses = []
-        for r, s, hf in zip(reps, shards, host_feats):
+        if e2e:
+            store.upload(host_X.numpy())
+        for r, s in zip(reps, shards):
             if e2e:
-                s.upload_features(hf.numpy())
+                s.gather_features(store)
             losses.append(r.train_step(s, want_loss=e2e))
         state["it"] += 1
         if state["it"] % args.sync == 0:
@@ -374,17 +380,17 @@ def main():
             "achieved_tflops": gemm_flops / (kt["gemm_ms"] / args.steps / 1e3) / 1e12 if kt["gemm_ms"] else None,
             "peak_tflops_tf32": bf16 / 2, "peak_note": "dense TF32 = half the measured bf16 figure"}
 
-    # end-to-end through the C ABI: features re-uploaded from pinned host memory each step, loss read back
+    # end-to-end through the C ABI: global features re-uploaded from pinned host memory each step, loss read back
     e2e = None
     if not args.no_e2e:
         for _ in range(1):
             step(True)
         e2e_ms = timed(args.steps, e2e=True) / args.steps
-        h2d = sum(int(h.numel()) * 4 for h in host_feats) * world
+        h2d = int(host_X.numel()) * 4 * world
         e2e = {"value": edges_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
-               "path": "catgnn_shard_upload_features (pinned H2D) + catgnn_model_train_step per partition "
-                       "+ loss D2H + model averaging"}
+               "path": "catgnn_features_upload (global features, pinned H2D) + per partition "
+                       "catgnn_shard_gather_features + catgnn_model_train_step + loss D2H; model averaging"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

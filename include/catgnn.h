@@ -42,6 +42,7 @@ typedef struct catgnn_artifact_s* catgnn_artifact; /* host view of a stored arti
 typedef struct catgnn_shard_s* catgnn_shard;     /* device-resident shard (CSR, features, roles) */
 typedef struct catgnn_model_s* catgnn_model;     /* GNN replica: params + optimizer state */
 typedef struct catgnn_comm_s* catgnn_comm;       /* NCCL communicator (one rank per GPU) */
+typedef struct catgnn_features_s* catgnn_features; /* device copy of the global feature matrix */
 
 const char* catgnn_last_error(void);
 int catgnn_version(void);
@@ -113,6 +114,15 @@ int catgnn_shard_set_labels(catgnn_shard s, const int32_t* labels, const uint32_
                             const uint32_t* test_rows, uint64_t n_test);
 /* Re-upload features (host rows x dim) into the resident device buffer. */
 int catgnn_shard_upload_features(catgnn_shard s, const float* features, uint32_t dim);
+/* Global feature matrix on the device (rows x dim f32, FEA1 row order, dense):
+ * the source load_training_data gathers replica rows from when a partition has
+ * no features.bin (proj/src/train.cpp:277-283).  upload copies host rows
+ * [row_begin, row_begin+nrows) (pinned memory for full PCIe/C2C bandwidth);
+ * gather sets the shard's input rows x[r] = F[ext_id(r)] on the device. */
+int catgnn_features_create(catgnn_ctx ctx, uint64_t rows, uint32_t dim, catgnn_features* out);
+int catgnn_features_destroy(catgnn_features f);
+int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_begin, uint64_t nrows);
+int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f);
 typedef struct {
   uint64_t rows;
   uint64_t nnz;

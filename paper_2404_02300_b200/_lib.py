@@ -58,6 +58,10 @@ def _load():
         "catgnn_shard_destroy": (C.c_int, [vp]),
         "catgnn_shard_set_labels": (C.c_int, [vp, vp, vp, u64, vp, u64, vp, u64]),
         "catgnn_shard_upload_features": (C.c_int, [vp, vp, u32]),
+        "catgnn_features_create": (C.c_int, [vp, u64, u32, P(vp)]),
+        "catgnn_features_destroy": (C.c_int, [vp]),
+        "catgnn_features_upload": (C.c_int, [vp, vp, u64, u64]),
+        "catgnn_shard_gather_features": (C.c_int, [vp, vp]),
         "catgnn_shard_get_info": (C.c_int, [vp, vp]),
         "catgnn_csr_export": (C.c_int, [vp, vp, vp]),
         "catgnn_shard_role_rows": (C.c_int, [vp, C.c_int, vp]),

@@ -326,12 +326,12 @@ AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
   if (w4 <= 16) {
     // narrow rows: lanes per neighbour x float4 per lane
     switch (narrow_mode()) {
-      case 1: *lpn_out = 8; return pick_pre<2, 8>(pre);
+      case 1: *lpn_out = 16; return pick_pre<1, 16>(pre);
       case 2: *lpn_out = 4; return pick_pre<4, 4>(pre);
       case 3: *lpn_out = 8; return pre ? agg_narrow_kernel<2, 8, true> : agg_narrow_kernel<2, 8, false>;
       case 4: *lpn_out = 16; return pre ? agg_narrow_kernel<1, 16, true> : agg_narrow_kernel<1, 16, false>;
       case 5: *lpn_out = 4; return pre ? agg_narrow_kernel<4, 4, true> : agg_narrow_kernel<4, 4, false>;
-      default: *lpn_out = 16; return pick_pre<1, 16>(pre);
+      default: *lpn_out = 8; return pick_pre<2, 8>(pre);  // fastest on reddit_gcn (44-wide)
     }
   }
   *lpn_out = 32;

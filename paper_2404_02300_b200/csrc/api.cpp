@@ -100,7 +100,6 @@ void upload_features(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   s->ld = round_up(std::max<uint32_t>(dim, 1), 4);
   s->x.alloc(std::max<uint64_t>(1, s->rows) * s->ld);
   s->xprop.release();
-  s->xT_valid = false;
   if (s->rows == 0 || dim == 0) return;
   if (s->ld != dim) CG_CUDA(cudaMemsetAsync(s->x.p, 0, s->x.bytes(), s->ctx->stream));
   if (feats) copy_features_in(s, feats, dim);
@@ -509,8 +508,7 @@ int catgnn_shard_upload_features(catgnn_shard s, const float* features, uint32_t
       return;
     }
     if (s->rows && dim) copy_features_in(s, features, dim);
-    s->xT_valid = false;
-  });
+    });
 }
 
 int catgnn_shard_get_info(catgnn_shard s, catgnn_shard_info* info) {

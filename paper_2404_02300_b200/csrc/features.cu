@@ -1,0 +1,134 @@
+// Global feature store + per-shard row gather: the device form of
+// load_training_data's "features gathered from the global matrix" branch
+// (/root/reference/proj/src/train.cpp:277-283: X_i.row(r) = global.row(ext_r)).
+//
+// The global matrix lives on the device exactly as it lies in host memory
+// (rows x dim f32, dense, FEA1 row order) so a host->device refresh is one
+// contiguous pinned copy of |V|*dim*4 bytes instead of the RF-times larger
+// per-shard copies (reddit-shaped p=8: 0.6 GB vs 3.9 GB).  The gather writes
+// the shard's padded layout x[r][0..ld) with ld = round_up(dim, 4); padding
+// columns stay zero.  HBM-bound: rows*dim*4 read + rows*ld*4 written.
+#include <algorithm>
+
+#include "shard.hpp"
+
+struct catgnn_features_s {
+  catgnn_ctx ctx = nullptr;
+  uint64_t rows = 0;
+  uint32_t dim = 0;
+  catgnn::DevBuf<float> x;  // rows x dim, dense
+};
+
+namespace catgnn {
+namespace {
+
+// One warp per destination row.  Source rows are dim*4 bytes apart, so their
+// alignment is 16 B only when dim % 4 == 0 (float4 path); otherwise 8 B
+// (dim even: float2) or 4 B.
+template <int V>
+__global__ void __launch_bounds__(256) gather_rows_kernel(const float* __restrict__ src, uint32_t dim,
+                                                          const uint64_t* __restrict__ ext, uint64_t rows,
+                                                          float* __restrict__ dst, uint32_t ld) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t r = warp; r < rows; r += nwarps) {
+    const float* s = src + __ldg(ext + r) * dim;
+    float* d = dst + r * ld;
+    if (V == 4) {
+      for (uint32_t c = lane * 4; c < dim; c += 128)
+        *reinterpret_cast<float4*>(d + c) = __ldg(reinterpret_cast<const float4*>(s + c));
+    } else if (V == 2) {
+      for (uint32_t c = lane * 2; c < dim; c += 64)
+        *reinterpret_cast<float2*>(d + c) = __ldg(reinterpret_cast<const float2*>(s + c));
+    } else {
+      for (uint32_t c = lane; c < dim; c += 32) d[c] = __ldg(s + c);
+    }
+  }
+}
+
+void check_features(catgnn_features f) {
+  if (!f || !f->ctx) throw ConfigError("null feature store");
+}
+
+}  // namespace
+}  // namespace catgnn
+
+using namespace catgnn;
+
+int catgnn_features_create(catgnn_ctx ctx, uint64_t rows, uint32_t dim, catgnn_features* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw ConfigError("null argument");
+    if (dim == 0) throw ConfigError("feature width must be positive");
+    auto f = new catgnn_features_s();
+    f->ctx = ctx;
+    f->rows = rows;
+    f->dim = dim;
+    try {
+      CG_CUDA(cudaSetDevice(ctx->device));
+      f->x.alloc(std::max<uint64_t>(1, rows) * dim);
+    } catch (...) {
+      delete f;
+      throw;
+    }
+    ctx_retain(ctx);
+    *out = f;
+  });
+}
+
+int catgnn_features_destroy(catgnn_features f) {
+  return guarded([&] {
+    if (!f) return;
+    catgnn_ctx c = f->ctx;
+    delete f;
+    ctx_release(c);
+  });
+}
+
+int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_begin, uint64_t nrows) {
+  return guarded([&] {
+    check_features(f);
+    if (row_begin > f->rows || nrows > f->rows - row_begin) throw ConfigError("feature rows out of range");
+    if (nrows && !host) throw ConfigError("null argument");
+    if (!nrows) return;
+    CG_CUDA(cudaMemcpyAsync(f->x.p + row_begin * f->dim, host, nrows * f->dim * sizeof(float),
+                            cudaMemcpyHostToDevice, f->ctx->stream));
+  });
+}
+
+int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
+  return guarded([&] {
+    if (!s || !s->ctx) throw ConfigError("null shard");
+    check_features(f);
+    if (f->ctx != s->ctx) throw ConfigError("shard and feature store must share one context");
+    if (s->ext_ids.size() != s->rows)
+      throw ConfigError("shard has no replica map (create it from a partition)");
+    cudaStream_t st = s->ctx->stream;
+    if (s->rows && !s->d_ext.p) {
+      // the node table is ascending (completion.cpp:54-55), but do not rely on it here
+      s->ext_max = *std::max_element(s->ext_ids.begin(), s->ext_ids.end());
+      s->d_ext.alloc(s->rows);
+      CG_CUDA(cudaMemcpyAsync(s->d_ext.p, s->ext_ids.data(), s->rows * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (s->rows && s->ext_max >= f->rows)  // train.cpp:279-281
+      throw DataError("feature row " + std::to_string(s->ext_max) + " out of range of the feature store");
+    const uint32_t ld = round_up(f->dim, 4);
+    if (s->dim != f->dim || !s->x.p) {
+      s->dim = f->dim;
+      s->ld = ld;
+      s->x.alloc(std::max<uint64_t>(1, s->rows) * ld);
+      if (ld != f->dim) CG_CUDA(cudaMemsetAsync(s->x.p, 0, s->x.bytes(), st));
+    }
+    s->xprop.release();
+    if (!s->rows) return;
+    const unsigned grid = (unsigned)std::min<uint64_t>((s->rows + 7) / 8, (uint64_t)s->ctx->num_sms * 8);
+    if (f->dim % 4 == 0)
+      gather_rows_kernel<4><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
+    else if (f->dim % 2 == 0)
+      gather_rows_kernel<2><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
+    else
+      gather_rows_kernel<1><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
+    CG_CHECK_LAUNCH();
+    s->ctx->launches++;
+  });
+}

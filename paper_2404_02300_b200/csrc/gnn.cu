@@ -68,11 +68,14 @@ __device__ __forceinline__ float wmax(float v) {
 
 // K4: softmax cross-entropy over the train rows.  dZ[r] = (softmax(z_r) - onehot)
 // / n_train (rows not listed keep the caller's zeros); per-row loss for a
-// deterministic reduction.  Warp per row, lanes over classes.
+// deterministic reduction.  Warp per row, lanes over classes.  With rs, also
+// writes dZs[r] = rs[r] * dZ[r] (the GCN source scale D^-1/2 of the next
+// backward aggregation, so K2 needs no per-edge scale loads).
 __global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uint32_t C,
                                   const int32_t* __restrict__ labels, const uint32_t* __restrict__ rows,
                                   uint64_t n, float* __restrict__ dZ, uint32_t lddz,
-                                  double* __restrict__ row_loss) {
+                                  double* __restrict__ row_loss, const float* __restrict__ rs,
+                                  float* __restrict__ dZs) {
   const int lane = threadIdx.x & 31;
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -91,10 +94,12 @@ __global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uin
     }
     s = wsum(s);
     zy = wsum(zy);
+    const float sc = rs ? rs[r] : 0.f;
     for (uint32_t c = lane; c < C; c += 32) {
       float p = expf(z[c] - m) / s;
       if ((int)c == y) p -= 1.0f;
       dZ[(size_t)r * lddz + c] = p * inv_n;
+      if (rs) dZs[(size_t)r * lddz + c] = sc * (p * inv_n);
     }
     if (lane == 0) row_loss[i] = (double)m + log((double)s) - (double)zy;
   }
@@ -154,11 +159,25 @@ __global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, 
   for (uint32_t cb = 0; cb < w4; cb += tpr) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const uint32_t c = cb + c4;
-    if (rs < rpi && c < w4)
-      for (uint64_t r = r0 + rs; r < r1; r += rpi) {
-        const float4 v = X4[r * ld4 + c];
+    if (rs < rpi && c < w4) {
+      // 4 independent row loads in flight per thread, combined in a fixed order
+      float4 a1 = acc, a2 = acc, a3 = acc;
+      uint64_t r = r0 + rs;
+      for (; r + 3 * rpi < r1; r += 4 * rpi) {
+        const float4 v0 = __ldg(X4 + r * ld4 + c), v1 = __ldg(X4 + (r + rpi) * ld4 + c);
+        const float4 v2 = __ldg(X4 + (r + 2 * rpi) * ld4 + c), v3 = __ldg(X4 + (r + 3 * rpi) * ld4 + c);
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        a1.x += v1.x; a1.y += v1.y; a1.z += v1.z; a1.w += v1.w;
+        a2.x += v2.x; a2.y += v2.y; a2.z += v2.z; a2.w += v2.w;
+        a3.x += v3.x; a3.y += v3.y; a3.z += v3.z; a3.w += v3.w;
+      }
+      for (; r < r1; r += rpi) {
+        const float4 v = __ldg(X4 + r * ld4 + c);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
+      acc.x += a1.x + (a2.x + a3.x); acc.y += a1.y + (a2.y + a3.y);
+      acc.z += a1.z + (a2.z + a3.z); acc.w += a1.w + (a2.w + a3.w);
+    }
     red[threadIdx.x] = acc;
     __syncthreads();
     if (rs == 0 && c < w4) {
@@ -454,9 +473,17 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   double loss = 0.0;
   double* row_loss = ctx->scratch_buf<double>("row_loss", std::max<uint64_t>(1, ntr));
   double* loss_dev = ctx->scratch_buf<double>("loss_dev", 1);
+  // GCN transform-first: the last layer's backward aggregation gathers
+  // dinv * dZ, produced here by K4 instead of per edge in K2
+  float* dZs = nullptr;
+  if (gcn && !LL.agg_first) {
+    dZs = act(ctx, "dZs", rows, LL.D_out, false);
+    CG_CUDA(cudaMemsetAsync(dZs, 0, std::max<uint64_t>(1, rows) * LL.D_out * 4, st));
+  }
   if (ntr) {
     softmax_ce_kernel<<<grid1d(ntr * 32), 256, 0, st>>>(B[nl - 1].out, B[nl - 1].out_ld, LL.d_out,
-                                                      S->labels.p, S->d_train.p, ntr, dZ, LL.D_out, row_loss);
+                                                      S->labels.p, S->d_train.p, ntr, dZ, LL.D_out, row_loss,
+                                                      dZs ? S->dinv.p : nullptr, dZs);
     CG_CHECK_LAUNCH();
     sum_doubles_kernel<<<1, 256, 0, st>>>(row_loss, ntr, loss_dev);
     CG_CHECK_LAUNCH();
@@ -521,6 +548,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       float* dT = act(ctx, "dmid", rows, L.D_out, false);
       AggArgs a;
       a.in = dZ; a.in_ld = dZ_ld; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
+      if (li == nl - 1 && dZs) { a.in = dZs; a.pre = nullptr; }  // pre-scaled by K4
       a.out = dT; a.out_ld = L.D_out; a.width = L.D_out;
       aggregate(S, a);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;

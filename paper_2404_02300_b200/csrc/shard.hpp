@@ -36,9 +36,6 @@ struct catgnn_shard_s {
   // features
   uint32_t dim = 0, ld = 0;
   catgnn::DevBuf<float> x, xprop;
-  catgnn::DevBuf<float> xT;  // transposed input [ld][rows_pad] for the layer-1 dW GEMM
-  uint32_t xT_ld = 0;
-  bool xT_valid = false;
   // labels / roles (host copies + device copies)
   std::vector<int32_t> h_labels;
   std::vector<uint32_t> h_train, h_val, h_test;
@@ -48,6 +45,8 @@ struct catgnn_shard_s {
   // replica map (only for shards created from a partition)
   std::vector<uint64_t> ext_ids;
   std::vector<uint8_t> owner, role;
+  catgnn::DevBuf<uint64_t> d_ext;  // device copy of ext_ids (feature gathers)
+  uint64_t ext_max = 0;
 };
 
 namespace catgnn {

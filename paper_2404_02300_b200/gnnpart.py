@@ -37,7 +37,7 @@ __all__ = [
     "SyncPoint", "DistTrainResult", "ConfigError", "DataError", "InternalError", "build_adjacency",
     "sgc_propagate", "zero_params", "softmax_loss", "softmax_gradient", "train_epochs", "train_local",
     "sync_weights", "model_average", "evaluate_micro_f1", "load_training_data", "distributed_train",
-    "replication_factor", "default_context",
+    "replication_factor", "default_context", "FeatureStore",
 ]
 
 
@@ -226,6 +226,10 @@ class Shard:
         f = np.ascontiguousarray(features, np.float32)
         check(lib.catgnn_shard_upload_features(self.handle, _ptr(f), f.shape[1]))
 
+    def gather_features(self, store: "FeatureStore"):
+        """x[r] = F[ext_id(r)] on the device (train.cpp:277-283)."""
+        check(lib.catgnn_shard_gather_features(self.handle, store.handle))
+
     def role_rows(self, role: int) -> np.ndarray:
         inf = self.info
         n = {1: inf.n_train, 2: inf.n_val, 3: inf.n_test}[role]
@@ -259,6 +263,36 @@ class Shard:
     def close(self):
         if getattr(self, "handle", None):
             lib.catgnn_shard_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class FeatureStore:
+    """Device copy of the global feature matrix (rows x dim f32, FEA1 row
+    order) that shards gather their rows from by external id."""
+
+    def __init__(self, rows: int, dim: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.rows, self.dim = int(rows), int(dim)
+        h = C.c_void_p()
+        check(lib.catgnn_features_create(self.ctx.handle, self.rows, self.dim, C.byref(h)))
+        self.handle = h
+
+    def upload(self, features: np.ndarray, row_begin: int = 0):
+        f = features if (features.dtype == np.float32 and features.flags.c_contiguous) \
+            else np.ascontiguousarray(features, np.float32)
+        if f.ndim != 2 or f.shape[1] != self.dim:
+            raise ConfigError(f"feature rows must be {self.dim} wide")
+        check(lib.catgnn_features_upload(self.handle, _ptr(f), row_begin, f.shape[0]))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.catgnn_features_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

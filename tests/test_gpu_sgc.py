@@ -82,6 +82,31 @@ def test_golden_shards_csr_and_replica_map(gp, golden):
     assert np.array_equal(adj.neighbors, g["g_neighbors"])
 
 
+@pytest.mark.parametrize("dim", [8, 6, 5, 602])
+def test_feature_store_gather_matches_reference_gather(gp, golden, dim):
+    """Device gather from the global matrix == train.cpp:277-283 (X_i.row(r) =
+    global.row(ext_r)), bit-exact, for every source-row alignment."""
+    g = golden
+    rng = np.random.default_rng(dim)
+    n = int(g["num_nodes"])
+    X = rng.normal(size=(n, dim)).astype(np.float32)
+    store = gp.FeatureStore(n, dim)
+    store.upload(X[:100])
+    store.upload(X[100:], row_begin=100)
+    for s in range(int(g["config"][5])):
+        ext = g[f"p{s}_ext"]
+        sh = gp.Shard.from_part(ext, g[f"p{s}_owner"], g[f"p{s}_role"], g[f"s{s}_labels"],
+                                g[f"p{s}_edges"], np.zeros((ext.size, 3), np.float32))
+        sh.gather_features(store)
+        assert sh.info.dim == dim
+        assert np.array_equal(sh.features(), X[ext.astype(np.int64)])
+    small = gp.FeatureStore(int(ext.max()), dim)  # one row short of the last shard's ids
+    with pytest.raises(gp.DataError, match="out of range"):
+        sh.gather_features(small)
+    with pytest.raises(gp.ConfigError):
+        store.upload(X[:1], row_begin=n)
+
+
 def test_load_training_data_matches_reference(gp, small_artifact):
     data = gp.load_training_data(small_artifact)
     td = ref.TrainingData(small_artifact)
