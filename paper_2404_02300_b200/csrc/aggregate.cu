@@ -51,6 +51,7 @@ struct AggKernelArgs {
   int relu;
   const float* __restrict__ mask;
   uint32_t mask_ld, mask_col;
+  int legacy;  // 1: row-by-row light units (A/B baseline)
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -81,9 +82,11 @@ __device__ __forceinline__ float post_scale(int norm, float deg) {
 
 // Final epilogue for one output row.  `acc` holds the neighbour sum for the
 // float4 columns c4 = li + LPN*q.
+// selfv: the row's own input columns when already loaded (light units).
 template <int VPL, int LPN>
 __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, float deg,
-                                             const float4 (&acc)[VPL], int li) {
+                                             const float4 (&acc)[VPL], int li,
+                                             const float4 (*selfv)[VPL] = nullptr) {
   const float post = post_scale(p.norm, deg);
   const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
 #pragma unroll
@@ -91,7 +94,7 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
     const uint32_t c4 = li + LPN * q;
     if (c4 >= p.w4) continue;
     float4 a = acc[q];
-    if (p.self) fma4(a, selfs, ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4));
+    if (p.self) fma4(a, selfs, selfv ? (*selfv)[q] : ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4));
     a.x *= post; a.y *= post; a.z *= post; a.w *= post;
     if (p.residual) add4(a, ldg4(p.residual + (size_t)r * p.res_ld + p.res_col + c4 * 4));
     if (p.bias) add4(a, ldg4(p.bias + c4 * 4));
@@ -152,8 +155,101 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
     for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], m));
 }
 
+// A light unit (whole rows [r0, r1), edges contiguous in col[]) walked as one
+// edge stream: the column indices (and source scales) of the unit are held in
+// two 32-edge register chunks, the next chunk loaded while the current one is
+// consumed, so a row costs no dependent index load; row offsets are fetched
+// 32 rows per coalesced load and each row's own input row (self term) is
+// requested together with its first neighbour batch.  Per row the G lane
+// groups split the neighbours, UNROLL batches in flight, xor-shuffle reduce.
 template <int VPL, int LPN, bool PRE>
-__global__ void __launch_bounds__(256, 2) agg_kernel(const AggKernelArgs p) {
+__device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, int64_t r1, int lane) {
+  constexpr int G = 32 / LPN;
+  constexpr int UNROLL0 = VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8);
+  constexpr int UNROLL = G * UNROLL0 > 32 ? 32 / G : UNROLL0;
+  constexpr int B = G * UNROLL;  // neighbours per batch (<= 32)
+  static_assert(B <= 32, "batch must fit one index chunk");
+  const int g = lane / LPN, li = lane % LPN;
+  const bool writer = lane < LPN;
+  const int64_t E0 = __ldg(p.row_ptr + r0), E1 = __ldg(p.row_ptr + r1);
+  int64_t cb = E0;  // first edge of the current chunk
+  int cur = (cb + lane < E1) ? __ldg(p.col + cb + lane) : 0;
+  int nxt = (cb + 32 + lane < E1) ? __ldg(p.col + cb + 32 + lane) : 0;
+  float curs = 1.f, nxts = 1.f;
+  if (PRE) {
+    curs = (cb + lane < E1) ? __ldg(p.pre + cur) : 0.f;
+    nxts = (cb + 32 + lane < E1) ? __ldg(p.pre + nxt) : 0.f;
+  }
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    const int64_t rr = rb + lane;
+    const int64_t rpa = rr < r1 ? __ldg(p.row_ptr + rr) : 0;
+    const int64_t rpb = rr < r1 ? __ldg(p.row_ptr + rr + 1) : 0;
+    const int nr = (int)((r1 - rb) < 32 ? (r1 - rb) : 32);
+    for (int i = 0; i < nr; ++i) {
+      const int64_t r = rb + i;
+      const int64_t e0 = __shfl_sync(0xffffffffu, rpa, i), e1 = __shfl_sync(0xffffffffu, rpb, i);
+      float4 selfv[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const uint32_t c4 = li + LPN * q;
+        selfv[q] = (p.self && writer && c4 < p.w4) ? ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float4 acc[VPL];
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t e = e0; e < e1; e += B) {
+        while (e >= cb + 32) {  // warp-uniform: advance the index window by one chunk
+          cb += 32;
+          cur = nxt;
+          curs = nxts;
+          const bool ok = cb + 32 + lane < E1;
+          nxt = ok ? __ldg(p.col + cb + 32 + lane) : 0;
+          if (PRE) nxts = ok ? __ldg(p.pre + nxt) : 0.f;
+        }
+        float4 v[UNROLL][VPL];
+        float s[UNROLL];
+#pragma unroll
+        for (int uu = 0; uu < UNROLL; ++uu) {
+          const int64_t ee = e + uu * G + g;
+          const int off = (int)(ee - cb);  // < 32 + B <= 64
+          const int ja = __shfl_sync(0xffffffffu, cur, off & 31);
+          const int jb = __shfl_sync(0xffffffffu, nxt, off & 31);
+          const int j = off < 32 ? ja : jb;
+          if (PRE) {
+            const float sa = __shfl_sync(0xffffffffu, curs, off & 31);
+            const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
+            s[uu] = off < 32 ? sa : sb;
+          } else {
+            s[uu] = 1.f;
+          }
+          const bool ok = ee < e1;
+          const float* src = p.in + (size_t)j * p.in_ld + p.in_col;
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const uint32_t c4 = li + LPN * q;
+            v[uu][q] = (ok && c4 < p.w4) ? ldg4(src + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int uu = 0; uu < UNROLL; ++uu)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            if (PRE) fma4(acc[q], s[uu], v[uu][q]);
+            else add4(acc[q], v[uu][q]);
+          }
+      }
+#pragma unroll
+      for (int m = LPN; m < 32; m <<= 1)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], m));
+      if (writer) epilogue_row<VPL, LPN>(p, r, (float)(e1 - e0), acc, li, &selfv);
+    }
+  }
+}
+
+template <int VPL, int LPN, bool PRE, int MINB>
+__global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
   const int lane = threadIdx.x & 31;
   const int li = lane % LPN;
   const bool writer = lane < LPN;
@@ -165,7 +261,9 @@ __global__ void __launch_bounds__(256, 2) agg_kernel(const AggKernelArgs p) {
     if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
     const int4 w = __ldg(p.units + u);
     float4 acc[VPL];
-    if (w.z < 0) {
+    if (w.z < 0 && !p.legacy) {
+      light_unit<VPL, LPN, PRE>(p, w.x, w.y, lane);
+    } else if (w.z < 0) {
       for (int64_t r = w.x; r < w.y; ++r) {
         const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
         gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
@@ -186,92 +284,6 @@ __global__ void __launch_bounds__(256, 2) agg_kernel(const AggKernelArgs p) {
         }
       }
     }
-    u = __shfl_sync(0xffffffffu, next, 0);
-  }
-}
-
-// Narrow rows (width <= 64 floats): each group of LPN lanes owns one row of a
-// light unit (32/LPN rows in flight per warp) and walks it with its own
-// indices staged in shared memory — no cross-lane shuffles, no cross-group
-// reduction.  Chunks of split rows are shared by the groups of the warp and
-// reduced with xor shuffles as in agg_kernel.
-template <int VPL, int LPN, bool PRE>
-__global__ void __launch_bounds__(256, 3) agg_narrow_kernel(const AggKernelArgs p) {
-  constexpr int G = 32 / LPN;
-  constexpr int UNROLL = VPL >= 2 ? 4 : 8;
-  __shared__ int s_idx[8][G][32];
-  __shared__ float s_pre[8][G][32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int g = lane / LPN, li = lane % LPN;
-  const unsigned gmask = (LPN == 32) ? 0xffffffffu : (((1u << LPN) - 1u) << (g * LPN));
-  int* sidx = s_idx[wib][g];
-  float* spre = s_pre[wib][g];
-  unsigned int u = 0;
-  if (lane == 0) u = atomicAdd(p.counter, 1u);
-  u = __shfl_sync(0xffffffffu, u, 0);
-  while (u < p.n_units) {
-    unsigned int next = 0;
-    if (lane == 0) next = atomicAdd(p.counter, 1u);
-    const int4 w = __ldg(p.units + u);
-    float4 acc[VPL];
-    if (w.z < 0) {
-      // light unit: rows w.x + g, w.x + g + G, ...  (group-uniform control flow)
-      for (int64_t r = w.x + g; r < w.y; r += G) {
-        const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int64_t e = e0; e < e1; e += 32) {
-          const int n = (int)((e1 - e) < 32 ? (e1 - e) : 32);
-          for (int t = li; t < n; t += LPN) {
-            const int j = __ldg(p.col + e + t);
-            sidx[t] = j;
-            if (PRE) spre[t] = __ldg(p.pre + j);
-          }
-          __syncwarp(gmask);
-          for (int kb = 0; kb < n; kb += UNROLL) {
-            float4 v[UNROLL][VPL];
-            float s[UNROLL];
-#pragma unroll
-            for (int uu = 0; uu < UNROLL; ++uu) {
-              const int kk = kb + uu;
-              const bool ok = kk < n;
-              const int j = ok ? sidx[kk] : 0;
-              s[uu] = (PRE && ok) ? spre[kk] : 1.0f;
-              const float* src = p.in + (size_t)j * p.in_ld + p.in_col;
-#pragma unroll
-              for (int q = 0; q < VPL; ++q) {
-                const uint32_t c4 = li + LPN * q;
-                v[uu][q] = (ok && c4 < p.w4) ? ldg4(src + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-            }
-#pragma unroll
-            for (int uu = 0; uu < UNROLL; ++uu)
-#pragma unroll
-              for (int q = 0; q < VPL; ++q) {
-                if (PRE) fma4(acc[q], s[uu], v[uu][q]);
-                else add4(acc[q], v[uu][q]);
-              }
-          }
-          __syncwarp(gmask);
-        }
-        epilogue_row<VPL, LPN>(p, r, (float)(e1 - e0), acc, li);
-      }
-    } else {
-      const int64_t r = w.x;
-      const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
-      const int64_t e0 = rb + (int64_t)w.y * p.U;
-      const int64_t e1 = (re < e0 + (int64_t)p.U) ? re : e0 + (int64_t)p.U;
-      gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
-      if (lane < LPN) {
-        float* dst = p.partials + (size_t)w.z * p.w4 * 4;
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          const uint32_t c4 = li + LPN * q;
-          if (c4 < p.w4) *reinterpret_cast<float4*>(dst + c4 * 4) = acc[q];
-        }
-      }
-    }
-    __syncwarp();
     u = __shfl_sync(0xffffffffu, next, 0);
   }
 }
@@ -304,9 +316,16 @@ __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
 
 using AggFn = void (*)(const AggKernelArgs);
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 template <int VPL, int LPN>
 AggFn pick_pre(bool pre) {
-  return pre ? agg_kernel<VPL, LPN, true> : agg_kernel<VPL, LPN, false>;
+  static const int minb = env_int("CATGNN_AGG_MINB", 3);
+  if (minb >= 3) return pre ? agg_kernel<VPL, LPN, true, 3> : agg_kernel<VPL, LPN, false, 3>;
+  return pre ? agg_kernel<VPL, LPN, true, 2> : agg_kernel<VPL, LPN, false, 2>;
 }
 
 // Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
@@ -325,13 +344,15 @@ AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
   if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre); }
   if (w4 <= 16) {
     // narrow rows: lanes per neighbour x float4 per lane
-    switch (narrow_mode()) {
+    int mode = narrow_mode();
+    if (mode == 0) mode = w4 <= 12 ? 6 : 3;
+    switch (mode) {
       case 1: *lpn_out = 16; return pick_pre<1, 16>(pre);
       case 2: *lpn_out = 4; return pick_pre<4, 4>(pre);
-      case 3: *lpn_out = 8; return pre ? agg_narrow_kernel<2, 8, true> : agg_narrow_kernel<2, 8, false>;
-      case 4: *lpn_out = 16; return pre ? agg_narrow_kernel<1, 16, true> : agg_narrow_kernel<1, 16, false>;
-      case 5: *lpn_out = 4; return pre ? agg_narrow_kernel<4, 4, true> : agg_narrow_kernel<4, 4, false>;
-      default: *lpn_out = 8; return pick_pre<2, 8>(pre);  // fastest on reddit_gcn (44-wide)
+      case 6:
+        if (w4 <= 12) { *lpn_out = 4; return pick_pre<3, 4>(pre); }  // 8 neighbours per load
+        [[fallthrough]];
+      default: *lpn_out = 8; return pick_pre<2, 8>(pre);
     }
   }
   *lpn_out = 32;
@@ -412,6 +433,8 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.mask = a.mask;
     p.mask_ld = a.mask_ld;
     p.mask_col = a.mask_col + c4 * 4;
+    static const int legacy = env_int("CATGNN_AGG_LEGACY", 0);
+    p.legacy = legacy;
     int lpn = 32;
     AggFn fn = pick_kernel(w4, a.pre != nullptr, &lpn);
     const int bps = blocks_per_sm(fn);

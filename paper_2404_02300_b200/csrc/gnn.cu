@@ -105,12 +105,18 @@ __global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uin
   }
 }
 
-// Deterministic sum of n doubles (single block, fixed order per thread, tree).
-__global__ void sum_doubles_kernel(const double* __restrict__ v, uint64_t n, double* out) {
-  __shared__ double sh[256];
-  double acc = 0.0;
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) acc += v[i];
-  sh[threadIdx.x] = acc;
+// Deterministic sum of n doubles (single block of 1024, 4 loads in flight per
+// thread, fixed order per thread, tree).
+__global__ void __launch_bounds__(1024) sum_doubles_kernel(const double* __restrict__ v, uint64_t n, double* out) {
+  __shared__ double sh[1024];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const uint64_t T = blockDim.x;
+  uint64_t i = threadIdx.x;
+  for (; i + 3 * T < n; i += 4 * T) {
+    a0 += v[i]; a1 += v[i + T]; a2 += v[i + 2 * T]; a3 += v[i + 3 * T];
+  }
+  for (; i < n; i += T) a0 += v[i];
+  sh[threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
@@ -192,13 +198,16 @@ __global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, 
     __syncthreads();
   }
 }
+// One warp per column: lanes stride the block partials, then a fixed xor tree.
 __global__ void colsum_reduce_kernel(const float* __restrict__ partial, uint32_t blocks, uint32_t width,
                                      uint32_t pstride, float* __restrict__ out) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (uint32_t b = 0; b < blocks; ++b) acc += partial[(size_t)b * pstride + c];
-    out[c] = acc;
-  }
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= width) return;
+  float acc = 0.f;
+  for (uint32_t b = lane; b < blocks; b += 32) acc += partial[(size_t)b * pstride + c];
+  acc = wsum(acc);
+  if (lane == 0) out[c] = acc;
 }
 
 // K5: fused optimizer over the flat parameter vector.
@@ -282,6 +291,15 @@ float* act(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld, 
   return p;
 }
 
+// Row stride of a layer activation.  Narrow rows are padded to 16 floats
+// (64 B) so every gathered row starts on a sector pair and the 44-wide class
+// rows of the reddit shape become 48 = 4 lanes x 3 float4 (agg_kernel<3,4>).
+const bool kPad16 = [] {
+  const char* v = std::getenv("CATGNN_PAD16");
+  return !(v && v[0] == '0');  // default on; CATGNN_PAD16=0 for round-to-4 rows
+}();
+uint32_t act_width(uint32_t d) { return (kPad16 && d < 128) ? round_up(d, 16) : round_up(d, 4); }
+
 void plan_layers(catgnn_model_s* M) {
   const auto& c = M->cfg;
   M->layers.clear();
@@ -290,8 +308,8 @@ void plan_layers(catgnn_model_s* M) {
     Layer L;
     L.d_in = l == 0 ? c.in_dim : c.hidden;
     L.d_out = l + 1 == c.layers ? c.classes : c.hidden;
-    L.K_in = round_up(L.d_in, 4);
-    L.D_out = round_up(L.d_out, 4);
+    L.K_in = l == 0 ? round_up(L.d_in, 4) : act_width(L.d_in);  // layer 0 reads the shard's x
+    L.D_out = act_width(L.d_out);
     if (c.kind == CATGNN_MODEL_SAGE) {
       L.agg_first = L.d_in <= L.d_out;
       if (L.agg_first) {
@@ -369,7 +387,7 @@ void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t
   float* part = ctx->scratch_buf<float>("colsum_part", (size_t)blocks * pstride);
   colsum_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part);
   CG_CHECK_LAUNCH();
-  colsum_reduce_kernel<<<(width + 255) / 256, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out);
+  colsum_reduce_kernel<<<(width + 7) / 8, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out);
   CG_CHECK_LAUNCH();
   ctx->launches += 2;
 }
@@ -419,7 +437,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.w_cols, e, 1, kFwdPrecision);
     } else if (sage) {
-      b.mid_ld = round_up(L.gemm_n, 4);
+      b.mid_ld = 2 * L.D_out;  // [P_s (D_out, padded) | P_n (d_out) | zero padding]
       b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
       GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld;
       gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.gemm_n, L.K_in, e, 1, kFwdPrecision);
@@ -485,7 +503,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
                                                       S->labels.p, S->d_train.p, ntr, dZ, LL.D_out, row_loss,
                                                       dZs ? S->dinv.p : nullptr, dZs);
     CG_CHECK_LAUNCH();
-    sum_doubles_kernel<<<1, 256, 0, st>>>(row_loss, ntr, loss_dev);
+    sum_doubles_kernel<<<1, 1024, 0, st>>>(row_loss, ntr, loss_dev);
     CG_CHECK_LAUNCH();
     ctx->launches += 2;
   }

@@ -1,40 +1,36 @@
-"""K2 micro-benchmark: one SGC aggregation pass over an RMAT shard, kernel time
-from CUDA events on the launching stream, algorithmic GB/s."""
+"""K2 micro-benchmark on the bench workload's partition 0 (reddit_gcn, RMAT
+scale 18, SPRING p=8): one SGC-normalised aggregation pass (self term, no
+source scale) per width, kernel time from CUDA events on the launching stream,
+algorithmic GB/s per SURVEY §8(d).  Env: WIDTHS=256,44,48 REPS=10."""
 import json
 import os
 import sys
-import time
 
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2404_02300_b200 import gnnpart as gp, synth  # noqa: E402
+from paper_2404_02300_b200 import gnnpart as gp, workloads as W  # noqa: E402
 
-scale = int(os.environ.get("SCALE", 18))
-edges = int(os.environ.get("EDGES", 14_000_000))
-t0 = time.time()
-e, n, _ = synth.rmat_edges(scale, edges, seed=42)
-print(f"gen {time.time()-t0:.1f}s rows={n} edges={edges}", flush=True)
+w = W.WORKLOADS[os.environ.get("WORKLOAD", "reddit_gcn")]
+prep = W.prepare(w, lambda *a: None)
+part = W.load_part(prep, int(os.environ.get("PART", 0)))
+widths = [int(x) for x in os.environ.get("WIDTHS", "256,44,48").split(",")]
+reps = int(os.environ.get("REPS", 10))
 ctx = gp.Context(0)
 out = {}
-for width in [256, 48, 64, 604]:
-    x = np.random.default_rng(0).standard_normal((n, width), dtype=np.float32)
-    t0 = time.time()
-    s = gp.Shard.from_edges(n, e.astype(np.uint32), x, ctx)
+for width in widths:
+    x = np.random.default_rng(0).standard_normal((part["ext"].size, width), dtype=np.float32)
+    s = gp.Shard.from_part(part["ext"], part["owner"], part["role"], part["labels"], part["edges"], x, ctx)
     inf = s.info
-    build_s = time.time() - t0
     gp.sgc_propagate(s, 1)
     ctx.set_kernel_timing(True)
-    reps = 5
     for _ in range(reps):
         gp.lib.catgnn_sgc_propagate(s.handle, 1)
     kt = ctx.kernel_time()
-    ms = kt["agg_ms"] / reps
-    nnz = inf.nnz
-    ld = (width + 3) // 4 * 4
-    algo = nnz * (4 + 4 * ld) + n * (4 * ld * 2 + 8)
-    out[width] = dict(ms=ms, gbs=algo / ms / 1e6, nnz=nnz, heavy=inf.heavy_rows, units=inf.tasks, build_s=build_s)
-    print(width, out[width], flush=True)
     ctx.set_kernel_timing(False)
+    ms = kt["agg_ms"] / reps
+    n, nnz = inf.rows, inf.nnz
+    algo = nnz * (4 + 4 * width) + n * (4 * width * 2 + 8)
+    out[width] = dict(us=round(ms * 1e3, 1), algo_gbs=round(algo / ms / 1e6), nnz=nnz, rows=n)
     s.close()
-print(json.dumps(out))
+print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("CATGNN_")}, "k2": out}))
