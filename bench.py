@@ -262,7 +262,10 @@ def main():
     # the device feature store every step; shards gather their rows from it
     host_X = torch.empty(X.shape, dtype=torch.float32, pin_memory=True)
     host_X.numpy()[:] = X
-    store = gp.FeatureStore(X.shape[0], X.shape[1], ctx) if not args.no_e2e else None
+    # two device stores on a copy stream: step t+1's upload overlaps step t's
+    # work (the library orders uploads and gathers with events)
+    copy_ctx = gp.Context(local) if not args.no_e2e else None
+    stores = [gp.FeatureStore(X.shape[0], X.shape[1], copy_ctx) for _ in range(2)] if not args.no_e2e else None
     log(f"[rank {rank}] {len(shards)} shards resident in {time.time() - t0:.1f}s")
     counts_all = meta["part_train"]
     alpha_all = sync_weights(counts_all)
@@ -294,13 +297,16 @@ def main():
 
     state = {"it": 0}
 
-    def step(e2e=False):
+    def step(e2e=False, t=0, n=1):
         losses = []
         if e2e:
-            store.upload(host_X.numpy())
+            if t == 0:
+                stores[0].upload(host_X.numpy())
+            if t + 1 < n:  # prefetch the next step's inputs on the copy stream
+                stores[(t + 1) % 2].upload(host_X.numpy())
         for r, s in zip(reps, shards):
             if e2e:
-                s.gather_features(store)
+                s.gather_features(stores[t % 2])
             losses.append(r.train_step(s, want_loss=e2e))
         state["it"] += 1
         if state["it"] % args.sync == 0:
@@ -315,8 +321,8 @@ def main():
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         wall0 = time.perf_counter()
-        for _ in range(n):
-            step(e2e)
+        for t in range(n):
+            step(e2e, t, n)
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
@@ -383,14 +389,15 @@ def main():
     # end-to-end through the C ABI: global features re-uploaded from pinned host memory each step, loss read back
     e2e = None
     if not args.no_e2e:
-        for _ in range(1):
-            step(True)
+        for t in range(2):
+            step(True, t, 2)
         e2e_ms = timed(args.steps, e2e=True) / args.steps
         h2d = int(host_X.numel()) * 4 * world
         e2e = {"value": edges_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
-               "path": "catgnn_features_upload (global features, pinned H2D) + per partition "
-                       "catgnn_shard_gather_features + catgnn_model_train_step + loss D2H; model averaging"}
+               "path": "catgnn_features_upload (global features, pinned H2D on a copy stream, double-buffered: "
+                       "step t+1's copy overlaps step t) + per partition catgnn_shard_gather_features + "
+                       "catgnn_model_train_step + loss D2H; model averaging"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -118,7 +118,11 @@ int catgnn_shard_upload_features(catgnn_shard s, const float* features, uint32_t
  * the source load_training_data gathers replica rows from when a partition has
  * no features.bin (proj/src/train.cpp:277-283).  upload copies host rows
  * [row_begin, row_begin+nrows) (pinned memory for full PCIe/C2C bandwidth);
- * gather sets the shard's input rows x[r] = F[ext_id(r)] on the device. */
+ * gather sets the shard's input rows x[r] = F[ext_id(r)] on the device.
+ * The store may live on another context (stream) of the same device: uploads
+ * then run on that stream and are ordered against gathers by events (an upload
+ * waits for the previous contents' gathers), so two stores can double-buffer
+ * the host->device copy of the next step's features behind this step's work. */
 int catgnn_features_create(catgnn_ctx ctx, uint64_t rows, uint32_t dim, catgnn_features* out);
 int catgnn_features_destroy(catgnn_features f);
 int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_begin, uint64_t nrows);

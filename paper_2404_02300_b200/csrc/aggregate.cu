@@ -51,7 +51,6 @@ struct AggKernelArgs {
   int relu;
   const float* __restrict__ mask;
   uint32_t mask_ld, mask_col;
-  int legacy;  // 1: row-by-row light units (A/B baseline)
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -133,11 +132,10 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
         const int j = __shfl_sync(0xffffffffu, myj, kk & 31);
         s[u] = PRE ? __shfl_sync(0xffffffffu, mys, kk & 31) : 1.0f;
         const bool ok = kk < n;
-        const float* src = p.in + (size_t)j * p.in_ld + p.in_col;
 #pragma unroll
         for (int q = 0; q < VPL; ++q) {
           const uint32_t c4 = li + LPN * q;
-          v[u][q] = (ok && c4 < p.w4) ? ldg4(src + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u][q] = (ok && c4 < p.w4) ? ldg4(p.in + (size_t)j * p.in_ld + p.in_col + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
 #pragma unroll
@@ -224,11 +222,10 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             s[uu] = 1.f;
           }
           const bool ok = ee < e1;
-          const float* src = p.in + (size_t)j * p.in_ld + p.in_col;
 #pragma unroll
           for (int q = 0; q < VPL; ++q) {
             const uint32_t c4 = li + LPN * q;
-            v[uu][q] = (ok && c4 < p.w4) ? ldg4(src + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[uu][q] = (ok && c4 < p.w4) ? ldg4(p.in + (size_t)j * p.in_ld + p.in_col + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
 #pragma unroll
@@ -248,8 +245,10 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   }
 }
 
-template <int VPL, int LPN, bool PRE, int MINB>
-__global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
+// Persistent unit loop shared by both aggregation kernels: warps pull work
+// units from the atomic counter (the next one prefetched by lane 0).
+template <int VPL, int LPN, bool PRE>
+__device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
   const int lane = threadIdx.x & 31;
   const int li = lane % LPN;
   const bool writer = lane < LPN;
@@ -260,16 +259,10 @@ __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
     unsigned int next = 0;
     if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
     const int4 w = __ldg(p.units + u);
-    float4 acc[VPL];
-    if (w.z < 0 && !p.legacy) {
+    if (w.z < 0) {
       light_unit<VPL, LPN, PRE>(p, w.x, w.y, lane);
-    } else if (w.z < 0) {
-      for (int64_t r = w.x; r < w.y; ++r) {
-        const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
-        gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
-        if (writer) epilogue_row<VPL, LPN>(p, r, (float)(e1 - e0), acc, li);
-      }
     } else {
+      float4 acc[VPL];
       const int64_t r = w.x;
       const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
       const int64_t e0 = rb + (int64_t)w.y * p.U;
@@ -288,6 +281,11 @@ __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
   }
 }
 
+template <int VPL, int LPN, bool PRE, int MINB>
+__global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
+  unit_loop<VPL, LPN, PRE>(p);
+}
+
 // One warp per split row: sum its chunk partials in chunk order, then the
 // same epilogue as a light row.
 template <int VPL>
@@ -298,16 +296,44 @@ __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
   for (uint64_t h = wid; h < p.n_heavy; h += nw) {
     const int4 hv = __ldg(p.heavy + h);
     const int64_t r = hv.x;
-    float4 acc[VPL];
+    // chunk c goes to partial sum c % 4 (4 independent load chains; a hub row
+    // has ~100 chunks), combined in a fixed order: deterministic
+    float4 acc[VPL], acc4[3][VPL];
 #pragma unroll
-    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c = 0; c < hv.z; ++c) {
-      const float* src = p.partials + (size_t)(hv.y + c) * p.w4 * 4;
+    for (int q = 0; q < VPL; ++q) {
+      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc4[k][q] = acc[q];
+    }
+    const float* base = p.partials + (size_t)hv.y * p.w4 * 4;
+    const size_t cs = (size_t)p.w4 * 4;
+    int c = 0;
+    for (; c + 4 <= hv.z; c += 4) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const uint32_t c4 = lane + 32 * q;
-        if (c4 < p.w4) add4(acc[q], *reinterpret_cast<const float4*>(src + c4 * 4));
+        if (c4 < p.w4) {
+          const float* src = base + (size_t)c * cs + c4 * 4;
+          const float4 v0 = *reinterpret_cast<const float4*>(src);
+          const float4 v1 = *reinterpret_cast<const float4*>(src + cs);
+          const float4 v2 = *reinterpret_cast<const float4*>(src + 2 * cs);
+          const float4 v3 = *reinterpret_cast<const float4*>(src + 3 * cs);
+          add4(acc[q], v0); add4(acc4[0][q], v1); add4(acc4[1][q], v2); add4(acc4[2][q], v3);
+        }
       }
+    }
+    for (; c < hv.z; ++c) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const uint32_t c4 = lane + 32 * q;
+        if (c4 < p.w4) add4(acc[q], *reinterpret_cast<const float4*>(base + (size_t)c * cs + c4 * 4));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      add4(acc4[0][q], acc4[1][q]);
+      add4(acc4[0][q], acc4[2][q]);
+      add4(acc[q], acc4[0][q]);
     }
     const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
     epilogue_row<VPL, 32>(p, r, deg, acc, lane);
@@ -433,16 +459,14 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.mask = a.mask;
     p.mask_ld = a.mask_ld;
     p.mask_col = a.mask_col + c4 * 4;
-    static const int legacy = env_int("CATGNN_AGG_LEGACY", 0);
-    p.legacy = legacy;
     int lpn = 32;
     AggFn fn = pick_kernel(w4, a.pre != nullptr, &lpn);
+    CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
+    int t = ctx->begin_timed(0);
     const int bps = blocks_per_sm(fn);
     const uint64_t warps_needed = std::max<uint64_t>(1, s->n_units);
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)ctx->num_sms * bps, (warps_needed + 7) / 8));
-    CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
-    int t = ctx->begin_timed(0);
     fn<<<grid, 256, 0, ctx->stream>>>(p);
     CG_CHECK_LAUNCH();
     ctx->launches++;

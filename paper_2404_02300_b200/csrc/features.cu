@@ -9,14 +9,27 @@
 // the shard's padded layout x[r][0..ld) with ld = round_up(dim, 4); padding
 // columns stay zero.  HBM-bound: rows*dim*4 read + rows*ld*4 written.
 #include <algorithm>
+#include <map>
 
 #include "shard.hpp"
 
+// Uploads run on the store's context stream (a dedicated copy stream when the
+// store is created on its own context); gathers on the shard's stream.  Two
+// events order them without host syncs: a gather waits for the last upload,
+// an upload waits until every stream that gathered from the previous contents
+// is done — so a caller can double-buffer stores and copy step t+1's features
+// while step t computes.
 struct catgnn_features_s {
   catgnn_ctx ctx = nullptr;
   uint64_t rows = 0;
   uint32_t dim = 0;
   catgnn::DevBuf<float> x;  // rows x dim, dense
+  cudaEvent_t uploaded = nullptr;
+  std::map<cudaStream_t, cudaEvent_t> consumed;  // per consumer stream: last gather
+  ~catgnn_features_s() {
+    if (uploaded) cudaEventDestroy(uploaded);
+    for (auto& kv : consumed) cudaEventDestroy(kv.second);
+  }
 };
 
 namespace catgnn {
@@ -67,6 +80,7 @@ int catgnn_features_create(catgnn_ctx ctx, uint64_t rows, uint32_t dim, catgnn_f
     try {
       CG_CUDA(cudaSetDevice(ctx->device));
       f->x.alloc(std::max<uint64_t>(1, rows) * dim);
+      CG_CUDA(cudaEventCreateWithFlags(&f->uploaded, cudaEventDisableTiming));
     } catch (...) {
       delete f;
       throw;
@@ -91,8 +105,12 @@ int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_be
     if (row_begin > f->rows || nrows > f->rows - row_begin) throw ConfigError("feature rows out of range");
     if (nrows && !host) throw ConfigError("null argument");
     if (!nrows) return;
+    cudaStream_t st = f->ctx->stream;
+    for (auto& kv : f->consumed)
+      if (kv.first != st) CG_CUDA(cudaStreamWaitEvent(st, kv.second, 0));
     CG_CUDA(cudaMemcpyAsync(f->x.p + row_begin * f->dim, host, nrows * f->dim * sizeof(float),
-                            cudaMemcpyHostToDevice, f->ctx->stream));
+                            cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaEventRecord(f->uploaded, st));
   });
 }
 
@@ -100,7 +118,7 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
   return guarded([&] {
     if (!s || !s->ctx) throw ConfigError("null shard");
     check_features(f);
-    if (f->ctx != s->ctx) throw ConfigError("shard and feature store must share one context");
+    if (f->ctx->device != s->ctx->device) throw ConfigError("shard and feature store must share one device");
     if (s->ext_ids.size() != s->rows)
       throw ConfigError("shard has no replica map (create it from a partition)");
     cudaStream_t st = s->ctx->stream;
@@ -121,6 +139,7 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
     }
     s->xprop.release();
     if (!s->rows) return;
+    if (f->ctx->stream != st) CG_CUDA(cudaStreamWaitEvent(st, f->uploaded, 0));
     const unsigned grid = (unsigned)std::min<uint64_t>((s->rows + 7) / 8, (uint64_t)s->ctx->num_sms * 8);
     if (f->dim % 4 == 0)
       gather_rows_kernel<4><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
@@ -130,5 +149,10 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
       gather_rows_kernel<1><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
     CG_CHECK_LAUNCH();
     s->ctx->launches++;
+    if (f->ctx->stream != st) {
+      cudaEvent_t& ev = f->consumed[st];
+      if (!ev) CG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CG_CUDA(cudaEventRecord(ev, st));
+    }
   });
 }

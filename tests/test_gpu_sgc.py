@@ -82,15 +82,16 @@ def test_golden_shards_csr_and_replica_map(gp, golden):
     assert np.array_equal(adj.neighbors, g["g_neighbors"])
 
 
-@pytest.mark.parametrize("dim", [8, 6, 5, 602])
-def test_feature_store_gather_matches_reference_gather(gp, golden, dim):
+@pytest.mark.parametrize("dim,copy_stream", [(8, False), (6, False), (5, False), (602, False), (602, True)])
+def test_feature_store_gather_matches_reference_gather(gp, golden, dim, copy_stream):
     """Device gather from the global matrix == train.cpp:277-283 (X_i.row(r) =
-    global.row(ext_r)), bit-exact, for every source-row alignment."""
+    global.row(ext_r)), bit-exact, for every source-row alignment; also with
+    the store on its own copy stream (event-ordered upload -> gather)."""
     g = golden
     rng = np.random.default_rng(dim)
     n = int(g["num_nodes"])
     X = rng.normal(size=(n, dim)).astype(np.float32)
-    store = gp.FeatureStore(n, dim)
+    store = gp.FeatureStore(n, dim, gp.Context(0) if copy_stream else None)
     store.upload(X[:100])
     store.upload(X[100:], row_begin=100)
     for s in range(int(g["config"][5])):
