@@ -112,11 +112,15 @@ def agg_bytes(nnz, rows, width, self_term):
     return nnz * (4 + 4 * width) + rows * (4 * width * (1 + self_term) + 8)
 
 
-def load_ncu_traffic():
+def load_ncu_traffic(workload):
+    """ncu DRAM bytes per K2 launch for this workload (profiles/r01_k2_traffic.json,
+    written from the `ncu --set full` capture of the same bench command)."""
     p = os.path.join(ROOT, "profiles", "r01_k2_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f)
+            d = json.load(f)
+        if d.get("workload", "reddit_gcn") == workload:
+            return d
     return None
 
 
@@ -361,7 +365,7 @@ def main():
     hbm, bf16, src = peaks()
     achieved_gbs = algo_bytes / (agg_ms_step / 1e3) / 1e9 if agg_ms_step > 0 else None
     per_launch = kt["agg_launches"] / args.steps
-    ncu = load_ncu_traffic()
+    ncu = load_ncu_traffic(w.name)
     roofline = {"bound": "hbm", "kernel": "catgnn::agg_kernel (K2 neighbourhood aggregation)",
                 "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved_gbs / hbm) if achieved_gbs else None,

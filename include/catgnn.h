@@ -43,6 +43,7 @@ typedef struct catgnn_shard_s* catgnn_shard;     /* device-resident shard (CSR, 
 typedef struct catgnn_model_s* catgnn_model;     /* GNN replica: params + optimizer state */
 typedef struct catgnn_comm_s* catgnn_comm;       /* NCCL communicator (one rank per GPU) */
 typedef struct catgnn_features_s* catgnn_features; /* device copy of the global feature matrix */
+typedef struct catgnn_completion_s* catgnn_completion; /* per-partition edges + node tables */
 
 const char* catgnn_last_error(void);
 int catgnn_version(void);
@@ -143,6 +144,25 @@ int catgnn_shard_role_rows(catgnn_shard s, int role, uint32_t* rows);
 int catgnn_shard_labels(catgnn_shard s, int32_t* labels);
 /* which: 0 = input features, 1 = SGC-propagated features. */
 int catgnn_shard_export_features(catgnn_shard s, int which, float* out);
+
+/* --------------------------------------------- neighbour completion (A1) */
+/* complete_edges (proj/src/completion.cpp:130-171, PartitionBuilder :13-58) on
+ * the device: edges = 2 x num_edges external ids in stream order, which must be
+ * dense (every id in [0, num_nodes) a node of the stream, as
+ * load_training_data requires, train.cpp:234-240); home[v] = SPRING's home
+ * partition (HomeMap, completion.hpp:55-59); roles[v] = 0 none / 1 train /
+ * 2 val / 3 test or NULL.  hops in {1,2,3}.  Per partition: one record per
+ * unordered pair (first occurrence, original orientation, stream order) and the
+ * node table (ascending ext id, owner flag, role on owners only).  Errors as
+ * the reference: hops outside {1,2,3} -> 2, home out of range -> 3. */
+int catgnn_complete_edges(catgnn_ctx ctx, const uint64_t* edges, uint64_t num_edges, const uint32_t* home,
+                          const uint8_t* roles, uint64_t num_nodes, uint32_t p, uint32_t hops,
+                          catgnn_completion* out);
+int catgnn_completion_part_counts(catgnn_completion c, uint32_t part, uint64_t* edges, uint64_t* nodes,
+                                  uint64_t* owned);
+int catgnn_completion_part(catgnn_completion c, uint32_t part, uint64_t* edges, uint64_t* ext, uint8_t* owner,
+                           uint8_t* role);
+int catgnn_completion_destroy(catgnn_completion c);
 
 /* ---------------------------------------------------------- SGC path (A5-A13) */
 /* sgc_propagate (train.cpp:49-65): hops rounds of (x_i + sum_j x_j)/(1+deg_i),

@@ -62,6 +62,10 @@ def _load():
         "catgnn_features_destroy": (C.c_int, [vp]),
         "catgnn_features_upload": (C.c_int, [vp, vp, u64, u64]),
         "catgnn_shard_gather_features": (C.c_int, [vp, vp]),
+        "catgnn_complete_edges": (C.c_int, [vp, vp, u64, vp, vp, u64, u32, u32, P(vp)]),
+        "catgnn_completion_part_counts": (C.c_int, [vp, u32, P(u64), P(u64), P(u64)]),
+        "catgnn_completion_part": (C.c_int, [vp, u32, vp, vp, vp, vp]),
+        "catgnn_completion_destroy": (C.c_int, [vp]),
         "catgnn_shard_get_info": (C.c_int, [vp, vp]),
         "catgnn_csr_export": (C.c_int, [vp, vp, vp]),
         "catgnn_shard_role_rows": (C.c_int, [vp, C.c_int, vp]),

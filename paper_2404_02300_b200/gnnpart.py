@@ -37,7 +37,7 @@ __all__ = [
     "SyncPoint", "DistTrainResult", "ConfigError", "DataError", "InternalError", "build_adjacency",
     "sgc_propagate", "zero_params", "softmax_loss", "softmax_gradient", "train_epochs", "train_local",
     "sync_weights", "model_average", "evaluate_micro_f1", "load_training_data", "distributed_train",
-    "replication_factor", "default_context", "FeatureStore",
+    "replication_factor", "default_context", "FeatureStore", "GraphPartition", "complete_edges",
 ]
 
 
@@ -270,6 +270,48 @@ class Shard:
             self.close()
         except Exception:
             pass
+
+
+@dataclass
+class GraphPartition:
+    """GraphPartition (completion.hpp:31-34): edges (E x 2 ext ids, stream
+    order), node table (ascending ext ids, owner flags, roles)."""
+    edges: np.ndarray
+    ext: np.ndarray
+    owner: np.ndarray
+    role: np.ndarray
+
+    @property
+    def rows(self) -> int:
+        return int(self.ext.size)
+
+
+def complete_edges(edges, home, roles=None, partitions: Optional[int] = None, hops: int = 1,
+                   ctx: Optional[Context] = None) -> List[GraphPartition]:
+    """complete_edges (completion.cpp:130-171) on the device for a stream with
+    dense external ids; home = SPRING's node -> partition map."""
+    ctx = ctx or default_context()
+    e = np.ascontiguousarray(np.asarray(edges, np.uint64).reshape(-1, 2))
+    h = np.ascontiguousarray(home, np.uint32)
+    r = None if roles is None else np.ascontiguousarray(roles, np.uint8)
+    p = int(partitions if partitions is not None else (int(h.max()) + 1 if h.size else 0))
+    c = C.c_void_p()
+    check(lib.catgnn_complete_edges(ctx.handle, _ptr(e), e.shape[0], _ptr(h), _ptr(r), h.size, p, hops,
+                                    C.byref(c)))
+    try:
+        out = []
+        for s in range(p):
+            ne, nn = C.c_uint64(), C.c_uint64()
+            check(lib.catgnn_completion_part_counts(c, s, C.byref(ne), C.byref(nn), None))
+            pe = np.zeros((ne.value, 2), np.uint64)
+            ext = np.zeros(nn.value, np.uint64)
+            own = np.zeros(nn.value, np.uint8)
+            rl = np.zeros(nn.value, np.uint8)
+            check(lib.catgnn_completion_part(c, s, _ptr(pe), _ptr(ext), _ptr(own), _ptr(rl)))
+            out.append(GraphPartition(pe, ext, own, rl))
+        return out
+    finally:
+        lib.catgnn_completion_destroy(c)
 
 
 class FeatureStore:

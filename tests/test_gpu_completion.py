@@ -1,0 +1,69 @@
+"""GPU neighbour completion (csrc/completion.cu) against the reference's own
+complete_edges + write_partitions (oracle/_ref, the unmodified
+proj/src/completion.cpp): bit-exact edges (first occurrence per unordered pair,
+original orientation, stream order), node tables, owner flags and roles, for
+1/2/3 hops on streams with duplicate and reversed records."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ref
+from test_synth import read_part
+
+pytestmark = pytest.mark.gpu
+
+
+def dup_stream(tmp, scale, edges, seed, classes=4):
+    from paper_2404_02300_b200 import synth
+    e, n, _ = synth.rmat_edges(scale, edges, seed=seed)
+    rng = np.random.default_rng(seed)
+    extra = e[rng.choice(e.shape[0], e.shape[0] // 5, replace=False)].copy()
+    flip = rng.random(extra.shape[0]) < 0.5
+    extra[flip] = extra[flip][:, ::-1]                 # reversed duplicates
+    stream = np.concatenate([e, extra])
+    stream = stream[rng.permutation(stream.shape[0])]  # duplicates before/after originals
+    lab, roles = synth.node_meta(n, classes, 0.6, 0.2, 0.2, seed=seed)
+    X = synth.class_features(lab, 4, classes, seed=seed)
+    d = os.path.join(str(tmp), f"dup_{scale}_{edges}_{seed}")
+    synth.write_dataset(d, stream, lab, roles, X)
+    return dict(dir=d, edges=stream, n=n, roles=roles, edge_file=os.path.join(d, "edges.bin"),
+                nodes_file=os.path.join(d, "nodes.tsv"))
+
+
+@pytest.mark.parametrize("p,hops,scale,edges,seed", [(2, 1, 10, 3000, 1), (4, 1, 12, 20000, 2),
+                                                     (8, 1, 12, 30000, 3), (4, 2, 11, 6000, 4),
+                                                     (3, 3, 10, 2500, 5), (1, 1, 9, 800, 6)])
+def test_device_completion_matches_reference(tmp_path, p, hops, scale, edges, seed):
+    from paper_2404_02300_b200 import gnnpart as gp
+    ds = dup_stream(tmp_path, scale, edges, seed)
+    art = os.path.join(ds["dir"], f"art_p{p}_h{hops}")
+    ref.partition(ds["edge_file"], art, p, nodes=ds["nodes_file"], hops=hops)
+    ref_parts = [read_part(art, s) for s in range(p)]
+    home = np.full(ds["n"], p, np.uint32)
+    for s, (_, ext, own, _) in enumerate(ref_parts):
+        home[ext[own == 1].astype(np.int64)] = s
+    assert np.all(home < p)
+    parts = gp.complete_edges(ds["edges"], home, ds["roles"], p, hops=hops)
+    for s in range(p):
+        edges, ext, own, role = ref_parts[s]
+        assert np.array_equal(parts[s].edges, edges), s
+        assert np.array_equal(parts[s].ext, ext), s
+        assert np.array_equal(parts[s].owner, own), s
+        assert np.array_equal(parts[s].role, role), s
+    rf, _ = ref.artifact_replication_factor(art)
+    assert sum(pt.rows for pt in parts) / ds["n"] == rf
+
+
+def test_device_completion_errors():
+    from paper_2404_02300_b200 import gnnpart as gp
+    e = np.array([[0, 1], [1, 2]], np.uint64)
+    with pytest.raises(gp.ConfigError, match="hop count"):
+        gp.complete_edges(e, np.zeros(3, np.uint32), None, 1, hops=4)
+    with pytest.raises(gp.DataError, match="home partition out of range"):
+        gp.complete_edges(e, np.array([0, 1, 2], np.uint32), None, 2)
+    with pytest.raises(gp.DataError, match="dense"):
+        gp.complete_edges(np.array([[0, 5]], np.uint64), np.zeros(3, np.uint32), None, 1)
+    # isolated owned node: present in its home's table without edges (completion.cpp:37)
+    parts = gp.complete_edges(e, np.array([0, 0, 0, 1], np.uint32), None, 2)
+    assert parts[1].ext.tolist() == [3] and parts[1].owner.tolist() == [1] and parts[1].edges.shape == (0, 2)
