@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.hpp"
@@ -46,6 +47,7 @@ struct GemmArgs {
   uint32_t split3;  // 1: 3xTF32 (hi*hi + hi*lo + lo*hi), 0: plain TF32
   uint32_t mt, nt, splits, tiles;
   uint32_t a_mn, b_mn;  // operand stored MN-major ([K rows][M or N cols] row-major)
+  uint32_t bm;          // tile rows: BM x CTAs per tile
   GemmEpi epi;
 };
 
@@ -133,9 +135,45 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
+}
+// CTA pair: arrive on the barrier at this offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+template <int NCTA>
+__device__ __forceinline__ void commit_to(uint32_t bar) {
+  if (NCTA == 2) mma_commit_pair(bar);
+  else mma_commit(bar);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at local offset `bar` in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cta(uint32_t bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(bar), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -174,7 +212,7 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, uint32_t t, uint3
                                             uint32_t& kb0, uint32_t& nkb) {
   // n fastest: CTAs working on the same M block at the same time share A in L2
   const uint32_t n = t % a.nt, m = (t / a.nt) % a.mt, z = t / (a.nt * a.mt);
-  m0 = m * BM;
+  m0 = m * a.bm;
   n0 = n * a.BN;
   const uint32_t nkb_total = (a.K + BK - 1) / BK;
   kb0 = z * a.kb_per_split;
@@ -215,20 +253,28 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Persistent warp-specialised kernel (one CTA per SM):
-//   warp 0     TMA producer over every tile's k-blocks (S-stage ring)
-//   warp 1     TMEM allocator + MMA issuer; accumulators double-buffered in
-//              TMEM (2 x acc_cols columns) so tile i's epilogue overlaps tile
-//              i+1's MMAs
-//   warps 2-5  3xTF32 converters (lo = x - tf32(x) tiles), idle otherwise
+// Persistent warp-specialised kernel (one CTA per SM; NCTA = 2: CTA pairs on
+// the two SMs of a TPC, cta_group::2, 256-row tiles):
+//   warp 0     TMA producer over every tile's k-blocks (S-stage ring); in a
+//              pair each CTA loads its own 128 rows of A and its half of B
+//   warp 1     TMEM allocator + MMA issuer (the pair's rank-0 CTA only);
+//              accumulators double-buffered in TMEM (2 x acc_cols columns) so
+//              tile i's epilogue overlaps tile i+1's MMAs
+//   warps 2-5  3xTF32 converters (lo = x - tf32(x) tiles); in a pair they also
+//              relay "stage ready" to the rank-0 CTA's barrier
 //   warps 6-9  epilogue: tcgen05.ld -> fused epilogue -> 128-bit stores
+// Pair protocol: full[s] / empty[s] are per CTA (local TMA, multicast MMA
+// commit); conv[s] and tempty[b] live in the rank-0 CTA and count the arrivals
+// of both CTAs' converter / epilogue warps; tfull[b] is multicast.
+template <int NCTA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t BN = args.BN;
-  const uint32_t B_STAGE = BN * BK * 4;
+  const uint32_t BNh = BN / NCTA;  // B rows (N) held by this CTA
+  const uint32_t B_STAGE = BNh * BK * 4;
   const uint32_t S = args.stages;
   const bool split3 = args.split3 != 0;
   uint8_t* sA = smem;
@@ -243,28 +289,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = NCTA == 2 ? cluster_rank() : 0;
+  const uint32_t cid = blockIdx.x / NCTA, ncl = gridDim.x / NCTA;  // pair index / count
+  // stage-ready signal the MMA waits on: the TMA barrier itself for a single
+  // CTA in plain TF32, else the converters' (relay) barrier
+  const bool via_conv = split3 || NCTA == 2;
 
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < S; ++i) {
       mbar_init(smem_u32(full + i), 1);
       mbar_init(smem_u32(empty + i), 1);
-      mbar_init(smem_u32(conv + i), 4);
+      mbar_init(smem_u32(conv + i), 4 * NCTA);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(tfull + b), 1);
-      mbar_init(smem_u32(tempty + b), 4);
+      mbar_init(smem_u32(tempty + b), 4 * NCTA);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(args.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (NCTA == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(args.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(args.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (NCTA == 2) cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_holder;
   const uint32_t acc_cols = args.tmem_cols / 2;
@@ -273,23 +331,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t bytes = A_STAGE + B_STAGE;
       uint32_t it = 0;
-      for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+      for (uint32_t t = cid; t < args.tiles; t += ncl) {
         uint32_t m0, n0, kb0, nkb;
         tile_coords(args, t, m0, n0, kb0, nkb);
+        m0 += crank * BM;
+        n0 += crank * BNh;
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           mbar_expect_tx(smem_u32(full + s), bytes);
           const int kx = (int)((kb0 + i) * BK);
           load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s));
-          load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BN, smem_u32(full + s));
+          load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s));
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {
       uint32_t it = 0, j = 0;
-      for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++j) {
+      for (uint32_t t = cid; t < args.tiles; t += ncl, ++j) {
         uint32_t m0, n0, kb0, nkb;
         tile_coords(args, t, m0, n0, kb0, nkb);
         const uint32_t b = j & 1;
@@ -299,47 +359,65 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool amn = args.a_mn != 0, bmn = args.b_mn != 0;
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
-          mbar_wait(smem_u32(split3 ? conv + s : full + s), ph);
+          mbar_wait(smem_u32(via_conv ? conv + s : full + s), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
           const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
-          if (split3) {
-            const uint32_t al = smem_u32(sAl + (size_t)s * A_STAGE);
-            const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
+          const uint32_t al = smem_u32(sAl + (size_t)s * A_STAGE);
+          const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
 #pragma unroll
-            for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first
-              mma_tf32(acc, op_desc(al, ks, amn), op_desc(b0, ks, bmn), args.idesc, (i > 0 || ks > 0) ? 1u : 0u);
-              mma_tf32(acc, op_desc(a0, ks, amn), op_desc(bl, ks, bmn), args.idesc, 1u);
-              mma_tf32(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, 1u);
+          for (int ks = 0; ks < BK / 8; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
+            const uint32_t first = (i > 0 || ks > 0) ? 1u : 0u;
+            if (NCTA == 2) {
+              if (split3) {  // small terms first
+                mma_tf32_pair(acc, op_desc(al, ks, amn), op_desc(b0, ks, bmn), args.idesc, first);
+                mma_tf32_pair(acc, op_desc(a0, ks, amn), op_desc(bl, ks, bmn), args.idesc, 1u);
+                mma_tf32_pair(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, 1u);
+              } else {
+                mma_tf32_pair(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, first);
+              }
+            } else {
+              if (split3) {
+                mma_tf32(acc, op_desc(al, ks, amn), op_desc(b0, ks, bmn), args.idesc, first);
+                mma_tf32(acc, op_desc(a0, ks, amn), op_desc(bl, ks, bmn), args.idesc, 1u);
+                mma_tf32(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, 1u);
+              } else {
+                mma_tf32(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, first);
+              }
             }
-          } else {
-#pragma unroll
-            for (int ks = 0; ks < BK / 8; ++ks)  // K = 8 tf32 (32 bytes) per instruction
-              mma_tf32(acc, op_desc(a0, ks, amn), op_desc(b0, ks, bmn), args.idesc, (i > 0 || ks > 0) ? 1u : 0u);
           }
-          mma_commit(smem_u32(empty + s));
+          commit_to<NCTA>(smem_u32(empty + s));
         }
-        if (nkb) mma_commit(smem_u32(tfull + b));
-        else mbar_arrive(smem_u32(tfull + b));  // empty K range: epilogue writes zeros
+        if (nkb) {
+          commit_to<NCTA>(smem_u32(tfull + b));
+        } else {  // empty K range: the epilogue writes zeros
+          mbar_arrive(smem_u32(tfull + b));
+          if (NCTA == 2) mbar_arrive_cta(smem_u32(tfull + b), 1);
+        }
       }
     }
     __syncwarp();
   } else if (warp < 6) {
-    if (split3) {
+    if (via_conv) {
       const uint32_t tt = threadIdx.x - 64;
       const uint32_t a4 = A_STAGE / 16, b4 = B_STAGE / 16;
       uint32_t it = 0;
-      for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+      for (uint32_t t = cid; t < args.tiles; t += ncl) {
         uint32_t m0, n0, kb0, nkb;
         tile_coords(args, t, m0, n0, kb0, nkb);
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(smem_u32(full + s), ph);
-          convert_tile(smem_u32(sA + (size_t)s * A_STAGE), smem_u32(sAl + (size_t)s * A_STAGE), a4, tt);
-          convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)s * B_STAGE), b4, tt);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (split3) {
+            convert_tile(smem_u32(sA + (size_t)s * A_STAGE), smem_u32(sAl + (size_t)s * A_STAGE), a4, tt);
+            convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)s * B_STAGE), b4, tt);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          }
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(conv + s));
+          if (lane == 0) {
+            if (NCTA == 2) mbar_arrive_cta(smem_u32(conv + s), 0);
+            else mbar_arrive(smem_u32(conv + s));
+          }
         }
       }
     }
@@ -347,9 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const GemmEpi& e = args.epi;
     uint32_t j = 0;
-    for (uint32_t t = blockIdx.x; t < args.tiles; t += gridDim.x, ++j) {
+    for (uint32_t t = cid; t < args.tiles; t += ncl, ++j) {
       uint32_t m0, n0, kb0, nkb;
       tile_coords(args, t, m0, n0, kb0, nkb);
+      m0 += crank * BM;
       const uint32_t b = j & 1;
       mbar_wait(smem_u32(tfull + b), (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -411,14 +490,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(tempty + b));
+      if (lane == 0) {
+        if (NCTA == 2) mbar_arrive_cta(smem_u32(tempty + b), 0);
+        else mbar_arrive(smem_u32(tempty + b));
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (NCTA == 2) cluster_sync();  // the peer's MMAs / remote arrivals are done
+  else __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(args.tmem_cols));
+    if (NCTA == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(args.tmem_cols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(args.tmem_cols));
   }
 }
 __global__ void gemm_reduce_kernel(const float* __restrict__ partial, uint32_t splits, uint32_t M,
@@ -515,18 +601,30 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     return;
   }
   const bool split3 = precision == 3;
-  // 3xTF32 doubles the stage (lo tiles): 128-wide N tiles keep 3 stages in flight
-  const uint32_t bn_max = split3 ? 128 : 256;
-  // MN-major B is loaded in 32-wide atoms
-  const uint32_t BN = N >= bn_max ? bn_max : round_up(N, b.mn_major ? 32 : 16);
+  // CTA pairs (cta_group::2, 256-row tiles) halve each SM's operand traffic —
+  // the SMEM port, not the tensor pipe, bounds the 3xTF32 main loop
+  static const int pair_env = [] {
+    const char* v = std::getenv("CATGNN_GEMM_PAIR");
+    return v ? std::atoi(v) : 1;
+  }();
+  const bool pair = pair_env != 0 && M >= 256;
+  const uint32_t ncta = pair ? 2 : 1;
+  // 3xTF32 doubles the stage (lo tiles): single-CTA 128-wide N tiles keep 3 stages in flight
+  const uint32_t bn_max = (split3 && !pair) ? 128 : 256;
+  // per-CTA B rows must be whole 8-row swizzle groups (K-major) or 32-wide atoms (MN-major)
+  const uint32_t bn_q = (b.mn_major ? 32 : 16) * ncta;
+  const uint32_t BN = N >= bn_max ? bn_max : round_up(N, bn_q);
+  const uint32_t BNh = BN / ncta;
   const uint32_t nkb = (K + BK - 1) / BK;
-  const uint32_t mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
+  const uint32_t bm = BM * ncta;
+  const uint32_t mt = (M + bm - 1) / bm, nt = (N + BN - 1) / BN;
+  const uint32_t units = (uint32_t)ctx->num_sms / ncta;  // persistent CTAs (pairs)
   uint32_t splits = 1;
   if (split_k == 0) {
     // fill the SMs when the tile grid is small and K is long
     const uint32_t tiles = mt * nt;
-    if (tiles < (uint32_t)ctx->num_sms && nkb >= 8)
-      splits = std::min<uint32_t>(std::max<uint32_t>(1, (uint32_t)ctx->num_sms / tiles), nkb / 4);
+    if (tiles < units && nkb >= 8)
+      splits = std::min<uint32_t>(std::max<uint32_t>(1, units / tiles), nkb / 4);
   } else {
     splits = std::min<uint32_t>(split_k, std::max<uint32_t>(1, nkb));
   }
@@ -536,7 +634,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   if ((epi.mask && (epi.mask_ld % 4 || epi.mask_col % 4)) || (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15)))
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
-  const uint32_t b_stage = BN * BK * 4;
+  const uint32_t b_stage = BNh * BK * 4;
   const size_t stage_bytes = (size_t)(A_STAGE + b_stage) * (split3 ? 2 : 1);
   const size_t budget = 227 * 1024 - 1024 - 512;
   uint32_t stages = (uint32_t)std::min<size_t>(6, budget / stage_bytes);
@@ -558,9 +656,10 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   args.tiles = mt * nt * splits;
   args.a_mn = a.mn_major ? 1u : 0u;
   args.b_mn = b.mn_major ? 1u : 0u;
+  args.bm = bm;
   // instruction descriptor: D f32, A/B tf32, A/B major (bit 15/16), N>>3, M>>4
   args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (args.a_mn << 15) | (args.b_mn << 16) | ((BN >> 3) << 17) |
-               ((uint32_t)(BM >> 4) << 24);
+               ((bm >> 4) << 24);
   float* partial = nullptr;
   if (splits > 1) {
     partial = ctx->scratch_buf<float>("gemm_partial", (size_t)splits * M * N);
@@ -571,15 +670,32 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     args.epi.partial = nullptr;
   }
   CUtensorMap ta = a.mn_major ? make_map_mn(A, M, K, lda) : make_map(A, M, K, lda, BM);
-  CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BN);
-  static bool attr_set = false;
-  if (!attr_set) {
-    CG_CUDA(cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
+  CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BNh);
+  static bool attr_set[2] = {false, false};
+  auto kern = pair ? gemm_tf32_kernel<2> : gemm_tf32_kernel<1>;
+  if (!attr_set[ncta - 1]) {
+    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set[ncta - 1] = true;
   }
   int t = ctx->begin_timed(1);
-  const unsigned grid = std::min<unsigned>(args.tiles, (unsigned)ctx->num_sms);  // persistent
-  gemm_tf32_kernel<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, args);
+  const unsigned grid = std::min<unsigned>(args.tiles, units) * ncta;  // persistent
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
+  } else {
+    kern<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, args);
+  }
   CG_CHECK_LAUNCH();
   ctx->launches++;
   if (splits > 1) {

@@ -26,7 +26,10 @@ def gemm(ctx, A, B, split=1, precision=1):
 
 @pytest.mark.parametrize("M,N,K,split", [(128, 16, 32, 1), (1, 16, 8, 1), (200, 48, 256, 1), (1000, 256, 602, 1),
                                          (300, 602, 256, 1), (48, 256, 5000, 0), (256, 602, 20000, 0),
-                                         (513, 41, 100, 1), (130, 128, 64, 3)])
+                                         (513, 41, 100, 1), (130, 128, 64, 3),
+                                         # CTA-pair (cta_group::2) tiles: M >= 256, row/column tails
+                                         (256, 16, 8, 1), (4096, 256, 604, 1), (2000, 48, 256, 1),
+                                         (777, 100, 48, 1), (1100, 602, 256, 1), (3000, 256, 1000, 4)])
 def test_gemm_tn(ctx, M, N, K, split):
     rng = np.random.default_rng(M * 7 + N + K)
     A = rng.standard_normal((M, K)).astype(np.float32)
@@ -68,7 +71,8 @@ def gemm_general(ctx, A, a_mn, B, b_mn, split=1, precision=1):
 
 @pytest.mark.parametrize("a_mn,b_mn", [(1, 1), (1, 0), (0, 1)])
 @pytest.mark.parametrize("M,N,K,split,prec", [(256, 604, 20000, 0, 3), (41, 256, 3000, 0, 1), (41, 256, 3000, 0, 3),
-                                              (128, 96, 64, 1, 1), (300, 33, 100, 1, 3), (16, 602, 999, 0, 1)])
+                                              (128, 96, 64, 1, 1), (300, 33, 100, 1, 3), (16, 602, 999, 0, 1),
+                                              (1024, 256, 700, 1, 3), (600, 130, 96, 1, 1)])
 def test_gemm_mn_major(ctx, a_mn, b_mn, M, N, K, split, prec):
     """Weight-gradient form C = X^T Y read from row-major activations (no transpose)."""
     rng = np.random.default_rng(M + 3 * N + K)
