@@ -36,6 +36,8 @@ constexpr int BM = 128;
 constexpr int BK = 32;              // fp32 elements per k-block row = 128 bytes
 constexpr int A_STAGE = BM * BK * 4;  // 16 KB
 constexpr int kThreads = 320;  // 10 warps: TMA, MMA, 4 converters, 4 epilogue
+constexpr uint32_t kTileLd4 = 9;  // epilogue staging tile row stride in float4 (144 B)
+constexpr size_t kEpiSmem = 4 * 32 * kTileLd4 * 16;
 
 struct GemmArgs {
   uint32_t M, N, K;
@@ -173,7 +175,9 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_cta(uint32_t bar, uint32_t cta) {
   uint32_t ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(bar), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+  // default .release.cta semantics (as CUTLASS's ClusterBarrier::arrive): a
+  // .cluster-scope release costs a MEMBAR.GPU per arrival
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -288,6 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = bars + 3 * S;    // [2] accumulator ready
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  // epilogue staging: per epilogue warp a 32-row x 32-column tile, rows 144 B
+  // apart (conflict-free 128-bit row and column-chunk accesses)
+  float4* epi_tiles = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(bars) + ((3 * S + 5) * 8 + 15) / 16 * 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = NCTA == 2 ? cluster_rank() : 0;
   const uint32_t cid = blockIdx.x / NCTA, ncl = gridDim.x / NCTA;  // pair index / count
@@ -436,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < args.M;
       const float rs = (row_ok && e.rowscale) ? __ldg(e.rowscale + row) : 1.f;
       const uint32_t z = t / (args.nt * args.mt);
+      float4* T = epi_tiles + q * (32 * kTileLd4);
       for (uint32_t c = 0; c < BN; c += 32) {
         float v[32];
         if (nkb) {
@@ -445,48 +453,72 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
         const uint32_t col0 = n0 + c;
-        if (!row_ok || col0 >= args.N) continue;
+        if (col0 >= args.N) continue;  // warp-uniform
+        const bool full = col0 + 32 <= args.N && (!e.partial || (args.N & 3) == 0);
+        if (full) {
+          // Staged through shared memory so global rows are read/written as
+          // whole 128-byte lines (a warp's lanes own 32 different rows).
+          const uint32_t r8 = lane >> 3, c4 = lane & 7;
+          const uint32_t rbase = m0 + q * 32;
+          if (!e.partial && e.mask) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t rr = 4 * i + r8, grow = rbase + rr;
+              T[rr * kTileLd4 + c4] = grow < args.M
+                  ? __ldg(reinterpret_cast<const float4*>(e.mask + (size_t)grow * e.mask_ld + e.mask_col + col0) + c4)
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            __syncwarp();
+          }
+          float4 o[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            if (e.partial) continue;
+            if (e.rowscale && col0 + 4 * i >= e.scale_col_begin) {
+              o[i].x *= rs; o[i].y *= rs; o[i].z *= rs; o[i].w *= rs;
+            }
+            if (e.bias) {
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + col0) + i);
+              o[i].x += bb.x; o[i].y += bb.y; o[i].z += bb.z; o[i].w += bb.w;
+            }
+            if (e.relu) {
+              o[i].x = fmaxf(o[i].x, 0.f); o[i].y = fmaxf(o[i].y, 0.f);
+              o[i].z = fmaxf(o[i].z, 0.f); o[i].w = fmaxf(o[i].w, 0.f);
+            }
+            if (e.mask) {
+              const float4 mm = T[lane * kTileLd4 + i];
+              o[i].x = mm.x > 0.f ? o[i].x : 0.f; o[i].y = mm.y > 0.f ? o[i].y : 0.f;
+              o[i].z = mm.z > 0.f ? o[i].z : 0.f; o[i].w = mm.w > 0.f ? o[i].w : 0.f;
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) T[lane * kTileLd4 + i] = o[i];
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t rr = 4 * i + r8, grow = rbase + rr;
+            if (grow >= args.M) continue;
+            float* dst = e.partial ? e.partial + ((size_t)z * args.M + grow) * args.N + col0
+                                   : e.out + (size_t)grow * e.ld_out + e.out_col + col0;
+            reinterpret_cast<float4*>(dst)[c4] = T[rr * kTileLd4 + c4];
+          }
+          __syncwarp();
+          continue;
+        }
+        if (!row_ok) continue;
         if (e.partial) {
           float* dst = e.partial + ((size_t)z * args.M + row) * args.N + col0;
-          if (col0 + 32 <= args.N && (args.N & 3) == 0) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < args.N) dst[i] = v[i];
-          }
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < args.N) dst[i] = v[i];
           continue;
         }
         float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
-        if (col0 + 32 <= args.N) {
-          const float* mrow = e.mask ? e.mask + (size_t)row * e.mask_ld + e.mask_col + col0 : nullptr;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            if (e.rowscale) {
-              if (col0 + i >= e.scale_col_begin) { o.x *= rs; o.y *= rs; o.z *= rs; o.w *= rs; }
-            }
-            if (e.bias) {
-              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + col0 + i));
-              o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
-            }
-            if (e.relu) {
-              o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
-            }
-            if (mrow) {
-              const float4 mm = __ldg(reinterpret_cast<const float4*>(mrow + i));
-              o.x = mm.x > 0.f ? o.x : 0.f; o.y = mm.y > 0.f ? o.y : 0.f;
-              o.z = mm.z > 0.f ? o.z : 0.f; o.w = mm.w > 0.f ? o.w : 0.f;
-            }
-            *reinterpret_cast<float4*>(dst + i) = o;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (col0 + i < args.N) dst[i] = apply_epi(e, row, col0 + i, v[i]);
-        }
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < args.N) dst[i] = apply_epi(e, row, col0 + i, v[i]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -607,7 +639,8 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     const char* v = std::getenv("CATGNN_GEMM_PAIR");
     return v ? std::atoi(v) : 1;
   }();
-  const bool pair = pair_env != 0 && M >= 256;
+  // (skinny N: the pair's per-tile handshakes outweigh the halved B traffic)
+  const bool pair = pair_env != 0 && M >= 256 && N >= 128;
   const uint32_t ncta = pair ? 2 : 1;
   // 3xTF32 doubles the stage (lo tiles): single-CTA 128-wide N tiles keep 3 stages in flight
   const uint32_t bn_max = (split3 && !pair) ? 128 : 256;
@@ -636,10 +669,10 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
 
   const uint32_t b_stage = BNh * BK * 4;
   const size_t stage_bytes = (size_t)(A_STAGE + b_stage) * (split3 ? 2 : 1);
-  const size_t budget = 227 * 1024 - 1024 - 512;
+  const size_t budget = 227 * 1024 - 1024 - 512 - kEpiSmem;
   uint32_t stages = (uint32_t)std::min<size_t>(6, budget / stage_bytes);
   if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (3 * stages + 5) * 8;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + ((3 * stages + 5) * 8 + 15) / 16 * 16 + kEpiSmem;
 
   GemmArgs args{};
   args.M = M;
