@@ -145,6 +145,11 @@ int catgnn_shard_labels(catgnn_shard s, int32_t* labels);
 /* which: 0 = input features, 1 = SGC-propagated features. */
 int catgnn_shard_export_features(catgnn_shard s, int which, float* out);
 
+/* Device read bandwidth (GB/s) over a `bytes` buffer read `passes` times with
+ * 128-bit L2-cached loads: < 126 MB measures L2, GBs measure HBM (roofline
+ * denominators; not a reference function). */
+int catgnn_probe_read_bandwidth(catgnn_ctx ctx, uint64_t bytes, int passes, double* gbs);
+
 /* --------------------------------------------- neighbour completion (A1) */
 /* complete_edges (proj/src/completion.cpp:130-171, PartitionBuilder :13-58) on
  * the device: edges = 2 x num_edges external ids in stream order, which must be

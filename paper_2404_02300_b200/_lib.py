@@ -66,6 +66,7 @@ def _load():
         "catgnn_completion_part_counts": (C.c_int, [vp, u32, P(u64), P(u64), P(u64)]),
         "catgnn_completion_part": (C.c_int, [vp, u32, vp, vp, vp, vp]),
         "catgnn_completion_destroy": (C.c_int, [vp]),
+        "catgnn_probe_read_bandwidth": (C.c_int, [vp, u64, C.c_int, P(f64)]),
         "catgnn_shard_get_info": (C.c_int, [vp, vp]),
         "catgnn_csr_export": (C.c_int, [vp, vp, vp]),
         "catgnn_shard_role_rows": (C.c_int, [vp, C.c_int, vp]),

@@ -51,6 +51,7 @@ struct AggKernelArgs {
   int relu;
   const float* __restrict__ mask;
   uint32_t mask_ld, mask_col;
+  int stream_hint;  // column indices and output rows with evict-first hints
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -68,6 +69,12 @@ __device__ __forceinline__ void add4(float4& a, const float4& v) {
 __device__ __forceinline__ float4 shfl_xor4(const float4& v, int m) {
   return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+
+// Column index e: read once per pass, so with stream_hint it is loaded
+// evict-first and leaves L2 to the gathered feature rows.
+__device__ __forceinline__ int ld_col(const AggKernelArgs& p, int64_t e) {
+  return p.stream_hint ? __ldcs(p.col + e) : __ldg(p.col + e);
 }
 
 __device__ __forceinline__ float post_scale(int norm, float deg) {
@@ -105,7 +112,9 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
       a.x = m.x > 0.f ? a.x : 0.f; a.y = m.y > 0.f ? a.y : 0.f;
       a.z = m.z > 0.f ? a.z : 0.f; a.w = m.w > 0.f ? a.w : 0.f;
     }
-    *reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4) = a;
+    float4* dst = reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4);
+    if (p.stream_hint) __stcs(dst, a);  // evict-first: keep L2 for the gathered rows
+    else *dst = a;
   }
 }
 
@@ -120,7 +129,7 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
   for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t e = e0; e < e1; e += 32) {
     const int n = (int)((e1 - e) < 32 ? (e1 - e) : 32);
-    const int myj = lane < n ? __ldg(p.col + e + lane) : 0;
+    const int myj = lane < n ? ld_col(p, e + lane) : 0;
     float mys = 1.0f;
     if (PRE) mys = lane < n ? __ldg(p.pre + myj) : 0.0f;
     for (int kb = 0; kb < n; kb += G * UNROLL) {
@@ -171,8 +180,8 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   const bool writer = lane < LPN;
   const int64_t E0 = __ldg(p.row_ptr + r0), E1 = __ldg(p.row_ptr + r1);
   int64_t cb = E0;  // first edge of the current chunk
-  int cur = (cb + lane < E1) ? __ldg(p.col + cb + lane) : 0;
-  int nxt = (cb + 32 + lane < E1) ? __ldg(p.col + cb + 32 + lane) : 0;
+  int cur = (cb + lane < E1) ? ld_col(p, cb + lane) : 0;
+  int nxt = (cb + 32 + lane < E1) ? ld_col(p, cb + 32 + lane) : 0;
   float curs = 1.f, nxts = 1.f;
   if (PRE) {
     curs = (cb + lane < E1) ? __ldg(p.pre + cur) : 0.f;
@@ -202,7 +211,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
           cur = nxt;
           curs = nxts;
           const bool ok = cb + 32 + lane < E1;
-          nxt = ok ? __ldg(p.col + cb + 32 + lane) : 0;
+          nxt = ok ? ld_col(p, cb + 32 + lane) : 0;
           if (PRE) nxts = ok ? __ldg(p.pre + nxt) : 0.f;
         }
         float4 v[UNROLL][VPL];
@@ -459,6 +468,8 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.mask = a.mask;
     p.mask_ld = a.mask_ld;
     p.mask_col = a.mask_col + c4 * 4;
+    static const int hint = env_int("CATGNN_AGG_HINT", 1);
+    p.stream_hint = hint;
     int lpn = 32;
     AggFn fn = pick_kernel(w4, a.pre != nullptr, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));

@@ -444,6 +444,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float rs = (row_ok && e.rowscale) ? __ldg(e.rowscale + row) : 1.f;
       const uint32_t z = t / (args.nt * args.mt);
       float4* T = epi_tiles + q * (32 * kTileLd4);
+      const uint32_t r8 = lane >> 3, c4 = lane & 7;
+      const uint32_t rbase = m0 + q * 32;
       for (uint32_t c = 0; c < BN; c += 32) {
         float v[32];
         if (nkb) {
@@ -454,57 +456,64 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t col0 = n0 + c;
         if (col0 >= args.N) continue;  // warp-uniform
-        const bool full = col0 + 32 <= args.N && (!e.partial || (args.N & 3) == 0);
-        if (full) {
-          // Staged through shared memory so global rows are read/written as
-          // whole 128-byte lines (a warp's lanes own 32 different rows).
-          const uint32_t r8 = lane >> 3, c4 = lane & 7;
-          const uint32_t rbase = m0 + q * 32;
-          if (!e.partial && e.mask) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint32_t rr = 4 * i + r8, grow = rbase + rr;
-              T[rr * kTileLd4 + c4] = grow < args.M
-                  ? __ldg(reinterpret_cast<const float4*>(e.mask + (size_t)grow * e.mask_ld + e.mask_col + col0) + c4)
-                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            __syncwarp();
-          }
-          float4 o[8];
+        // Plain outputs (forward GEMMs: row scale / bias / ReLU) are staged
+        // through shared memory so a warp writes whole 128-byte lines (its lanes
+        // own 32 different rows).  Masked and split-K outputs store directly:
+        // their kernels are epilogue-bound and the extra shared-memory round
+        // trips cost more than the coalescing gains (measured).
+        if (col0 + 32 <= args.N && !e.partial && !e.mask) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            if (e.partial) continue;
-            if (e.rowscale && col0 + 4 * i >= e.scale_col_begin) {
-              o[i].x *= rs; o[i].y *= rs; o[i].z *= rs; o[i].w *= rs;
-            }
+            float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            if (e.rowscale && col0 + 4 * i >= e.scale_col_begin) { o.x *= rs; o.y *= rs; o.z *= rs; o.w *= rs; }
             if (e.bias) {
               const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + col0) + i);
-              o[i].x += bb.x; o[i].y += bb.y; o[i].z += bb.z; o[i].w += bb.w;
+              o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
             }
             if (e.relu) {
-              o[i].x = fmaxf(o[i].x, 0.f); o[i].y = fmaxf(o[i].y, 0.f);
-              o[i].z = fmaxf(o[i].z, 0.f); o[i].w = fmaxf(o[i].w, 0.f);
+              o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
             }
-            if (e.mask) {
-              const float4 mm = T[lane * kTileLd4 + i];
-              o[i].x = mm.x > 0.f ? o[i].x : 0.f; o[i].y = mm.y > 0.f ? o[i].y : 0.f;
-              o[i].z = mm.z > 0.f ? o[i].z : 0.f; o[i].w = mm.w > 0.f ? o[i].w : 0.f;
-            }
+            T[lane * kTileLd4 + i] = o;
           }
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 8; ++i) T[lane * kTileLd4 + i] = o[i];
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const uint32_t rr = 4 * i + r8, grow = rbase + rr;
-            if (grow >= args.M) continue;
-            float* dst = e.partial ? e.partial + ((size_t)z * args.M + grow) * args.N + col0
-                                   : e.out + (size_t)grow * e.ld_out + e.out_col + col0;
-            reinterpret_cast<float4*>(dst)[c4] = T[rr * kTileLd4 + c4];
+            if (grow < args.M)
+              reinterpret_cast<float4*>(e.out + (size_t)grow * e.ld_out + e.out_col + col0)[c4] = T[rr * kTileLd4 + c4];
           }
           __syncwarp();
+          continue;
+        }
+        if (!row_ok) continue;
+        if (e.partial) {
+          float* dst = e.partial + ((size_t)z * args.M + row) * args.N + col0;
+          if (col0 + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            continue;
+          }
+        }
+        if (!e.partial && col0 + 32 <= args.N) {  // masked: ReLU backward
+          float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
+          const float* mrow = e.mask + (size_t)row * e.mask_ld + e.mask_col + col0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            if (e.rowscale && col0 + i >= e.scale_col_begin) { o.x *= rs; o.y *= rs; o.z *= rs; o.w *= rs; }
+            if (e.bias) {
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + col0 + i));
+              o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+            }
+            if (e.relu) {
+              o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+            }
+            const float4 mm = __ldg(reinterpret_cast<const float4*>(mrow + i));
+            o.x = mm.x > 0.f ? o.x : 0.f; o.y = mm.y > 0.f ? o.y : 0.f;
+            o.z = mm.z > 0.f ? o.z : 0.f; o.w = mm.w > 0.f ? o.w : 0.f;
+            *reinterpret_cast<float4*>(dst + i) = o;
+          }
           continue;
         }
         if (!row_ok) continue;

@@ -314,6 +314,14 @@ def complete_edges(edges, home, roles=None, partitions: Optional[int] = None, ho
         lib.catgnn_completion_destroy(c)
 
 
+def probe_read_bandwidth(nbytes: int, passes: int = 20, ctx: Optional[Context] = None) -> float:
+    """Device read bandwidth in GB/s (L2 when nbytes fits the 126 MB L2)."""
+    ctx = ctx or default_context()
+    out = C.c_double()
+    check(lib.catgnn_probe_read_bandwidth(ctx.handle, int(nbytes), int(passes), C.byref(out)))
+    return out.value
+
+
 class FeatureStore:
     """Device copy of the global feature matrix (rows x dim f32, FEA1 row
     order) that shards gather their rows from by external id."""
