@@ -107,6 +107,11 @@ def dist_env():
     return world, rank, local
 
 
+def act_width(d):
+    """Row stride of a device activation (gnn.cu act_width): 16-float multiples below 128."""
+    return (d + 15) // 16 * 16 if d < 128 else (d + 3) // 4 * 4
+
+
 def agg_bytes(nnz, rows, width, self_term):
     """nnz*(4 + 4d) + N*(4d*(1+self) + 8)."""
     return nnz * (4 + 4 * width) + rows * (4 * width * (1 + self_term) + 8)
@@ -205,7 +210,8 @@ def workload_config(w, prep, args):
             "feature_dim": w.dim, "classes": w.classes, "partitions": w.partitions,
             "partitioner": f"reference SPRING beta={w.beta} tau_vol={m['tau_vol']} + 1-hop completion",
             "replication_factor": m["rf"], "part_nnz": m["part_nnz"], "sum_over_max_edges": m["sum_over_max"],
-            "aggregation_widths": [(x + 3) // 4 * 4 for x in w.passes()], "sync_interval": args.sync,
+            "aggregation_widths": w.passes(),
+            "aggregation_row_stride_floats": [act_width(x) for x in w.passes()], "sync_interval": args.sync,
             "optimizer": "adam lr 0.01", "gemm_precision": "3xTF32 (tcgen05 kind::tf32)",
             "global_batch": "full-batch per partition", "parallelism": f"partition-parallel p={w.partitions}",
             "l2": "inputs larger than L2 (per-partition features 0.5 GB, activations > 126 MB)"}
@@ -351,7 +357,7 @@ def main():
     launches = ctx.launches - launches0
     ms_step = total_ms / args.steps
 
-    widths = [(x + 3) // 4 * 4 for x in w.passes()]
+    widths = w.passes()  # logical widths: algorithmic bytes exclude the row padding
     part_nnz = [meta["part_nnz"][i] for i in mine]
     part_rows = [meta["part_rows"][i] for i in mine]
     edges_per_step_rank = sum(part_nnz) * len(widths)
