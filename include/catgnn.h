@@ -44,6 +44,7 @@ typedef struct catgnn_model_s* catgnn_model;     /* GNN replica: params + optimi
 typedef struct catgnn_comm_s* catgnn_comm;       /* NCCL communicator (one rank per GPU) */
 typedef struct catgnn_features_s* catgnn_features; /* device copy of the global feature matrix */
 typedef struct catgnn_completion_s* catgnn_completion; /* per-partition edges + node tables */
+typedef struct catgnn_index_s* catgnn_index;           /* GraphIndex: interned ids + degrees */
 
 const char* catgnn_last_error(void);
 int catgnn_version(void);
@@ -149,6 +150,17 @@ int catgnn_shard_export_features(catgnn_shard s, int which, float* out);
  * 128-bit L2-cached loads: < 126 MB measures L2, GBs measure HBM (roofline
  * denominators; not a reference function). */
 int catgnn_probe_read_bandwidth(catgnn_ctx ctx, uint64_t bytes, int passes, double* gbs);
+
+/* ------------------------------------------------ graph index (§8(f) row 3) */
+/* compute_degrees (proj/src/edge_stream.cpp:192-215) on the device: external ids
+ * interned in first-seen order (record (u, v): u first), degree per node with
+ * self-loops counting 2, record and self-loop counts.  edges = 2 x num_edges
+ * host ids in stream order. */
+int catgnn_index_build(catgnn_ctx ctx, const uint64_t* edges, uint64_t num_edges, catgnn_index* out);
+int catgnn_index_info(catgnn_index idx, uint64_t* num_nodes, uint64_t* num_edges, uint64_t* num_self_loops);
+/* dense_to_ext[num_nodes], degree[num_nodes] (GraphIndex fields) */
+int catgnn_index_export(catgnn_index idx, uint64_t* dense_to_ext, uint32_t* degree);
+int catgnn_index_destroy(catgnn_index idx);
 
 /* --------------------------------------------- neighbour completion (A1) */
 /* complete_edges (proj/src/completion.cpp:130-171, PartitionBuilder :13-58) on

@@ -174,6 +174,16 @@ def spring_homes(input_path, num_ids, partitions, beta=1.05, tau_vol=0, seed=0, 
     return home
 
 
+def compute_degrees(input_path, capacity, add_reverse=False):
+    """GraphIndex of edge_stream.cpp:192-215: (dense_to_ext, degree, num_edges, num_self_loops)."""
+    d2e = np.zeros(max(capacity, 1), np.uint64)
+    deg = np.zeros(max(capacity, 1), np.uint32)
+    n = C.c_uint64(); m = C.c_uint64(); sl = C.c_uint64()
+    _check(lib().ref_compute_degrees(str(input_path).encode(), int(add_reverse), _p(d2e), _p(deg),
+                                     C.c_uint64(capacity), C.byref(n), C.byref(m), C.byref(sl)))
+    return d2e[:n.value], deg[:n.value], m.value, sl.value
+
+
 def artifact_replication_factor(d):
     """metrics.cpp:9-12 over read_partitions (store.cpp:269-333); also the manifest's value."""
     rf = C.c_double(); mrf = C.c_double()

@@ -308,6 +308,27 @@ int ref_spring_homes(const char* input, int add_reverse, std::uint32_t partition
   });
 }
 
+// ---- edge_stream.cpp:192-215 compute_degrees -------------------------------------
+// dense_to_ext / degree need `capacity` entries (2 x records is always enough).
+int ref_compute_degrees(const char* input, int add_reverse, std::uint64_t* dense_to_ext, std::uint32_t* degree,
+                        std::uint64_t capacity, std::uint64_t* num_nodes, std::uint64_t* num_edges,
+                        std::uint64_t* num_self_loops) {
+  return guarded([&] {
+    fs::path in(input);
+    EdgeFormat fmt = in.extension() == ".bin" ? EdgeFormat::binary_u64 : EdgeFormat::text_tsv;
+    EdgeStream stream(in, fmt, add_reverse != 0);
+    GraphIndex index = compute_degrees(stream);
+    if (index.num_nodes() > capacity) throw ConfigError("index buffer too small");
+    for (NodeId v = 0; v < index.num_nodes(); ++v) {
+      dense_to_ext[v] = index.dense_to_ext[v];
+      degree[v] = index.degree[v];
+    }
+    *num_nodes = index.num_nodes();
+    *num_edges = index.num_edges;
+    *num_self_loops = index.num_self_loops;
+  });
+}
+
 // ---- metrics.cpp:9-12 over a stored artifact (store.cpp:269-333) ----------------
 int ref_artifact_replication_factor(const char* dir, double* rf, double* manifest_rf) {
   return guarded([&] {

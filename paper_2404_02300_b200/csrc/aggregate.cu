@@ -358,7 +358,10 @@ int env_int(const char* name, int dflt) {
 
 template <int VPL, int LPN>
 AggFn pick_pre(bool pre) {
+  // narrow rows run 4 CTAs/SM (<= 64 registers; CATGNN_AGG_NARROW_MINB=3 for 3)
   static const int minb = env_int("CATGNN_AGG_MINB", 3);
+  static const int minb_narrow = env_int("CATGNN_AGG_NARROW_MINB", 4);
+  if (LPN < 32 && minb_narrow >= 4) return pre ? agg_kernel<VPL, LPN, true, 4> : agg_kernel<VPL, LPN, false, 4>;
   if (minb >= 3) return pre ? agg_kernel<VPL, LPN, true, 3> : agg_kernel<VPL, LPN, false, 3>;
   return pre ? agg_kernel<VPL, LPN, true, 2> : agg_kernel<VPL, LPN, false, 2>;
 }
@@ -380,7 +383,7 @@ AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
   if (w4 <= 16) {
     // narrow rows: lanes per neighbour x float4 per lane
     int mode = narrow_mode();
-    if (mode == 0) mode = w4 <= 12 ? 6 : 3;
+    if (mode == 0) mode = 3;  // 8 lanes x 2 float4, 4 CTAs/SM: fastest for the 41/44/48-wide class rows
     switch (mode) {
       case 1: *lpn_out = 16; return pick_pre<1, 16>(pre);
       case 2: *lpn_out = 4; return pick_pre<4, 4>(pre);
