@@ -175,6 +175,12 @@ int catgnn_index_destroy(catgnn_index idx);
 int catgnn_complete_edges(catgnn_ctx ctx, const uint64_t* edges, uint64_t num_edges, const uint32_t* home,
                           const uint8_t* roles, uint64_t num_nodes, uint32_t p, uint32_t hops,
                           catgnn_completion* out);
+/* Same for arbitrary 64-bit external ids: endpoints are routed through the
+ * device graph index (GraphIndex::dense); home[] and roles[] are indexed by
+ * dense id as the reference's HomeMap (completion.hpp:55-59) is. */
+int catgnn_complete_edges_indexed(catgnn_ctx ctx, catgnn_index index, const uint64_t* edges, uint64_t num_edges,
+                                  const uint32_t* home, const uint8_t* roles, uint32_t p, uint32_t hops,
+                                  catgnn_completion* out);
 int catgnn_completion_part_counts(catgnn_completion c, uint32_t part, uint64_t* edges, uint64_t* nodes,
                                   uint64_t* owned);
 int catgnn_completion_part(catgnn_completion c, uint32_t part, uint64_t* edges, uint64_t* ext, uint8_t* owner,

@@ -63,6 +63,11 @@ def _load():
         "catgnn_features_upload": (C.c_int, [vp, vp, u64, u64]),
         "catgnn_shard_gather_features": (C.c_int, [vp, vp]),
         "catgnn_complete_edges": (C.c_int, [vp, vp, u64, vp, vp, u64, u32, u32, P(vp)]),
+        "catgnn_complete_edges_indexed": (C.c_int, [vp, vp, vp, u64, vp, vp, u32, u32, P(vp)]),
+        "catgnn_index_build": (C.c_int, [vp, vp, u64, P(vp)]),
+        "catgnn_index_info": (C.c_int, [vp, P(u64), P(u64), P(u64)]),
+        "catgnn_index_export": (C.c_int, [vp, vp, vp]),
+        "catgnn_index_destroy": (C.c_int, [vp]),
         "catgnn_completion_part_counts": (C.c_int, [vp, u32, P(u64), P(u64), P(u64)]),
         "catgnn_completion_part": (C.c_int, [vp, u32, vp, vp, vp, vp]),
         "catgnn_completion_destroy": (C.c_int, [vp]),

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "index.hpp"
 #include "shard.hpp"
 
 struct catgnn_completion_s {
@@ -88,15 +89,36 @@ __global__ void first_of_key_kernel(const uint64_t* __restrict__ skey, const uin
     keep[sidx[j]] = (uint8_t)(j == 0 || skey[j] != skey[j - 1]);
 }
 
-__global__ void gather_edges_mark_kernel(const uint64_t* __restrict__ e, const uint64_t* __restrict__ kept, uint64_t nk,
-                                         uint64_t* __restrict__ out, uint8_t* __restrict__ present) {
+__global__ void gather_edges_mark_kernel(const uint64_t* __restrict__ e, const uint64_t* __restrict__ ext,
+                                         const uint64_t* __restrict__ kept, uint64_t nk, uint64_t* __restrict__ out,
+                                         uint8_t* __restrict__ present) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = kept[i];
-    const uint64_t u = e[2 * k], v = e[2 * k + 1];
-    out[2 * i] = u;
-    out[2 * i + 1] = v;
-    present[u] = 1;
-    present[v] = 1;
+    out[2 * i] = ext[2 * k];  // original record, original orientation
+    out[2 * i + 1] = ext[2 * k + 1];
+    present[e[2 * k]] = 1;
+    present[e[2 * k + 1]] = 1;
+  }
+}
+
+__global__ void ids_to_ext_kernel(uint64_t* __restrict__ ids, uint64_t n, const uint64_t* __restrict__ id_to_ext) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    ids[i] = id_to_ext[ids[i]];
+}
+
+__global__ void runs_to_u64_kernel(const uint32_t* __restrict__ runs, uint64_t n, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = runs[i];
+}
+
+// per run: home / role of its dense id (HomeMap and NodeMetaMap are by dense id)
+__global__ void by_run_kernel(const uint32_t* __restrict__ dense_of_run, uint64_t n, const uint32_t* __restrict__ home,
+                              const uint8_t* __restrict__ roles, uint32_t* __restrict__ home_run,
+                              uint8_t* __restrict__ roles_run) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = dense_of_run[r];
+    home_run[r] = home[d];
+    if (roles) roles_run[r] = roles[d];
   }
 }
 
@@ -125,6 +147,105 @@ struct Temp {
 template <typename T>
 T* dev(catgnn_ctx ctx, const char* name, size_t n) {
   return ctx->scratch_buf<T>(name, std::max<size_t>(n, 1));
+}
+
+// The per-partition work on node ids 0..n-1 (dense ids, or the ascending-ext
+// "runs" of a graph index): d_e routes and keys, d_ext is the original record
+// for the output, id_to_ext (ascending in id) maps node-table ids back.
+void complete_core(catgnn_ctx ctx, const uint64_t* d_e, const uint64_t* d_ext, uint64_t m, const uint32_t* d_home,
+                   const uint8_t* d_roles, uint64_t n, const uint64_t* id_to_ext, uint32_t p, uint32_t hops,
+                   catgnn_completion_s* res) {
+  cudaStream_t st = ctx->stream;
+  // reach masks
+  unsigned long long* reach = dev<unsigned long long>(ctx, "cmp_reach", n);
+  if (n) init_reach_kernel<<<grid_of(n), 256, 0, st>>>(d_home, n, reach);
+  for (uint32_t r = 1; r < hops; ++r) {
+    unsigned long long* next = dev<unsigned long long>(ctx, "cmp_reach_next", n);
+    CG_CUDA(cudaMemcpyAsync(next, reach, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (m) grow_reach_kernel<<<grid_of(m), 256, 0, st>>>(d_e, m, reach, next);
+    CG_CUDA(cudaMemcpyAsync(reach, next, n * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  CG_CHECK_LAUNCH();
+
+  res->p = p;
+  res->num_nodes = n;
+  res->parts.resize(p);
+  uint8_t* flag = dev<uint8_t>(ctx, "cmp_flag", m);
+  uint64_t* sel = dev<uint64_t>(ctx, "cmp_sel", m);
+  // per-partition buffers are sized by the routed count (grow-only scratch)
+  uint64_t *key = nullptr, *key2 = nullptr, *idx = nullptr, *idx2 = nullptr, *kept = nullptr, *oute = nullptr;
+  uint8_t* keep = nullptr;
+  uint8_t* present = dev<uint8_t>(ctx, "cmp_present", n);
+  uint64_t* ids = dev<uint64_t>(ctx, "cmp_ids", n);
+  uint8_t* own = dev<uint8_t>(ctx, "cmp_own", n);
+  uint8_t* rol = dev<uint8_t>(ctx, "cmp_rol", n);
+  uint64_t* count = dev<uint64_t>(ctx, "cmp_count", 1);
+  Temp tmp{ctx};
+  auto counted = [&]() {
+    uint64_t c = 0;
+    CG_CUDA(cudaMemcpyAsync(&c, count, 8, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    return c;
+  };
+  cub::CountingInputIterator<uint64_t> pos(0);
+  const int key_bits = 64;
+  for (uint32_t s = 0; s < p; ++s) {
+    auto& P = res->parts[s];
+    uint64_t nk = 0;
+    if (m) {
+      route_flags_kernel<<<grid_of(m), 256, 0, st>>>(d_e, m, reach, s, flag);
+      size_t tb = 0;
+      CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos, flag, sel, count, m, st));
+      CG_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, pos, flag, sel, count, m, st));
+      const uint64_t ns = counted();
+      key = dev<uint64_t>(ctx, "cmp_key", ns);
+      key2 = dev<uint64_t>(ctx, "cmp_key2", ns);
+      idx = dev<uint64_t>(ctx, "cmp_idx", ns);
+      idx2 = dev<uint64_t>(ctx, "cmp_idx2", ns);
+      keep = dev<uint8_t>(ctx, "cmp_keep", ns);
+      kept = dev<uint64_t>(ctx, "cmp_kept", ns);
+      oute = dev<uint64_t>(ctx, "cmp_oute", 2 * ns);
+      if (ns) {
+        pair_keys_kernel<<<grid_of(ns), 256, 0, st>>>(d_e, sel, ns, key, idx);
+        CG_CHECK_LAUNCH();
+        tb = 0;
+        CG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, idx, idx2, ns, 0, key_bits, st));
+        CG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(tb), tb, key, key2, idx, idx2, ns, 0, key_bits, st));
+        first_of_key_kernel<<<grid_of(ns), 256, 0, st>>>(key2, idx2, ns, keep);
+        CG_CHECK_LAUNCH();
+        tb = 0;
+        CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, sel, keep, kept, count, ns, st));
+        CG_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, sel, keep, kept, count, ns, st));
+        nk = counted();
+      }
+    }
+    if (n) CG_CUDA(cudaMemsetAsync(present, 0, n, st));
+    if (nk) gather_edges_mark_kernel<<<grid_of(nk), 256, 0, st>>>(d_e, d_ext, kept, nk, oute, present);
+    if (n) mark_owned_kernel<<<grid_of(n), 256, 0, st>>>(d_home, n, s, present);
+    CG_CHECK_LAUNCH();
+    uint64_t nn = 0;
+    if (n) {
+      size_t tb = 0;
+      CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos, present, ids, count, n, st));
+      CG_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, pos, present, ids, count, n, st));
+      nn = counted();
+    }
+    if (nn) node_records_kernel<<<grid_of(nn), 256, 0, st>>>(ids, nn, d_home, d_roles, s, own, rol);
+    if (nn && id_to_ext) ids_to_ext_kernel<<<grid_of(nn), 256, 0, st>>>(ids, nn, id_to_ext);
+    CG_CHECK_LAUNCH();
+    P.edges.resize(2 * nk);
+    P.ext.resize(nn);
+    P.owner.resize(nn);
+    P.role.resize(nn);
+    if (nk) CG_CUDA(cudaMemcpyAsync(P.edges.data(), oute, 2 * nk * 8, cudaMemcpyDeviceToHost, st));
+    if (nn) {
+      CG_CUDA(cudaMemcpyAsync(P.ext.data(), ids, nn * 8, cudaMemcpyDeviceToHost, st));
+      CG_CUDA(cudaMemcpyAsync(P.owner.data(), own, nn, cudaMemcpyDeviceToHost, st));
+      CG_CUDA(cudaMemcpyAsync(P.role.data(), rol, nn, cudaMemcpyDeviceToHost, st));
+    }
+    CG_CUDA(cudaStreamSynchronize(st));
+    ctx->launches += 6;
+  }
 }
 
 }  // namespace
@@ -160,97 +281,52 @@ int catgnn_complete_edges(catgnn_ctx ctx, const uint64_t* edges, uint64_t num_ed
     CG_CUDA(cudaStreamSynchronize(st));
     if (h_bad) throw DataError("edge endpoint outside the node set (external ids must be dense)");
 
-    // reach masks
-    unsigned long long* reach = dev<unsigned long long>(ctx, "cmp_reach", n);
-    if (n) init_reach_kernel<<<grid_of(n), 256, 0, st>>>(d_home, n, reach);
-    for (uint32_t r = 1; r < hops; ++r) {
-      unsigned long long* next = dev<unsigned long long>(ctx, "cmp_reach_next", n);
-      CG_CUDA(cudaMemcpyAsync(next, reach, n * 8, cudaMemcpyDeviceToDevice, st));
-      if (m) grow_reach_kernel<<<grid_of(m), 256, 0, st>>>(d_e, m, reach, next);
-      CG_CUDA(cudaMemcpyAsync(reach, next, n * 8, cudaMemcpyDeviceToDevice, st));
-    }
-    CG_CHECK_LAUNCH();
-
     auto res = std::make_unique<catgnn_completion_s>();
-    res->p = p;
-    res->num_nodes = n;
-    res->parts.resize(p);
-    uint8_t* flag = dev<uint8_t>(ctx, "cmp_flag", m);
-    uint64_t* sel = dev<uint64_t>(ctx, "cmp_sel", m);
-    // per-partition buffers are sized by the routed count (grow-only scratch)
-    uint64_t *key = nullptr, *key2 = nullptr, *idx = nullptr, *idx2 = nullptr, *kept = nullptr, *oute = nullptr;
-    uint8_t* keep = nullptr;
-    uint8_t* present = dev<uint8_t>(ctx, "cmp_present", n);
-    uint64_t* ids = dev<uint64_t>(ctx, "cmp_ids", n);
-    uint8_t* own = dev<uint8_t>(ctx, "cmp_own", n);
-    uint8_t* rol = dev<uint8_t>(ctx, "cmp_rol", n);
-    uint64_t* count = dev<uint64_t>(ctx, "cmp_count", 1);
-    Temp tmp{ctx};
-    auto counted = [&]() {
-      uint64_t c = 0;
-      CG_CUDA(cudaMemcpyAsync(&c, count, 8, cudaMemcpyDeviceToHost, st));
-      CG_CUDA(cudaStreamSynchronize(st));
-      return c;
-    };
-    cub::CountingInputIterator<uint64_t> pos(0);
-    const int key_bits = 64;
-    for (uint32_t s = 0; s < p; ++s) {
-      auto& P = res->parts[s];
-      uint64_t nk = 0;
-      if (m) {
-        route_flags_kernel<<<grid_of(m), 256, 0, st>>>(d_e, m, reach, s, flag);
-        size_t tb = 0;
-        CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos, flag, sel, count, m, st));
-        CG_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, pos, flag, sel, count, m, st));
-        const uint64_t ns = counted();
-        key = dev<uint64_t>(ctx, "cmp_key", ns);
-        key2 = dev<uint64_t>(ctx, "cmp_key2", ns);
-        idx = dev<uint64_t>(ctx, "cmp_idx", ns);
-        idx2 = dev<uint64_t>(ctx, "cmp_idx2", ns);
-        keep = dev<uint8_t>(ctx, "cmp_keep", ns);
-        kept = dev<uint64_t>(ctx, "cmp_kept", ns);
-        oute = dev<uint64_t>(ctx, "cmp_oute", 2 * ns);
-        if (ns) {
-          pair_keys_kernel<<<grid_of(ns), 256, 0, st>>>(d_e, sel, ns, key, idx);
-          CG_CHECK_LAUNCH();
-          tb = 0;
-          CG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, idx, idx2, ns, 0, key_bits, st));
-          CG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(tb), tb, key, key2, idx, idx2, ns, 0, key_bits, st));
-          first_of_key_kernel<<<grid_of(ns), 256, 0, st>>>(key2, idx2, ns, keep);
-          CG_CHECK_LAUNCH();
-          tb = 0;
-          CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, sel, keep, kept, count, ns, st));
-          CG_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, sel, keep, kept, count, ns, st));
-          nk = counted();
-        }
-      }
-      if (n) CG_CUDA(cudaMemsetAsync(present, 0, n, st));
-      if (nk) gather_edges_mark_kernel<<<grid_of(nk), 256, 0, st>>>(d_e, kept, nk, oute, present);
-      if (n) mark_owned_kernel<<<grid_of(n), 256, 0, st>>>(d_home, n, s, present);
-      CG_CHECK_LAUNCH();
-      uint64_t nn = 0;
-      if (n) {
-        size_t tb = 0;
-        CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos, present, ids, count, n, st));
-        CG_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, pos, present, ids, count, n, st));
-        nn = counted();
-      }
-      if (nn) node_records_kernel<<<grid_of(nn), 256, 0, st>>>(ids, nn, d_home, d_roles, s, own, rol);
-      CG_CHECK_LAUNCH();
-      P.edges.resize(2 * nk);
-      P.ext.resize(nn);
-      P.owner.resize(nn);
-      P.role.resize(nn);
-      if (nk) CG_CUDA(cudaMemcpyAsync(P.edges.data(), oute, 2 * nk * 8, cudaMemcpyDeviceToHost, st));
-      if (nn) {
-        CG_CUDA(cudaMemcpyAsync(P.ext.data(), ids, nn * 8, cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaMemcpyAsync(P.owner.data(), own, nn, cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaMemcpyAsync(P.role.data(), rol, nn, cudaMemcpyDeviceToHost, st));
-      }
-      CG_CUDA(cudaStreamSynchronize(st));
-      ctx->launches += 6;
-    }
+    complete_core(ctx, d_e, d_e, m, d_home, d_roles, n, nullptr, p, hops, res.get());
     // the completion scratch is sized by the stream: give it back
+    for (auto it = ctx->scratch.begin(); it != ctx->scratch.end();)
+      it = it->first.rfind("cmp_", 0) == 0 ? ctx->scratch.erase(it) : std::next(it);
+    *out = res.release();
+  });
+}
+
+int catgnn_complete_edges_indexed(catgnn_ctx ctx, catgnn_index index, const uint64_t* edges, uint64_t num_edges,
+                                  const uint32_t* home, const uint8_t* roles, uint32_t p, uint32_t hops,
+                                  catgnn_completion* out) {
+  return guarded([&] {
+    if (!ctx || !index || !out || (num_edges && !edges) || (index->n && !home)) throw ConfigError("null argument");
+    if (index->ctx->device != ctx->device) throw ConfigError("index and context must share one device");
+    if (hops < 1 || hops > 3) throw ConfigError("hop count must be in {1,2,3}");                 // :133
+    if (p == 0) throw DataError("home map does not cover the node set");                         // :65-66
+    if (p > 64) throw ConfigError("device completion supports at most 64 partitions");           // :147-148
+    const uint64_t m = num_edges, n = index->n;
+    for (uint64_t v = 0; v < n; ++v)
+      if (home[v] >= p) throw DataError("home partition out of range");                         // :67-68
+    CG_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    uint64_t* d_ext = dev<uint64_t>(ctx, "cmp_ext", 2 * m);
+    uint64_t* d_e = dev<uint64_t>(ctx, "cmp_edges", 2 * m);
+    uint32_t* runs = dev<uint32_t>(ctx, "cmp_runs", 2 * m);
+    uint32_t* home_d = dev<uint32_t>(ctx, "cmp_home_dense", n);
+    uint8_t* roles_d = roles ? dev<uint8_t>(ctx, "cmp_roles_dense", n) : nullptr;
+    uint32_t* home_run = dev<uint32_t>(ctx, "cmp_home", n);
+    uint8_t* roles_run = roles ? dev<uint8_t>(ctx, "cmp_roles", n) : nullptr;
+    if (m) CG_CUDA(cudaMemcpyAsync(d_ext, edges, 2 * m * 8, cudaMemcpyHostToDevice, st));
+    if (n) CG_CUDA(cudaMemcpyAsync(home_d, home, n * 4, cudaMemcpyHostToDevice, st));
+    if (roles && n) CG_CUDA(cudaMemcpyAsync(roles_d, roles, n, cudaMemcpyHostToDevice, st));
+    int* missing = dev<int>(ctx, "cmp_bad", 1);
+    CG_CUDA(cudaMemsetAsync(missing, 0, 4, st));
+    // GraphIndex::dense (edge_stream.hpp:113-118) for every endpoint, as runs
+    if (m) map_to_runs_kernel<<<grid_of(2 * m), 256, 0, st>>>(index->sorted_ext.p, n, d_ext, 2 * m, runs, missing);
+    if (m) runs_to_u64_kernel<<<grid_of(2 * m), 256, 0, st>>>(runs, 2 * m, d_e);
+    if (n) by_run_kernel<<<grid_of(n), 256, 0, st>>>(index->dense_of_run.p, n, home_d, roles_d, home_run, roles_run);
+    CG_CHECK_LAUNCH();
+    int h_missing = 0;
+    CG_CUDA(cudaMemcpyAsync(&h_missing, missing, 4, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    if (h_missing) throw DataError("node missing from degree table");                           // :115-116
+    auto res = std::make_unique<catgnn_completion_s>();
+    complete_core(ctx, d_e, d_ext, m, home_run, roles_run, n, index->sorted_ext.p, p, hops, res.get());
     for (auto it = ctx->scratch.begin(); it != ctx->scratch.end();)
       it = it->first.rfind("cmp_", 0) == 0 ? ctx->scratch.erase(it) : std::next(it);
     *out = res.release();

@@ -37,7 +37,7 @@ __all__ = [
     "SyncPoint", "DistTrainResult", "ConfigError", "DataError", "InternalError", "build_adjacency",
     "sgc_propagate", "zero_params", "softmax_loss", "softmax_gradient", "train_epochs", "train_local",
     "sync_weights", "model_average", "evaluate_micro_f1", "load_training_data", "distributed_train",
-    "replication_factor", "default_context", "FeatureStore", "GraphPartition", "complete_edges",
+    "replication_factor", "default_context", "FeatureStore", "GraphPartition", "complete_edges", "GraphIndex", "compute_degrees",
 ]
 
 
@@ -286,18 +286,59 @@ class GraphPartition:
         return int(self.ext.size)
 
 
+class GraphIndex:
+    """GraphIndex (edge_stream.hpp:104-128) built on the device by
+    compute_degrees (edge_stream.cpp:192-215)."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self.handle, self.ctx = handle, ctx
+        n, m, sl = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib.catgnn_index_info(handle, C.byref(n), C.byref(m), C.byref(sl)))
+        self.num_nodes, self.num_edges, self.num_self_loops = n.value, m.value, sl.value
+        self.dense_to_ext = np.zeros(self.num_nodes, np.uint64)
+        self.degree = np.zeros(self.num_nodes, np.uint32)
+        check(lib.catgnn_index_export(handle, _ptr(self.dense_to_ext), _ptr(self.degree)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.catgnn_index_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def compute_degrees(edges, ctx: Optional[Context] = None) -> GraphIndex:
+    """compute_degrees (edge_stream.cpp:192-215) over an in-memory stream."""
+    ctx = ctx or default_context()
+    e = np.ascontiguousarray(np.asarray(edges, np.uint64).reshape(-1, 2))
+    h = C.c_void_p()
+    check(lib.catgnn_index_build(ctx.handle, _ptr(e), e.shape[0], C.byref(h)))
+    return GraphIndex(h, ctx)
+
+
 def complete_edges(edges, home, roles=None, partitions: Optional[int] = None, hops: int = 1,
-                   ctx: Optional[Context] = None) -> List[GraphPartition]:
-    """complete_edges (completion.cpp:130-171) on the device for a stream with
-    dense external ids; home = SPRING's node -> partition map."""
+                   ctx: Optional[Context] = None, index: Optional[GraphIndex] = None) -> List[GraphPartition]:
+    """complete_edges (completion.cpp:130-171) on the device.  Without `index`
+    the external ids must be dense (home/roles indexed by ext id); with a
+    GraphIndex any 64-bit ids work and home/roles are indexed by dense id."""
     ctx = ctx or default_context()
     e = np.ascontiguousarray(np.asarray(edges, np.uint64).reshape(-1, 2))
     h = np.ascontiguousarray(home, np.uint32)
     r = None if roles is None else np.ascontiguousarray(roles, np.uint8)
     p = int(partitions if partitions is not None else (int(h.max()) + 1 if h.size else 0))
     c = C.c_void_p()
-    check(lib.catgnn_complete_edges(ctx.handle, _ptr(e), e.shape[0], _ptr(h), _ptr(r), h.size, p, hops,
-                                    C.byref(c)))
+    if index is None:
+        check(lib.catgnn_complete_edges(ctx.handle, _ptr(e), e.shape[0], _ptr(h), _ptr(r), h.size, p, hops,
+                                        C.byref(c)))
+    else:
+        if h.size != index.num_nodes:
+            raise DataError("home map does not cover the node set")
+        check(lib.catgnn_complete_edges_indexed(ctx.handle, index.handle, _ptr(e), e.shape[0], _ptr(h), _ptr(r),
+                                                p, hops, C.byref(c)))
     try:
         out = []
         for s in range(p):

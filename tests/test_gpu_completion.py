@@ -67,3 +67,64 @@ def test_device_completion_errors():
     # isolated owned node: present in its home's table without edges (completion.cpp:37)
     parts = gp.complete_edges(e, np.array([0, 0, 0, 1], np.uint32), None, 2)
     assert parts[1].ext.tolist() == [3] and parts[1].owner.tolist() == [1] and parts[1].edges.shape == (0, 2)
+
+
+def sparse_id_stream(rng, n, m, self_loops=True):
+    """Records over arbitrary 64-bit external ids (not dense, not sorted)."""
+    ids = rng.choice(np.uint64(1) << np.uint64(62), size=n, replace=False).astype(np.uint64)
+    a = rng.integers(0, n, size=m)
+    b = rng.integers(0, n, size=m)
+    if not self_loops:
+        b = np.where(a == b, (b + 1) % n, b)
+    return ids, np.stack([ids[a], ids[b]], 1).astype(np.uint64)
+
+
+@pytest.mark.parametrize("n,m,seed", [(1, 1, 0), (50, 200, 1), (3000, 20000, 2), (40000, 300000, 3)])
+def test_device_compute_degrees_matches_reference(tmp_path, n, m, seed):
+    """compute_degrees (edge_stream.cpp:192-215): first-seen interning order,
+    degrees with self-loops counting 2, record and self-loop counts."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    rng = np.random.default_rng(seed)
+    _, e = sparse_id_stream(rng, n, m)
+    f = os.path.join(str(tmp_path), "edges.bin")
+    with open(f, "wb") as fh:
+        fh.write(b"EDG1")
+        e.tofile(fh)
+    d2e, deg, rm, rsl = ref.compute_degrees(f, 2 * m)
+    idx = gp.compute_degrees(e)
+    assert np.array_equal(idx.dense_to_ext, d2e)
+    assert np.array_equal(idx.degree, deg)
+    assert (idx.num_edges, idx.num_self_loops) == (rm, rsl)
+
+
+@pytest.mark.parametrize("p,hops", [(2, 1), (4, 1), (3, 2)])
+def test_indexed_completion_matches_reference(tmp_path, p, hops):
+    """complete_edges over arbitrary 64-bit ids through the device index, vs the
+    reference pipeline (compute_degrees -> SPRING -> complete_edges ->
+    write_partitions) on the same EDG1 stream."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    rng = np.random.default_rng(10 + p + hops)
+    _, e = sparse_id_stream(rng, 2500, 12000, self_loops=False)
+    e = np.concatenate([e, e[:1500, ::-1]])  # reversed duplicates
+    d = str(tmp_path)
+    f = os.path.join(d, "edges.bin")
+    with open(f, "wb") as fh:
+        fh.write(b"EDG1")
+        e.tofile(fh)
+    art = os.path.join(d, f"art_{p}_{hops}")
+    ref.partition(f, art, p, hops=hops)
+    ref_parts = [read_part(art, s) for s in range(p)]
+    idx = gp.compute_degrees(e)
+    dense_of = {int(x): i for i, x in enumerate(idx.dense_to_ext)}
+    home = np.full(idx.num_nodes, p, np.uint32)
+    for s, (_, ext, own, _) in enumerate(ref_parts):
+        for x in ext[own == 1]:
+            home[dense_of[int(x)]] = s
+    assert np.all(home < p)
+    parts = gp.complete_edges(e, home, None, p, hops=hops, index=idx)
+    for s in range(p):
+        edges, ext, own, role = ref_parts[s]
+        assert np.array_equal(parts[s].edges, edges), s
+        assert np.array_equal(parts[s].ext, ext), s
+        assert np.array_equal(parts[s].owner, own), s
+        assert np.array_equal(parts[s].role, role), s
