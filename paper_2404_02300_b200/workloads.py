@@ -74,6 +74,10 @@ WORKLOADS = {
     "cfg1_sage": Workload("cfg1_sage", "sage", 2, 256, 16, 524_288, 64, 8, 2, (0.70, 0.15, 0.15), seed=1),
     # configs[2]: 3-layer GraphSAGE, ogbn-products-shaped (2.45M nodes, 62M edges, 100-d, 47 classes)
     "products_sage": Workload("products_sage", "sage", 3, 256, 22, 61_859_140, 100, 47, 8, (0.08, 0.02, 0.90)),
+    # configs[3] scaled to one B200: GIN-sum on a papers100M-shaped RMAT stream (128-d, 172
+    # classes, papers' ~14.5 records per node and 1%/0.1%/0.2% roles), 2^24 ids, 220M records, p=8
+    "papers_gin_s24": Workload("papers_gin_s24", "gin", 2, 256, 24, 220_000_000, 128, 172, 8,
+                               (0.01, 0.001, 0.002), seed=4),
     # small smoke workload
     "tiny_gcn": Workload("tiny_gcn", "gcn", 2, 64, 12, 40_000, 32, 8, 4, (0.6, 0.2, 0.2), seed=3),
 }
@@ -106,7 +110,18 @@ def prepare(w: Workload, log=print) -> dict:
     home, tau = spring_homes(edge_file, n, w.partitions, beta=w.beta, tau_vol=w.tau_vol, seed=0)
     t2 = time.time()
     labels, roles = synth.node_meta(n, w.classes, *w.fracs, seed=w.seed)
-    parts = synth.complete_edges(e, home, roles, w.partitions)
+    parts = None
+    if w.edges >= 100_000_000:
+        # device completion (csrc/completion.cu, bit-exact with the reference) when a GPU is here
+        try:
+            import torch
+            if torch.cuda.is_available():
+                from . import gnnpart as gp
+                parts = gp.complete_edges(e, home, roles, w.partitions)
+        except Exception as ex:  # pragma: no cover
+            log(f"[prep] device completion unavailable ({ex}); NumPy completion")
+    if parts is None:
+        parts = synth.complete_edges(e, home, roles, w.partitions)
     t3 = time.time()
     for i, p in enumerate(parts):
         np.save(os.path.join(d, f"p{i}_edges.npy"), p.edges)
