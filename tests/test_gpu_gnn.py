@@ -163,3 +163,29 @@ def test_config5_partition_sync_sweep(sweep_ds, k, s):
     for (e1, s1, v1, t1), (e2, s2, v2, t2) in zip(res.history, want["history"]):
         assert (e1, s1) == (e2, s2)
         assert abs(v1 - v2) <= tol_v and abs(t1 - t2) <= tol_t, (res.history, want["history"])
+
+
+def test_e2e_feature_gather_path_identical(tmp_path_factory):
+    """bench.py's e2e path (global feature store -> device row gather, on a copy
+    stream) trains exactly like shards built with their features resident."""
+    from paper_2404_02300_b200 import gnnpart as gp, gnn, synth
+    ds = make_dataset(tmp_path_factory.mktemp("e2e"), scale=10, edges=4000, dim=20, classes=5, seed=8)
+    art = make_artifact(ds, p=2)
+    td = ref.TrainingData(art)
+    X = ds["X"]
+    ctx = gp.Context(0)
+    copy_ctx = gp.Context(0)
+    store = gp.FeatureStore(X.shape[0], X.shape[1], copy_ctx)
+    store.upload(X)
+    res = []
+    for mode in ("resident", "gathered"):
+        data = gp.load_training_data(art, ctx=ctx)
+        if mode == "gathered":
+            for s in data.shards:
+                s.upload_features(np.zeros((s.rows, X.shape[1]), np.float32))
+                s.gather_features(store)
+        counts = [int(s.info.n_train) for s in data.shards]
+        r = gnn.distributed_train("gcn", data.shards, counts, 1, 3, 2, 32, 5, seed=2, ctx=ctx)
+        res.append(r)
+    assert res[0].losses == res[1].losses
+    assert np.array_equal(res[0].params, res[1].params)
