@@ -129,23 +129,25 @@ def load_ncu_traffic(workload):
     return None
 
 
-def reference_jobs(prep, parts_idx, budget_edges):
-    """Bounded samples for the reference CPU path: partition CSR from the
-    reference's own build_adjacency; the first R rows keep their neighbour
-    lists (~budget_edges local edges), later rows have none."""
+def reference_jobs(prep, samples, budget_edges):
+    """Bounded samples for the reference CPU path: samples = [(partition,
+    block)]; the partition CSR comes from the reference's own build_adjacency
+    and rows [R0, R1) holding the block-th ~budget_edges local edges keep their
+    neighbour lists (other rows have none, as gather sources only)."""
     from oracle import ref
-    jobs = []
-    for i in parts_idx:
-        d = prep["dir"]
-        edges = np.load(os.path.join(d, f"p{i}_edges.npy"))
-        ext = np.load(os.path.join(d, f"p{i}_ext.npy"))
-        local = np.searchsorted(ext, edges.ravel()).astype(np.uint32).reshape(-1, 2)
-        rows = ext.size
-        off, nb = ref.build_adjacency(rows, local)
-        R = max(1, min(int(np.searchsorted(off, budget_edges)), rows))
-        off_s = off.copy()
-        off_s[R + 1:] = off[R]
-        jobs.append((rows, off_s, nb[: off[R]].copy(), int(off[R])))
+    jobs, csr = [], {}
+    for i, blk in samples:
+        if i not in csr:
+            d = prep["dir"]
+            edges = np.load(os.path.join(d, f"p{i}_edges.npy"))
+            ext = np.load(os.path.join(d, f"p{i}_ext.npy"))
+            local = np.searchsorted(ext, edges.ravel()).astype(np.uint32).reshape(-1, 2)
+            csr[i] = (ext.size,) + tuple(ref.build_adjacency(ext.size, local))
+        rows, off, nb = csr[i]
+        R0 = min(int(np.searchsorted(off, blk * budget_edges)), rows)
+        R1 = max(R0 + 1, min(int(np.searchsorted(off, (blk + 1) * budget_edges)), rows))
+        off_s = np.clip(off, off[R0], off[R1]) - off[R0]
+        jobs.append((rows, off_s, nb[off[R0]: off[R1]].copy(), int(off[R1] - off[R0])))
     return jobs
 
 
@@ -155,7 +157,7 @@ def cpu_reference_rate(w, jobs, seed=0):
     this workload's epoch schedule; one host thread per partition sample (the
     reference is single-threaded and its workers are schedule-independent)."""
     from oracle import ref
-    widths = [(x + 3) // 4 * 4 for x in w.passes()]
+    widths = w.passes()
     results = [None] * len(jobs)
 
     def run(j):
@@ -176,9 +178,9 @@ def cpu_reference_rate(w, jobs, seed=0):
         th.join()
     edges = sum(r[0] for r in results)
     wall = max(r[1] for r in results)
-    sample = (f"reference sgc_propagate (1 hop) over the first ~{jobs[0][3]} local edges of "
-              f"{len(jobs)} partition(s), one pass per epoch width {widths}, f64 column-major, "
-              f"{len(jobs)} host thread(s)")
+    sample = (f"reference sgc_propagate (1 hop) over {len(jobs)} row blocks of ~{jobs[0][3]} local edges "
+              f"(distinct rows of the partitions, round-robin), one pass per epoch width {widths}, f64 "
+              f"column-major (Eigen MatrixXd), {len(jobs)} host thread(s), one block each")
     return edges / wall, len(jobs), sample
 
 
@@ -186,8 +188,10 @@ def run_reference(args, w, prep):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    threads = min(os.cpu_count() or 1, w.partitions)
-    jobs = reference_jobs(prep, list(range(threads)), args.ref_edges)
+    # every host thread: the reference is single-threaded and its workers are
+    # schedule-independent, so blocks of the partitions run side by side
+    threads = os.cpu_count() or 1
+    jobs = reference_jobs(prep, [(t % w.partitions, t // w.partitions) for t in range(threads)], args.ref_edges)
     vals = []
     for s in range(args.warmup + args.steps):
         v, cores, sample = cpu_reference_rate(w, jobs, seed=s)
@@ -421,7 +425,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample = cpu_reference_rate(w, reference_jobs(prep, [0], args.ref_edges))
+        v, cores, sample = cpu_reference_rate(w, reference_jobs(prep, [(0, 0)], args.ref_edges))
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
 
     if rank == 0:
