@@ -321,7 +321,9 @@ def main():
         for r, s in zip(reps, shards):
             if e2e:
                 s.gather_features(stores[t % 2])
-            losses.append(r.train_step(s, want_loss=e2e))
+            r.train_step(s, want_loss=False)
+        if e2e:  # the step's result back on the host: one sync after every replica's step
+            losses = [r.last_loss() for r in reps]
         state["it"] += 1
         if state["it"] % args.sync == 0:
             average()
@@ -421,7 +423,8 @@ def main():
                "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
                "path": "catgnn_features_upload (global features, pinned H2D on a copy stream, double-buffered: "
                        "step t+1's copy overlaps step t) + per partition catgnn_shard_gather_features + "
-                       "catgnn_model_train_step + loss D2H; model averaging"}
+                       "catgnn_model_train_step; every partition's loss D2H once per step "
+                       "(catgnn_model_last_loss); model averaging"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

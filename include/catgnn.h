@@ -266,6 +266,9 @@ int catgnn_model_get_grads(catgnn_model m, float* out);
  * the shard's train rows (mean CE), then one optimizer step.  loss may be NULL
  * (then no device->host read happens). */
 int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss);
+/* Loss of the last train_step (computed on the device either way); lets a
+ * caller run several replicas' steps back to back and sync once. */
+int catgnn_model_last_loss(catgnn_model m, double* loss);
 /* Forward + backward only (no update); gradients readable by get_grads. */
 int catgnn_model_forward_backward(catgnn_model m, catgnn_shard s, double* loss);
 /* Forward only; logits rows x classes into out (host) when out != NULL;

@@ -94,6 +94,7 @@ def _load():
         "catgnn_model_copy_params": (C.c_int, [vp, vp]),
         "catgnn_model_get_grads": (C.c_int, [vp, vp]),
         "catgnn_model_train_step": (C.c_int, [vp, vp, P(f64)]),
+        "catgnn_model_last_loss": (C.c_int, [vp, P(f64)]),
         "catgnn_model_forward_backward": (C.c_int, [vp, vp, P(f64)]),
         "catgnn_model_forward": (C.c_int, [vp, vp, vp, C.c_int, P(f64)]),
         "catgnn_model_export": (C.c_int, [vp, u32, C.c_int, vp, P(u32)]),

@@ -268,6 +268,8 @@ struct catgnn_model_s {
   uint64_t last_rows = 0;
   catgnn_shard last_shard = nullptr;
   double last_loss = 0.0;
+  DevBuf<double> loss_dev;  // sum of the last step's per-row losses (read lazily)
+  uint64_t loss_rows = 0;   // train rows of that step
 };
 
 namespace catgnn {
@@ -490,7 +492,10 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   const uint64_t ntr = S->h_train.size();
   double loss = 0.0;
   double* row_loss = ctx->scratch_buf<double>("row_loss", std::max<uint64_t>(1, ntr));
-  double* loss_dev = ctx->scratch_buf<double>("loss_dev", 1);
+  if (!M->loss_dev.p) M->loss_dev.alloc(1);
+  double* loss_dev = M->loss_dev.p;
+  CG_CUDA(cudaMemsetAsync(loss_dev, 0, 8, st));
+  M->loss_rows = ntr;
   // GCN transform-first: the last layer's backward aggregation gathers
   // dinv * dZ, produced here by K4 instead of per edge in K2
   float* dZs = nullptr;
@@ -764,6 +769,22 @@ int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss) {
     optimizer_step(m);
     if (loss) *loss = l;
     m->last_shard = s;
+  });
+}
+
+// Loss of the model's last train step (mean CE over its train rows), read
+// back now: a caller training several replicas per step issues every
+// train_step without a host sync and reads the losses once at the end.
+int catgnn_model_last_loss(catgnn_model m, double* loss) {
+  return guarded([&] {
+    check_model(m);
+    if (!loss) throw ConfigError("null argument");
+    *loss = 0.0;
+    if (!m->loss_dev.p || m->loss_rows == 0) return;
+    double sum = 0.0;
+    CG_CUDA(cudaMemcpyAsync(&sum, m->loss_dev.p, 8, cudaMemcpyDeviceToHost, m->ctx->stream));
+    CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    *loss = sum / (double)m->loss_rows;
   });
 }
 

@@ -81,6 +81,12 @@ class GNNModel:
         check(lib.catgnn_model_train_step(self.handle, shard.handle, C.byref(loss) if want_loss else None))
         return loss.value if want_loss else None
 
+    def last_loss(self) -> float:
+        """Loss of the last train_step, read back now (one sync)."""
+        loss = C.c_double()
+        check(lib.catgnn_model_last_loss(self.handle, C.byref(loss)))
+        return loss.value
+
     def forward_backward(self, shard: Shard) -> float:
         loss = C.c_double()
         check(lib.catgnn_model_forward_backward(self.handle, shard.handle, C.byref(loss)))

@@ -189,3 +189,15 @@ def test_e2e_feature_gather_path_identical(tmp_path_factory):
         res.append(r)
     assert res[0].losses == res[1].losses
     assert np.array_equal(res[0].params, res[1].params)
+
+
+def test_last_loss_matches_synchronous_loss(graph):
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    s, _ = make(gp, graph, 16, 4)
+    a = GNNModel("gcn", 2, 16, 32, 4, seed=1)
+    b = GNNModel("gcn", 2, 16, 32, 4, seed=1)
+    for _ in range(3):
+        la = a.train_step(s, want_loss=True)
+        b.train_step(s, want_loss=False)
+        assert b.last_loss() == la
