@@ -3,7 +3,8 @@
 // to the north-star layers (SGC mean-with-self, GCN-norm, SAGE-mean, GIN-sum).
 //
 //   out[r] = epi( post(deg_r) * ( self * pre[r]*in[r] + sum_{j in N(r)} pre[j]*in[j] ) )
-//   epi    = (+ residual[r]) (+ bias) (ReLU) (* [mask[r] > 0])
+//   epi    = (+ residual[r]) (+ bias) (ReLU) (* mask bit (r, c)); optionally
+//            also writes the bits (out > 0) for the backward's ReLU mask
 //
 // Roofline: HBM-bound gather.  Algorithmic bytes per pass =
 //   nnz*(4 + 4*width) + rows*(4*width*(1+self) + 8)
@@ -49,9 +50,11 @@ struct AggKernelArgs {
   const float* __restrict__ residual;
   uint32_t res_ld, res_col;
   int relu;
-  const float* __restrict__ mask;
-  uint32_t mask_ld, mask_col;
   int stream_hint;  // column indices and output rows with evict-first hints
+  const uint32_t* __restrict__ mask_bits;  // ReLU-backward mask, 1 bit per column
+  uint32_t mask_words;                     // 32-bit words per row
+  uint32_t* __restrict__ bits_out;         // output > 0 bits (forward ReLU layers)
+  uint32_t bits_words;
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -89,15 +92,20 @@ __device__ __forceinline__ float post_scale(int norm, float deg) {
 // Final epilogue for one output row.  `acc` holds the neighbour sum for the
 // float4 columns c4 = li + LPN*q.
 // selfv: the row's own input columns when already loaded (light units).
-template <int VPL, int LPN>
+template <int VPL, int LPN, bool BITS>
 __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, float deg,
                                              const float4 (&acc)[VPL], int li,
                                              const float4 (*selfv)[VPL] = nullptr) {
+  // lanes [0, LPN) run this together (bit words are assembled across them)
+  constexpr unsigned kLanes = LPN == 32 ? 0xffffffffu : ((1u << LPN) - 1u);
+  constexpr int kGroup = LPN < 8 ? LPN : 8;  // lanes whose nibbles form one 32-bit word
   const float post = post_scale(p.norm, deg);
   const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
+  uint32_t nib[VPL];  // (out > 0) per column of each float4, for bits_out
 #pragma unroll
   for (int q = 0; q < VPL; ++q) {
     const uint32_t c4 = li + LPN * q;
+    nib[q] = 0;
     if (c4 >= p.w4) continue;
     float4 a = acc[q];
     if (p.self) fma4(a, selfs, selfv ? (*selfv)[q] : ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4));
@@ -107,14 +115,25 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
     if (p.relu) {
       a.x = fmaxf(a.x, 0.f); a.y = fmaxf(a.y, 0.f); a.z = fmaxf(a.z, 0.f); a.w = fmaxf(a.w, 0.f);
     }
-    if (p.mask) {
-      float4 m = ldg4(p.mask + (size_t)r * p.mask_ld + p.mask_col + c4 * 4);
-      a.x = m.x > 0.f ? a.x : 0.f; a.y = m.y > 0.f ? a.y : 0.f;
-      a.z = m.z > 0.f ? a.z : 0.f; a.w = m.w > 0.f ? a.w : 0.f;
+    if (BITS && p.mask_bits) {  // ReLU backward: bit (r, col) of the forward activation
+      const uint32_t m = __ldg(p.mask_bits + (size_t)r * p.mask_words + c4 / 8) >> ((c4 % 8) * 4);
+      a.x = (m & 1u) ? a.x : 0.f; a.y = (m & 2u) ? a.y : 0.f;
+      a.z = (m & 4u) ? a.z : 0.f; a.w = (m & 8u) ? a.w : 0.f;
     }
+    if (BITS) nib[q] = (a.x > 0.f) | ((a.y > 0.f) << 1) | ((a.z > 0.f) << 2) | ((a.w > 0.f) << 3);
     float4* dst = reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4);
     if (p.stream_hint) __stcs(dst, a);  // evict-first: keep L2 for the gathered rows
     else *dst = a;
+  }
+  if (BITS && p.bits_out) {  // 1 bit per output element (> 0): the next backward's ReLU mask
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const uint32_t c4 = li + LPN * q;
+      uint32_t w = nib[q] << ((c4 % 8) * 4);
+#pragma unroll
+      for (int m = 1; m < kGroup; m <<= 1) w |= __shfl_xor_sync(kLanes, w, m);
+      if (c4 < p.w4 && c4 % 8 == 0) p.bits_out[(size_t)r * p.bits_words + c4 / 8] = w;
+    }
   }
 }
 
@@ -169,7 +188,7 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
 // 32 rows per coalesced load and each row's own input row (self term) is
 // requested together with its first neighbour batch.  Per row the G lane
 // groups split the neighbours, UNROLL batches in flight, xor-shuffle reduce.
-template <int VPL, int LPN, bool PRE>
+template <int VPL, int LPN, bool PRE, bool BITS>
 __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, int64_t r1, int lane) {
   constexpr int G = 32 / LPN;
   constexpr int UNROLL0 = VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8);
@@ -249,14 +268,14 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
       for (int m = LPN; m < 32; m <<= 1)
 #pragma unroll
         for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], m));
-      if (writer) epilogue_row<VPL, LPN>(p, r, (float)(e1 - e0), acc, li, &selfv);
+      if (writer) epilogue_row<VPL, LPN, BITS>(p, r, (float)(e1 - e0), acc, li, &selfv);
     }
   }
 }
 
 // Persistent unit loop shared by both aggregation kernels: warps pull work
 // units from the atomic counter (the next one prefetched by lane 0).
-template <int VPL, int LPN, bool PRE>
+template <int VPL, int LPN, bool PRE, bool BITS>
 __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
   const int lane = threadIdx.x & 31;
   const int li = lane % LPN;
@@ -269,7 +288,7 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
     if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
     const int4 w = __ldg(p.units + u);
     if (w.z < 0) {
-      light_unit<VPL, LPN, PRE>(p, w.x, w.y, lane);
+      light_unit<VPL, LPN, PRE, BITS>(p, w.x, w.y, lane);
     } else {
       float4 acc[VPL];
       const int64_t r = w.x;
@@ -290,9 +309,11 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
   }
 }
 
-template <int VPL, int LPN, bool PRE, int MINB>
+// BITS: the epilogue reads / writes ReLU bit masks (a separate instantiation
+// keeps the plain passes' register budget: the narrow kernel runs at 64).
+template <int VPL, int LPN, bool PRE, int MINB, bool BITS>
 __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
-  unit_loop<VPL, LPN, PRE>(p);
+  unit_loop<VPL, LPN, PRE, BITS>(p);
 }
 
 // One warp per split row: sum its chunk partials in chunk order, then the
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
       add4(acc[q], acc4[0][q]);
     }
     const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
-    epilogue_row<VPL, 32>(p, r, deg, acc, lane);
+    epilogue_row<VPL, 32, true>(p, r, deg, acc, lane);
   }
 }
 
@@ -357,52 +378,33 @@ int env_int(const char* name, int dflt) {
 }
 
 template <int VPL, int LPN>
-AggFn pick_pre(bool pre) {
-  // narrow rows run 4 CTAs/SM (<= 64 registers; CATGNN_AGG_NARROW_MINB=3 for 3)
-  static const int minb = env_int("CATGNN_AGG_MINB", 3);
-  static const int minb_narrow = env_int("CATGNN_AGG_NARROW_MINB", 4);
-  if (LPN < 32 && minb_narrow >= 4) return pre ? agg_kernel<VPL, LPN, true, 4> : agg_kernel<VPL, LPN, false, 4>;
-  if (minb >= 3) return pre ? agg_kernel<VPL, LPN, true, 3> : agg_kernel<VPL, LPN, false, 3>;
-  return pre ? agg_kernel<VPL, LPN, true, 2> : agg_kernel<VPL, LPN, false, 2>;
+AggFn pick_pre(bool pre, bool bits) {
+  // 3 CTAs/SM for rows >= 128 floats, 4 for plain narrow rows (<= 80 / 64 registers)
+  constexpr int MINB = LPN < 32 ? 4 : 3;
+  if (bits) return pre ? agg_kernel<VPL, LPN, true, 3, true> : agg_kernel<VPL, LPN, false, 3, true>;
+  return pre ? agg_kernel<VPL, LPN, true, MINB, false> : agg_kernel<VPL, LPN, false, MINB, false>;
 }
 
 // Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
 constexpr uint32_t kMaxSlab4 = 256;
 
-int narrow_mode() {
-  static int m = [] {
-    const char* s = std::getenv("CATGNN_NARROW");
-    return s ? std::atoi(s) : 0;
-  }();
-  return m;
-}
 
-AggFn pick_kernel(uint32_t w4, bool pre, int* lpn_out) {
-  if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre); }
-  if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre); }
-  if (w4 <= 16) {
-    // narrow rows: lanes per neighbour x float4 per lane
-    int mode = narrow_mode();
-    if (mode == 0) mode = 3;  // 8 lanes x 2 float4, 4 CTAs/SM: fastest for the 41/44/48-wide class rows
-    switch (mode) {
-      case 1: *lpn_out = 16; return pick_pre<1, 16>(pre);
-      case 2: *lpn_out = 4; return pick_pre<4, 4>(pre);
-      case 6:
-        if (w4 <= 12) { *lpn_out = 4; return pick_pre<3, 4>(pre); }  // 8 neighbours per load
-        [[fallthrough]];
-      default: *lpn_out = 8; return pick_pre<2, 8>(pre);
-    }
-  }
+AggFn pick_kernel(uint32_t w4, bool pre, bool bits, int* lpn_out) {
+  // lanes per neighbour x float4 per lane; the narrow class rows (41-48 floats)
+  // use 8 lanes x 2 float4 (4 neighbours per load instruction)
+  if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre, bits); }
+  if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre, bits); }
+  if (w4 <= 16) { *lpn_out = 8; return pick_pre<2, 8>(pre, bits); }
   *lpn_out = 32;
   switch ((w4 + 31) / 32) {
-    case 1: return pick_pre<1, 32>(pre);
-    case 2: return pick_pre<2, 32>(pre);
-    case 3: return pick_pre<3, 32>(pre);
-    case 4: return pick_pre<4, 32>(pre);
-    case 5: return pick_pre<5, 32>(pre);
-    case 6: return pick_pre<6, 32>(pre);
-    case 7: return pick_pre<7, 32>(pre);
-    default: return pick_pre<8, 32>(pre);
+    case 1: return pick_pre<1, 32>(pre, bits);
+    case 2: return pick_pre<2, 32>(pre, bits);
+    case 3: return pick_pre<3, 32>(pre, bits);
+    case 4: return pick_pre<4, 32>(pre, bits);
+    case 5: return pick_pre<5, 32>(pre, bits);
+    case 6: return pick_pre<6, 32>(pre, bits);
+    case 7: return pick_pre<7, 32>(pre, bits);
+    default: return pick_pre<8, 32>(pre, bits);
   }
 }
 
@@ -435,7 +437,7 @@ int blocks_per_sm(AggFn fn) {
 void aggregate(catgnn_shard_s* s, const AggArgs& a) {
   catgnn_ctx ctx = s->ctx;
   if (a.width % 4 || a.in_ld % 4 || a.out_ld % 4 || a.in_col % 4 || a.out_col % 4 ||
-      (a.residual && (a.res_ld % 4 || a.res_col % 4)) || (a.mask && (a.mask_ld % 4 || a.mask_col % 4)))
+      (a.residual && (a.res_ld % 4 || a.res_col % 4)))
     throw ConfigError("aggregation widths/strides must be multiples of 4 floats");
   if (a.in == a.out && a.in) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
@@ -468,13 +470,16 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.res_ld = a.res_ld;
     p.res_col = a.res_col + c4 * 4;
     p.relu = a.relu;
-    p.mask = a.mask;
-    p.mask_ld = a.mask_ld;
-    p.mask_col = a.mask_col + c4 * 4;
+    if ((a.mask_bits || a.bits_out) && c4 % 8)
+      throw ConfigError("bit masks need 32-column aligned aggregation slabs");
+    p.mask_bits = a.mask_bits ? a.mask_bits + c4 / 8 : nullptr;
+    p.mask_words = a.mask_words;
+    p.bits_out = a.bits_out ? a.bits_out + c4 / 8 : nullptr;
+    p.bits_words = a.bits_words;
     static const int hint = env_int("CATGNN_AGG_HINT", 1);
     p.stream_hint = hint;
     int lpn = 32;
-    AggFn fn = pick_kernel(w4, a.pre != nullptr, &lpn);
+    AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
     int t = ctx->begin_timed(0);
     const int bps = blocks_per_sm(fn);

@@ -17,7 +17,7 @@
 //               MMA issues lo*hi + hi*lo + hi*hi (~fp32 accuracy)
 //   warps 6..9  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
 //               32*(w%4)..+31 = tile rows), fused row-scale / bias / ReLU /
-//               ReLU-backward mask, 128-bit stores — or raw split-K partials
+//               ReLU-backward bit mask, staged line-coalesced stores — or raw split-K partials
 //               that gemm_reduce_kernel sums in split order (deterministic).
 // Tail rows/columns and K past the tensor extent are zero-filled by TMA.
 #include <cuda.h>
@@ -208,7 +208,7 @@ __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint3
   if (e.rowscale && col >= e.scale_col_begin) v *= __ldg(e.rowscale + row);
   if (e.bias) v += __ldg(e.bias + col);
   if (e.relu) v = fmaxf(v, 0.f);
-  if (e.mask && !(__ldg(e.mask + (size_t)row * e.mask_ld + e.mask_col + col) > 0.f)) v = 0.f;
+  if (e.mask_bits && !((__ldg(e.mask_bits + (size_t)row * e.mask_words + col / 32) >> (col % 32)) & 1u)) v = 0.f;
   return v;
 }
 
@@ -456,12 +456,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t col0 = n0 + c;
         if (col0 >= args.N) continue;  // warp-uniform
-        // Plain outputs (forward GEMMs: row scale / bias / ReLU) are staged
-        // through shared memory so a warp writes whole 128-byte lines (its lanes
-        // own 32 different rows).  Masked and split-K outputs store directly:
-        // their kernels are epilogue-bound and the extra shared-memory round
-        // trips cost more than the coalescing gains (measured).
-        if (col0 + 32 <= args.N && !e.partial && !e.mask) {
+        // Outputs are staged through shared memory so a warp writes whole
+        // 128-byte lines (its lanes own 32 different rows); the ReLU-backward
+        // mask is one 32-bit word per row and chunk, and ReLU layers emit the
+        // same word for their own backward (bits_out).
+        if (col0 + 32 <= args.N && !e.partial) {
+          const uint32_t mw = (e.mask_bits && row_ok) ? __ldg(e.mask_bits + (size_t)row * e.mask_words + col0 / 32)
+                                                     : 0xffffffffu;
+          uint32_t bw = 0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -473,8 +475,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (e.relu) {
               o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
             }
+            if (e.mask_bits) {
+              const uint32_t nib = mw >> (4 * i);
+              o.x = (nib & 1u) ? o.x : 0.f; o.y = (nib & 2u) ? o.y : 0.f;
+              o.z = (nib & 4u) ? o.z : 0.f; o.w = (nib & 8u) ? o.w : 0.f;
+            }
+            bw |= ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3)) << (4 * i);
             T[lane * kTileLd4 + i] = o;
           }
+          if (e.bits_out && row_ok) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -495,27 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
         }
-        if (!e.partial && col0 + 32 <= args.N) {  // masked: ReLU backward
-          float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
-          const float* mrow = e.mask + (size_t)row * e.mask_ld + e.mask_col + col0;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            if (e.rowscale && col0 + i >= e.scale_col_begin) { o.x *= rs; o.y *= rs; o.z *= rs; o.w *= rs; }
-            if (e.bias) {
-              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + col0 + i));
-              o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
-            }
-            if (e.relu) {
-              o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
-            }
-            const float4 mm = __ldg(reinterpret_cast<const float4*>(mrow + i));
-            o.x = mm.x > 0.f ? o.x : 0.f; o.y = mm.y > 0.f ? o.y : 0.f;
-            o.z = mm.z > 0.f ? o.z : 0.f; o.w = mm.w > 0.f ? o.w : 0.f;
-            *reinterpret_cast<float4*>(dst + i) = o;
-          }
-          continue;
-        }
         if (!row_ok) continue;
         if (e.partial) {
           float* dst = e.partial + ((size_t)z * args.M + row) * args.N + col0;
@@ -525,9 +513,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
+        uint32_t bw = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (col0 + i < args.N) dst[i] = apply_epi(e, row, col0 + i, v[i]);
+          if (col0 + i < args.N) {
+            const float o = apply_epi(e, row, col0 + i, v[i]);
+            dst[i] = o;
+            bw |= (uint32_t)(o > 0.f) << i;
+          }
+        if (e.bits_out) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -673,7 +667,8 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   splits = std::max<uint32_t>(1, splits);
   const uint32_t kbps = std::max<uint32_t>(1, (nkb + splits - 1) / splits);
   splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
-  if ((epi.mask && (epi.mask_ld % 4 || epi.mask_col % 4)) || (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15)))
+  if (epi.bits_out && splits > 1) throw ConfigError("GEMM bit output needs an unsplit K");
+  if (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15))
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
   const uint32_t b_stage = BNh * BK * 4;

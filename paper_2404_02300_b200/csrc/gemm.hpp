@@ -6,7 +6,8 @@ namespace catgnn {
 
 // Fused epilogue of K3, applied per output element (row, col):
 //   v = acc; v *= rowscale[row] (cols >= scale_col_begin); v += bias[col];
-//   v = relu(v); v = mask[row][mask_col+col] > 0 ? v : 0;  out[row][out_col+col] = v
+//   v = relu(v); v = bit(mask_bits, row, col) ? v : 0;  out[row][out_col+col] = v
+//   bits_out: bit (row, col) = v > 0 (the ReLU mask of this output's backward)
 struct GemmEpi {
   float* out = nullptr;
   uint32_t ld_out = 0, out_col = 0;
@@ -14,8 +15,10 @@ struct GemmEpi {
   uint32_t scale_col_begin = 0;
   const float* bias = nullptr;
   int relu = 0;
-  const float* mask = nullptr;
-  uint32_t mask_ld = 0, mask_col = 0;
+  const uint32_t* mask_bits = nullptr;  // 32-bit words per row: mask_words
+  uint32_t mask_words = 0;
+  uint32_t* bits_out = nullptr;
+  uint32_t bits_words = 0;
   float* partial = nullptr;  // internal (split-K workspace)
 };
 

@@ -405,7 +405,13 @@ struct Bufs {
   uint32_t mid_ld;
   float* out;       // H_l
   uint32_t out_ld;
+  uint32_t* bits = nullptr;  // H_l > 0, one bit per column (ReLU layers): the backward's mask
+  uint32_t bits_words = 0;
 };
+
+uint32_t* act_bits(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t words) {
+  return ctx->scratch_buf<uint32_t>(name, std::max<uint64_t>(1, rows) * words);
+}
 
 std::string nm(const char* base, size_t l) { return std::string(base) + std::to_string(l); }
 
@@ -427,6 +433,10 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
     b.in_ld = in_ld;
     b.out_ld = L.D_out;
     b.out = act(ctx, nm("H", l), rows, b.out_ld, fresh);
+    if (!last) {
+      b.bits_words = (L.D_out + 31) / 32;
+      b.bits = act_bits(ctx, nm("Hbits", l), rows, b.bits_words);
+    }
     const float* bias = M->params.p + L.off_b;
     if (sage && L.agg_first) {
       b.mid_ld = 2 * L.K_in;
@@ -437,6 +447,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       a.width = L.K_in; a.norm = kNormMean;
       aggregate(S, a);
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
+      e.bits_out = b.bits; e.bits_words = b.bits_words;
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.w_cols, e, 1, kFwdPrecision);
     } else if (sage) {
       b.mid_ld = 2 * L.D_out;  // [P_s (D_out, padded) | P_n (d_out) | zero padding]
@@ -448,6 +459,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out; a.norm = kNormMean;
       a.residual = b.mid; a.res_ld = b.mid_ld; a.res_col = 0;
       a.bias = bias; a.relu = !last;
+      a.bits_out = b.bits; a.bits_words = b.bits_words;
       aggregate(S, a);
     } else if (L.agg_first) {  // GCN / GIN aggregate-first
       b.mid_ld = L.K_in;
@@ -457,6 +469,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       a.self = 1; a.norm = agg_norm(M); a.pre = gcn ? S->dinv.p : nullptr;
       aggregate(S, a);
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
+      e.bits_out = b.bits; e.bits_words = b.bits_words;
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN transform-first
       b.mid_ld = L.D_out;
@@ -466,6 +479,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
       a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
+      a.bits_out = b.bits; a.bits_words = b.bits_words;
       aggregate(S, a);
     }
     in = b.out;
@@ -519,7 +533,9 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
     float* gW = M->grads.p + L.off_w;
     colsum(ctx, dZ, dZ_ld, rows, L.d_out, M->grads.p + L.off_b);
     const bool need_dx = li > 0;
-    const float* hprev = b.in;  // ReLU mask source for the previous layer
+    // ReLU mask of the previous layer's output: its bits
+    const uint32_t* hbits = li > 0 ? B[li - 1].bits : nullptr;
+    const uint32_t hwords = li > 0 ? B[li - 1].bits_words : 0;
     float* dZprev = need_dx ? act(ctx, nm("dZ", li - 1), rows, L.K_in, false) : nullptr;
     if (sage && L.agg_first) {
       // dW = dZ^T cat (both operands read MN-major in place)
@@ -534,7 +550,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         a.in = dcat; a.in_ld = b.mid_ld; a.in_col = L.K_in; a.pre = S->inv_deg.p;
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in; a.norm = kNormNone;
         a.residual = dcat; a.res_ld = b.mid_ld; a.res_col = 0;
-        a.mask = hprev; a.mask_ld = b.in_ld;
+        a.mask_bits = hbits; a.mask_words = hwords;
         aggregate(S, a);
       }
     } else if (sage) {
@@ -550,7 +566,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       gemm(ctx, GemmOperand{dP, b.mid_ld, true}, GemmOperand{b.in, b.in_ld, true}, L.gemm_n, L.w_cols,
            (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
-        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
+        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
         gemm_tn(ctx, dP, b.mid_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1, kBwdPrecision);
       }
     } else if (L.agg_first) {  // GCN / GIN
@@ -564,7 +580,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         AggArgs a;
         a.in = dA; a.in_ld = L.K_in; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in;
-        a.mask = hprev; a.mask_ld = b.in_ld;
+        a.mask_bits = hbits; a.mask_words = hwords;
         aggregate(S, a);
       }
     } else {  // GCN / GIN transform-first
@@ -578,7 +594,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       gemm(ctx, GemmOperand{dT, L.D_out, true}, GemmOperand{b.in, b.in_ld, true}, L.d_out, L.w_cols,
            (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
-        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask = hprev; e2.mask_ld = b.in_ld;
+        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
         gemm_tn(ctx, dT, L.D_out, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
       }
     }

@@ -72,8 +72,10 @@ struct AggArgs {
   const float* residual = nullptr; // rows x res_ld at res_col
   uint32_t res_ld = 0, res_col = 0;
   int relu = 0;
-  const float* mask = nullptr;     // ReLU backward: keep where mask[r][c] > 0
-  uint32_t mask_ld = 0, mask_col = 0;
+  const uint32_t* mask_bits = nullptr;  // ReLU backward: keep where bit (r, c) is set
+  uint32_t mask_words = 0;              // 32-bit words per row
+  uint32_t* bits_out = nullptr;         // write out > 0 as bits (forward ReLU layers)
+  uint32_t bits_words = 0;
 };
 
 // K1: CSR builder (stable radix sort by source row, bit-exact with
