@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcatgnn.so")
+# CATGNN_LIB: an alternative in-tree build of the same library (kernel A/B runs)
+LIB_PATH = os.environ.get("CATGNN_LIB") or os.path.join(_HERE, "libcatgnn.so")
 
 
 class CatgnnError(RuntimeError):

@@ -191,7 +191,10 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
 template <int VPL, int LPN, bool PRE, bool BITS>
 __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, int64_t r1, int lane) {
   constexpr int G = 32 / LPN;
-  constexpr int UNROLL0 = VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8);
+#ifndef AGG_NARROW_UNROLL
+#define AGG_NARROW_UNROLL 4
+#endif
+  constexpr int UNROLL0 = (LPN < 32 && VPL == 2) ? AGG_NARROW_UNROLL : (VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8));
   constexpr int UNROLL = G * UNROLL0 > 32 ? 32 / G : UNROLL0;
   constexpr int B = G * UNROLL;  // neighbours per batch (<= 32)
   static_assert(B <= 32, "batch must fit one index chunk");
@@ -380,7 +383,10 @@ int env_int(const char* name, int dflt) {
 template <int VPL, int LPN>
 AggFn pick_pre(bool pre, bool bits) {
   // 3 CTAs/SM for rows >= 128 floats, 4 for plain narrow rows (<= 80 / 64 registers)
-  constexpr int MINB = LPN < 32 ? 4 : 3;
+#ifndef AGG_NARROW_MINB
+#define AGG_NARROW_MINB 4
+#endif
+  constexpr int MINB = LPN < 32 ? AGG_NARROW_MINB : 3;
   if (bits) return pre ? agg_kernel<VPL, LPN, true, 3, true> : agg_kernel<VPL, LPN, false, 3, true>;
   return pre ? agg_kernel<VPL, LPN, true, MINB, false> : agg_kernel<VPL, LPN, false, MINB, false>;
 }
