@@ -194,7 +194,12 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 #ifndef AGG_NARROW_UNROLL
 #define AGG_NARROW_UNROLL 4
 #endif
-  constexpr int UNROLL0 = (LPN < 32 && VPL == 2) ? AGG_NARROW_UNROLL : (VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8));
+#ifndef AGG_WIDE_UNROLL
+#define AGG_WIDE_UNROLL 6
+#endif
+  constexpr int UNROLL0 = (LPN < 32 && VPL == 2) ? AGG_NARROW_UNROLL
+                          : (LPN == 32 && VPL == 2) ? AGG_WIDE_UNROLL
+                                                    : (VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8));
   constexpr int UNROLL = G * UNROLL0 > 32 ? 32 / G : UNROLL0;
   constexpr int B = G * UNROLL;  // neighbours per batch (<= 32)
   static_assert(B <= 32, "batch must fit one index chunk");
@@ -386,7 +391,10 @@ AggFn pick_pre(bool pre, bool bits) {
 #ifndef AGG_NARROW_MINB
 #define AGG_NARROW_MINB 4
 #endif
-  constexpr int MINB = LPN < 32 ? AGG_NARROW_MINB : 3;
+#ifndef AGG_WIDE_MINB
+#define AGG_WIDE_MINB 3
+#endif
+  constexpr int MINB = LPN < 32 ? AGG_NARROW_MINB : AGG_WIDE_MINB;
   if (bits) return pre ? agg_kernel<VPL, LPN, true, 3, true> : agg_kernel<VPL, LPN, false, 3, true>;
   return pre ? agg_kernel<VPL, LPN, true, MINB, false> : agg_kernel<VPL, LPN, false, MINB, false>;
 }
