@@ -245,9 +245,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # CATGNN_BENCH_HOST_COLLECTIVES=1: validation mode for the multi-rank flow on a
+    # single-GPU box (ranks share the device, gloo on the host replaces NCCL)
+    host_coll = os.environ.get("CATGNN_BENCH_HOST_COLLECTIVES") == "1"
+    if host_coll:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_coll:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if w.partitions % world:
         raise SystemExit(f"partition count {w.partitions} must be a multiple of the GPU count {world}")
     # data preparation (untimed; rank 0 builds the cache, the others wait)
@@ -286,7 +294,7 @@ def main():
     my_alpha = [alpha_all[i] for i in mine]
     my_counts = [counts_all[i] for i in mine]
     comm = None
-    if world > 1:
+    if world > 1 and not host_coll:
         uid = [Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = Comm(ctx, world, rank, uid[0])
@@ -297,7 +305,7 @@ def main():
         r.copy_params_from(shared)
 
     def average():
-        if comm is None:
+        if world == 1:
             model_average(reps, my_counts, shared)
         else:
             if len(reps) == 1:
@@ -305,7 +313,12 @@ def main():
             else:
                 model_average(reps, my_counts, shared)
             shared.scale(sum(my_alpha))
-            shared.allreduce(comm)
+            if comm is not None:
+                shared.allreduce(comm)  # C1: NCCL all-reduce on the library stream
+            else:  # host-collective validation mode
+                t = torch.from_numpy(shared.get_params())
+                dist.all_reduce(t)
+                shared.set_params(t.numpy())
         for r in reps:
             r.copy_params_from(shared)
 
@@ -346,7 +359,7 @@ def main():
         if e2e:
             ms = max(ms, wall * 1e3)  # host-side copies/syncs are part of the end-to-end time
         if world > 1:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device="cpu" if host_coll else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
