@@ -201,3 +201,38 @@ def test_last_loss_matches_synchronous_loss(graph):
         la = a.train_step(s, want_loss=True)
         b.train_step(s, want_loss=False)
         assert b.last_loss() == la
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage", "gin"])
+def test_edge_cases_no_edges_no_train_rows(kind):
+    """Shards without edges (aggregation = self term / SAGE mean 0) and without
+    train rows (loss 0, zero gradients, Adam leaves the parameters unchanged) —
+    the empty SPRING partition case of the DC-SBM generator."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    k = {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[kind]
+    rng = np.random.default_rng(3)
+    rows, dim, C = 300, 10, 4
+    X = rng.normal(size=(rows, dim)).astype(np.float32)
+    labels = rng.integers(0, C, rows).astype(np.int32)
+    train = np.arange(0, rows, 3, dtype=np.uint32)
+    s = gp.Shard.from_edges(rows, np.zeros((0, 2), np.uint32), X)
+    s.set_labels(labels, train)
+    off = np.zeros(rows + 1, np.int64)
+    o = go.OracleShard(go.Graph.from_csr(off, np.zeros(0, np.int64), rows), X.astype(np.float64), labels,
+                       train.astype(np.int64))
+    m = GNNModel(kind, 2, dim, 32, C, seed=4)
+    init = go.init_params(k, 2, dim, 32, C, seed=4)
+    loss = m.forward_backward(s)
+    loss_ref, H, Zs, grads = go.Replica(k, go.unflatten(m.get_params().astype(np.float64), init)).forward_backward(o)
+    assert abs(loss - loss_ref) <= 1e-3 * abs(loss_ref)
+    for (gW, gb), (rW, rb) in zip(m.unflatten(m.get_grads()), grads):
+        assert rel_err(gW, rW) < 2e-3 and rel_err(gb, rb) < 2e-3
+    # no train rows
+    s2 = gp.Shard.from_edges(rows, rng.integers(0, rows, size=(1000, 2)).astype(np.uint32), X)
+    s2.set_labels(labels, np.zeros(0, np.uint32))
+    m2 = GNNModel(kind, 2, dim, 32, C, seed=4)
+    p0 = m2.get_params()
+    assert m2.train_step(s2, want_loss=True) == 0.0
+    assert np.all(m2.get_grads() == 0)
+    assert np.array_equal(m2.get_params(), p0)
