@@ -95,23 +95,6 @@ __global__ void copy_rows_kernel(const float4* __restrict__ in, uint32_t in_ld4,
   }
 }
 
-__global__ void transpose_kernel(const float* __restrict__ in, uint32_t in_ld, uint64_t rows,
-                                 uint32_t cols, float* __restrict__ out, uint32_t out_ld) {
-  __shared__ float tile[32][33];
-  uint64_t r0 = (uint64_t)blockIdx.x * 32;
-  uint32_t c0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    uint64_t r = r0 + i;
-    uint32_t c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (r < rows && c < cols) ? in[r * in_ld + c] : 0.f;
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    uint32_t c = c0 + i;
-    uint64_t r = r0 + threadIdx.x;
-    if (c < cols && r < out_ld) out[(uint64_t)c * out_ld + r] = tile[threadIdx.x][i];
-  }
-}
 
 inline unsigned grid_for(uint64_t n, unsigned block = 256) {
   uint64_t g = (n + block - 1) / block;
@@ -272,13 +255,5 @@ void copy_rows(catgnn_ctx ctx, const float* in, uint32_t in_ld, float* out, uint
   ctx->launches++;
 }
 
-void transpose(catgnn_ctx ctx, const float* in, uint32_t in_ld, uint64_t rows, uint32_t cols,
-               float* out, uint32_t out_ld) {
-  if (!rows || !cols) return;
-  dim3 grid((unsigned)((std::max<uint64_t>(rows, out_ld) + 31) / 32), (cols + 31) / 32);
-  transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, in_ld, rows, cols, out, out_ld);
-  CG_CHECK_LAUNCH();
-  ctx->launches++;
-}
 
 }  // namespace catgnn

@@ -21,7 +21,8 @@
 // Backward uses the same CSR (A is symmetric, train.cpp:41-45 inserts both
 // directions) with the source-row scale applied as K2's `pre`, and the
 // weight gradients as split-K K3 GEMMs that read the row-major activations as
-// MN-major tensor-core operands (no transposes).
+// MN-major tensor-core operands, and the input gradients read W itself as an
+// MN-major operand (no transposes anywhere).
 #include <nccl.h>
 
 #include <cmath>
@@ -262,8 +263,6 @@ struct catgnn_model_s {
   std::vector<Layer> layers;
   uint64_t n_params = 0;
   DevBuf<float> params, grads, m, v;
-  std::vector<DevBuf<float>> wT;  // per-layer W^T (w_cols x w_rows, ld round4(w_rows))
-  bool wT_valid = false;
   uint64_t step = 0;
   uint64_t last_rows = 0;
   catgnn_shard last_shard = nullptr;
@@ -373,14 +372,6 @@ void internal_to_logical(const catgnn_model_s* M, const std::vector<float>& in, 
   }
 }
 
-void refresh_wT(catgnn_model_s* M) {
-  if (M->wT_valid) return;
-  for (size_t l = 0; l < M->layers.size(); ++l) {
-    const Layer& L = M->layers[l];
-    transpose(M->ctx, M->params.p + L.off_w, L.w_cols, L.w_rows, L.w_cols, M->wT[l].p, round_up(L.w_rows, 4));
-  }
-  M->wT_valid = true;
-}
 
 void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t width, float* out) {
   if (ld % 4) throw ConfigError("column sum needs a row stride multiple of 4");
@@ -498,7 +489,6 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   const bool gcn = M->cfg.kind == CATGNN_MODEL_GCN;
   const bool sage = M->cfg.kind == CATGNN_MODEL_SAGE;
   const size_t nl = M->layers.size();
-  refresh_wT(M);
   // K4: dZ of the last layer
   const Layer& LL = M->layers[nl - 1];
   float* dZ = act(ctx, nm("dZ", nl - 1), rows, LL.D_out, false);
@@ -545,7 +535,8 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       if (need_dx) {
         float* dcat = act(ctx, "dmid", rows, b.mid_ld, false);
         GemmEpi e2; e2.out = dcat; e2.ld_out = b.mid_ld;
-        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
+        gemm(ctx, GemmOperand{dZ, dZ_ld, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true}, (uint32_t)rows,
+             L.w_cols, L.d_out, e2, 1, kBwdPrecision);
         AggArgs a;
         a.in = dcat; a.in_ld = b.mid_ld; a.in_col = L.K_in; a.pre = S->inv_deg.p;
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in; a.norm = kNormNone;
@@ -567,7 +558,8 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
            (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
-        gemm_tn(ctx, dP, b.mid_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1, kBwdPrecision);
+        gemm(ctx, GemmOperand{dP, b.mid_ld, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true},
+             (uint32_t)rows, L.w_cols, L.gemm_n, e2, 1, kBwdPrecision);
       }
     } else if (L.agg_first) {  // GCN / GIN
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
@@ -576,7 +568,8 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       if (need_dx) {
         float* dA = act(ctx, "dmid", rows, L.K_in, false);
         GemmEpi e2; e2.out = dA; e2.ld_out = L.K_in;
-        gemm_tn(ctx, dZ, dZ_ld, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
+        gemm(ctx, GemmOperand{dZ, dZ_ld, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true}, (uint32_t)rows,
+             L.w_cols, L.d_out, e2, 1, kBwdPrecision);
         AggArgs a;
         a.in = dA; a.in_ld = L.K_in; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in;
@@ -595,7 +588,8 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
            (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
-        gemm_tn(ctx, dT, L.D_out, M->wT[li].p, round_up(L.w_rows, 4), (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
+        gemm(ctx, GemmOperand{dT, L.D_out, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true},
+             (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
       }
     }
     dZ = dZprev;
@@ -624,7 +618,6 @@ void optimizer_step(catgnn_model_s* M) {
   }
   CG_CHECK_LAUNCH();
   ctx->launches++;
-  M->wT_valid = false;
 }
 
 void check_pair(catgnn_model m, catgnn_shard s) {
@@ -666,12 +659,6 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
     CG_CUDA(cudaMemsetAsync(M->grads.p, 0, M->n_params * 4, ctx->stream));
     CG_CUDA(cudaMemsetAsync(M->m.p, 0, M->n_params * 4, ctx->stream));
     CG_CUDA(cudaMemsetAsync(M->v.p, 0, M->n_params * 4, ctx->stream));
-    for (const auto& L : M->layers) {
-      DevBuf<float> t;
-      t.alloc((size_t)L.w_cols * round_up(L.w_rows, 4));
-      CG_CUDA(cudaMemsetAsync(t.p, 0, t.bytes(), ctx->stream));
-      M->wT.push_back(std::move(t));
-    }
     // Glorot-uniform init: W[i] = (2u-1)*sqrt(6/(d_in+d_out)), u from
     // splitmix64(seed_for(seed, layer) + i) over the logical row-major index;
     // biases zero.  (The reference's SGC model is zero-initialised,
@@ -752,7 +739,6 @@ int catgnn_model_set_params(catgnn_model m, const float* in) {
     logical_to_internal(m, in, internal);
     CG_CUDA(cudaMemcpyAsync(m->params.p, internal.data(), m->n_params * 4, cudaMemcpyHostToDevice, m->ctx->stream));
     CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
-    m->wT_valid = false;
   });
 }
 
@@ -763,7 +749,6 @@ int catgnn_model_copy_params(catgnn_model dst, catgnn_model src) {
     if (dst->n_params != src->n_params) throw DataError("model shapes differ across replicas");
     CG_CUDA(cudaMemcpyAsync(dst->params.p, src->params.p, dst->n_params * 4, cudaMemcpyDeviceToDevice,
                             dst->ctx->stream));
-    dst->wT_valid = false;
   });
 }
 
@@ -881,7 +866,6 @@ int catgnn_model_average(uint32_t n, const catgnn_model* src, const uint64_t* tr
     float* tmp = dst->ctx->scratch_buf<float>("avg_tmp", dst->n_params);
     average_params(dst->ctx, ptrs, alpha, dst->n_params, tmp);
     CG_CUDA(cudaMemcpyAsync(dst->params.p, tmp, dst->n_params * 4, cudaMemcpyDeviceToDevice, dst->ctx->stream));
-    dst->wT_valid = false;
   });
 }
 
@@ -891,7 +875,6 @@ int catgnn_model_scale(catgnn_model m, double alpha) {
     scale_kernel<<<grid1d(m->n_params), 256, 0, m->ctx->stream>>>(m->params.p, m->n_params, alpha);
     CG_CHECK_LAUNCH();
     m->ctx->launches++;
-    m->wT_valid = false;
   });
 }
 
@@ -936,7 +919,6 @@ int catgnn_model_allreduce(catgnn_model m, catgnn_comm c) {
     ncclResult_t r = ncclAllReduce(m->params.p, m->params.p, m->n_params, ncclFloat32, ncclSum, c->comm,
                                    m->ctx->stream);
     if (r != ncclSuccess) throw InternalError(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
-    m->wT_valid = false;
   });
 }
 

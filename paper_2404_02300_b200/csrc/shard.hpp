@@ -91,8 +91,5 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a);
 // Copy rows x width between strided buffers (hops = 0 propagate).
 void copy_rows(catgnn_ctx ctx, const float* in, uint32_t in_ld, float* out, uint32_t out_ld,
                uint64_t rows, uint32_t width);
-// Tiled transpose: out[c][r] = in[r][c], out_ld >= rows.
-void transpose(catgnn_ctx ctx, const float* in, uint32_t in_ld, uint64_t rows, uint32_t cols,
-               float* out, uint32_t out_ld);
 
 }  // namespace catgnn
