@@ -287,17 +287,36 @@ def main():
     # two device stores on a copy stream: step t+1's upload overlaps step t's
     # work (the library orders uploads and gathers with events)
     copy_ctx = gp.Context(local) if not args.no_e2e else None
-    stores = [gp.FeatureStore(X.shape[0], X.shape[1], copy_ctx) for _ in range(2)] if not args.no_e2e else None
+    # N > 1 (NCCL): each rank uploads 1/N of the rows over its own host link and an
+    # in-place NCCL all-gather over NVLink completes every rank's store
+    shard_feats = world > 1 and not host_coll and not args.no_e2e
+    rows_per_rank = -(-X.shape[0] // world)
+    store_rows = rows_per_rank * world if shard_feats else X.shape[0]
+    stores = [gp.FeatureStore(store_rows, X.shape[1], copy_ctx) for _ in range(2)] if not args.no_e2e else None
     log(f"[rank {rank}] {len(shards)} shards resident in {time.time() - t0:.1f}s")
     counts_all = meta["part_train"]
     alpha_all = sync_weights(counts_all)
     my_alpha = [alpha_all[i] for i in mine]
     my_counts = [counts_all[i] for i in mine]
     comm = None
+    feat_comm = None
     if world > 1 and not host_coll:
-        uid = [Comm.unique_id() if rank == 0 else None]
+        uid = [Comm.unique_id() if rank == 0 else None, Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = Comm(ctx, world, rank, uid[0])
+        if shard_feats:  # its own communicator on the copy stream
+            feat_comm = Comm(copy_ctx, world, rank, uid[1])
+
+    def refresh_features(store):
+        """This step's input features from pinned host memory into a device store."""
+        if feat_comm is None:
+            store.upload(host_X.numpy())
+        else:
+            lo = rank * rows_per_rank
+            hi = min(X.shape[0], lo + rows_per_rank)
+            if hi > lo:
+                store.upload(host_X.numpy()[lo:hi], row_begin=lo)
+            store.allgather(feat_comm, rows_per_rank)
     kw = dict(optimizer=ADAM, lr=0.01, seed=0, ctx=ctx)
     shared = GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **kw)
     reps = [GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **kw) for _ in shards]
@@ -328,9 +347,9 @@ def main():
         losses = []
         if e2e:
             if t == 0:
-                stores[0].upload(host_X.numpy())
+                refresh_features(stores[0])
             if t + 1 < n:  # prefetch the next step's inputs on the copy stream
-                stores[(t + 1) % 2].upload(host_X.numpy())
+                refresh_features(stores[(t + 1) % 2])
         for r, s in zip(reps, shards):
             if e2e:
                 s.gather_features(stores[t % 2])
@@ -431,10 +450,11 @@ def main():
         for t in range(2):
             step(True, t, 2)
         e2e_ms = timed(args.steps, e2e=True) / args.steps
-        h2d = int(host_X.numel()) * 4 * world
+        h2d = int(host_X.numel()) * 4 * (1 if feat_comm is not None else world)
         e2e = {"value": edges_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
-               "path": "catgnn_features_upload (global features, pinned H2D on a copy stream, double-buffered: "
+               "path": "catgnn_features_upload (global features, pinned H2D on a copy stream, double-buffered; "
+                       "N > 1: 1/N of the rows per rank + catgnn_features_allgather over NVLink; "
                        "step t+1's copy overlaps step t) + per partition catgnn_shard_gather_features + "
                        "catgnn_model_train_step; every partition's loss D2H once per step "
                        "(catgnn_model_last_loss); model averaging"}
@@ -454,6 +474,8 @@ def main():
                 "global_nnz_edges_per_s": meta["nnz"] * len(widths) * args.steps / (total_ms / 1e3),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
+    if feat_comm is not None:
+        feat_comm.close()
     if comm is not None:
         comm.close()
     if world > 1:

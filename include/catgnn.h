@@ -129,6 +129,12 @@ int catgnn_features_create(catgnn_ctx ctx, uint64_t rows, uint32_t dim, catgnn_f
 int catgnn_features_destroy(catgnn_features f);
 int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_begin, uint64_t nrows);
 int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f);
+/* Multi-GPU refresh of a feature store: rank r uploads rows [r*R, (r+1)*R)
+ * (catgnn_features_upload with row_begin = r*R), then this in-place NCCL
+ * all-gather over NVLink completes every rank's copy (store rows >= R x ranks)
+ * — each GPU's host link carries 1/N of the matrix.  Runs on the store's stream
+ * (use a communicator created on that context). */
+int catgnn_features_allgather(catgnn_features f, catgnn_comm c, uint64_t rows_per_rank);
 typedef struct {
   uint64_t rows;
   uint64_t nnz;

@@ -63,6 +63,7 @@ def _load():
         "catgnn_features_destroy": (C.c_int, [vp]),
         "catgnn_features_upload": (C.c_int, [vp, vp, u64, u64]),
         "catgnn_shard_gather_features": (C.c_int, [vp, vp]),
+        "catgnn_features_allgather": (C.c_int, [vp, vp, u64]),
         "catgnn_complete_edges": (C.c_int, [vp, vp, u64, vp, vp, u64, u32, u32, P(vp)]),
         "catgnn_complete_edges_indexed": (C.c_int, [vp, vp, vp, u64, vp, vp, u32, u32, P(vp)]),
         "catgnn_index_build": (C.c_int, [vp, vp, u64, P(vp)]),

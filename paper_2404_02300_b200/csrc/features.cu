@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <map>
 
+#include "comm.hpp"
 #include "shard.hpp"
 
 // Uploads run on the store's context stream (a dedicated copy stream when the
@@ -110,6 +111,23 @@ int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_be
       if (kv.first != st) CG_CUDA(cudaStreamWaitEvent(st, kv.second, 0));
     CG_CUDA(cudaMemcpyAsync(f->x.p + row_begin * f->dim, host, nrows * f->dim * sizeof(float),
                             cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaEventRecord(f->uploaded, st));
+  });
+}
+
+int catgnn_features_allgather(catgnn_features f, catgnn_comm c, uint64_t rows_per_rank) {
+  return guarded([&] {
+    check_features(f);
+    if (!c || !c->comm) throw ConfigError("null communicator");
+    if (rows_per_rank * (uint64_t)c->nranks > std::max<uint64_t>(f->rows, 1) || !rows_per_rank)
+      throw ConfigError("feature store too small for rows_per_rank x ranks");
+    cudaStream_t st = f->ctx->stream;
+    for (auto& kv : f->consumed)
+      if (kv.first != st) CG_CUDA(cudaStreamWaitEvent(st, kv.second, 0));
+    const size_t count = rows_per_rank * f->dim;
+    float* mine = f->x.p + (size_t)c->rank * count;
+    const ncclResult_t r = ncclAllGather(mine, f->x.p, count, ncclFloat32, c->comm, st);  // in place
+    if (r != ncclSuccess) throw InternalError(std::string("ncclAllGather: ") + ncclGetErrorString(r));
     CG_CUDA(cudaEventRecord(f->uploaded, st));
   });
 }

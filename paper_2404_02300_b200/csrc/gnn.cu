@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "artifact.hpp"
+#include "comm.hpp"
 #include "gemm.hpp"
 #include "sgc.hpp"
 #include "shard.hpp"
@@ -630,10 +631,6 @@ void check_pair(catgnn_model m, catgnn_shard s) {
 }  // namespace
 }  // namespace catgnn
 
-struct catgnn_comm_s {
-  ncclComm_t comm = nullptr;
-  catgnn_ctx ctx = nullptr;
-};
 
 extern "C" {
 
@@ -898,6 +895,8 @@ int catgnn_comm_create(catgnn_ctx ctx, int nranks, int rank, const char id[128],
     ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
     if (r != ncclSuccess) throw InternalError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     c->ctx = ctx;
+    c->nranks = nranks;
+    c->rank = rank;
     *out = c.release();
   });
 }

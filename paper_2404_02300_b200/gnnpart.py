@@ -381,6 +381,10 @@ class FeatureStore:
             raise ConfigError(f"feature rows must be {self.dim} wide")
         check(lib.catgnn_features_upload(self.handle, _ptr(f), row_begin, f.shape[0]))
 
+    def allgather(self, comm, rows_per_rank: int):
+        """In-place NCCL all-gather of every rank's row slice (see catgnn.h)."""
+        check(lib.catgnn_features_allgather(self.handle, comm.handle, int(rows_per_rank)))
+
     def close(self):
         if getattr(self, "handle", None):
             lib.catgnn_features_destroy(self.handle)

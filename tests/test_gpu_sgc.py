@@ -274,3 +274,25 @@ def test_config1_distributed_parity(gp, tmp_path_factory):
     assert rel_err(got.params.weight, want["W"]) < 1e-3
     for h, w in zip(got.history, want["history"]):
         assert abs(h.val_f1 - w[2]) <= 0.005 and abs(h.test_f1 - w[3]) <= 0.005
+
+
+def test_feature_store_allgather_single_rank(gp, golden):
+    """catgnn_features_allgather plumbing (in-place NCCL all-gather on the store's
+    stream, event-ordered before the gathers) with a one-rank communicator."""
+    from paper_2404_02300_b200.gnn import Comm
+    g = golden
+    n = int(g["num_nodes"])
+    X = np.random.default_rng(5).normal(size=(n, 12)).astype(np.float32)
+    copy_ctx = gp.Context(0)
+    comm = Comm(copy_ctx, 1, 0, Comm.unique_id())
+    store = gp.FeatureStore(n, 12, copy_ctx)
+    store.upload(X)
+    store.allgather(comm, n)
+    ext = g["p0_ext"]
+    sh = gp.Shard.from_part(ext, g["p0_owner"], g["p0_role"], g["s0_labels"], g["p0_edges"],
+                            np.zeros((ext.size, 12), np.float32))
+    sh.gather_features(store)
+    assert np.array_equal(sh.features(), X[ext.astype(np.int64)])
+    with pytest.raises(gp.ConfigError):
+        store.allgather(comm, n + 1)
+    comm.close()
