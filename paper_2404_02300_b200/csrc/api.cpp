@@ -33,16 +33,24 @@ cudaEvent_t catgnn_ctx_s::take_event() {
   CG_CUDA(cudaEventCreate(&e));
   return e;
 }
+// Under stream capture the timing events become event-record nodes of the
+// graph (cudaEventRecordExternal), re-recorded by every replay.
+static void record_timing_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CG_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive) CG_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  else CG_CUDA(cudaEventRecord(e, st));
+}
 int catgnn_ctx_s::begin_timed(int kind) {
   if (!timing) return -1;
   Pending p{take_event(), take_event(), kind};
-  CG_CUDA(cudaEventRecord(p.a, stream));
+  record_timing_event(p.a, stream);
   pending.push_back(p);
   return (int)pending.size() - 1;
 }
 void catgnn_ctx_s::end_timed(int idx) {
   if (idx < 0) return;
-  CG_CUDA(cudaEventRecord(pending[idx].b, stream));
+  record_timing_event(pending[idx].b, stream);
 }
 void catgnn_ctx_s::drain_timing() {
   for (auto& p : pending) {

@@ -295,12 +295,14 @@ float* act(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld, 
 
 // Row stride of a layer activation.  Narrow rows are padded to 16 floats
 // (64 B) so every gathered row starts on a sector pair and the 44-wide class
-// rows of the reddit shape become 48 = 4 lanes x 3 float4 (agg_kernel<3,4>).
-const bool kPad16 = [] {
-  const char* v = std::getenv("CATGNN_PAD16");
-  return !(v && v[0] == '0');  // default on; CATGNN_PAD16=0 for round-to-4 rows
+// rows of the reddit shape become 48 (agg_kernel<2,8>).  CATGNN_PAD=4 gives
+// round-to-4 rows, CATGNN_PAD=32 128-byte rows (A/B knobs).
+const uint32_t kPadNarrow = [] {
+  const char* v = std::getenv("CATGNN_PAD");
+  if (const char* o = std::getenv("CATGNN_PAD16")) if (o[0] == '0') return 4u;
+  return v ? (uint32_t)std::atoi(v) : 16u;
 }();
-uint32_t act_width(uint32_t d) { return (kPad16 && d < 128) ? round_up(d, 16) : round_up(d, 4); }
+uint32_t act_width(uint32_t d) { return d < 128 ? round_up(d, kPadNarrow) : round_up(d, 4); }
 
 void plan_layers(catgnn_model_s* M) {
   const auto& c = M->cfg;

@@ -238,6 +238,23 @@ __global__ void average_kernel(const float* const* __restrict__ src, const doubl
   }
 }
 
+// Replica pointers and weights passed by value (kernel parameters): no
+// host-to-device staging, so averaging needs no host synchronisation and a
+// step that ends with it can be enqueued (or graph-captured) back to back.
+constexpr uint32_t kAvgByValue = 32;
+struct AvgArgs {
+  const float* src[kAvgByValue];
+  double alpha[kAvgByValue];
+};
+__global__ void average_kernel_v(const AvgArgs a, uint32_t n, uint64_t count, float* __restrict__ out) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;  // same order and arithmetic as average_kernel
+    for (uint32_t i = 0; i < n; ++i) acc += a.alpha[i] * (double)__ldg(a.src[i] + j);
+    out[j] = (float)acc;
+  }
+}
+
 size_t sgc_smem_bytes(uint32_t dim, uint32_t C, uint32_t batch) {
   return sizeof(float) * ((size_t)dim * C + ((C + 3) & ~3u) + (size_t)batch * C) +
          sizeof(uint32_t) * batch;
@@ -305,11 +322,19 @@ void sgc_eval(catgnn_ctx ctx, const float* x, uint32_t ld, uint32_t dim, const f
 void average_params(catgnn_ctx ctx, const std::vector<const float*>& d_src,
                     const std::vector<double>& alpha, uint64_t count, float* d_out) {
   const uint32_t n = (uint32_t)d_src.size();
+  unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, 148 * 8));
+  if (n <= kAvgByValue) {
+    AvgArgs a{};
+    for (uint32_t i = 0; i < n; ++i) { a.src[i] = d_src[i]; a.alpha[i] = alpha[i]; }
+    average_kernel_v<<<grid, 256, 0, ctx->stream>>>(a, n, count, d_out);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+    return;
+  }
   const float** dp = ctx->scratch_buf<const float*>("avg_src", n);
   double* da = ctx->scratch_buf<double>("avg_alpha", n);
   CG_CUDA(cudaMemcpyAsync(dp, d_src.data(), n * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
   CG_CUDA(cudaMemcpyAsync(da, alpha.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, 148 * 8));
   average_kernel<<<grid, 256, 0, ctx->stream>>>(dp, da, n, count, d_out);
   CG_CHECK_LAUNCH();
   ctx->launches++;
