@@ -392,7 +392,8 @@ def main():
 
     # CUDA graph of one averaging period (s local iterations + the average):
     # the step's ~180 launches replayed without host work between them
-    use_graph = bool(args.graph) and args.steps % args.sync == 0
+    # (not in the host-collective validation mode: its gloo all-reduce syncs the host)
+    use_graph = bool(args.graph) and args.steps % args.sync == 0 and not host_coll
     ctx.set_kernel_timing(True)  # warm the event pool before a capture
     for _ in range(args.warmup):
         step()
@@ -401,11 +402,18 @@ def main():
     graph = None
     launches0 = ctx.launches
     if use_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
-            for _ in range(args.sync):
-                step()
-        launches_per_replay = ctx.launches - launches0
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
+                for _ in range(args.sync):
+                    step()
+            launches_per_replay = ctx.launches - launches0
+        except Exception as ex:  # pragma: no cover - fall back to eager launches
+            log(f"[rank {rank}] CUDA graph capture failed ({ex}); timing eager steps")
+            graph = None
+            torch.cuda.synchronize()
+            ctx.set_kernel_timing(True)
+            launches0 = ctx.launches
     with ClockSampler(local) as clk:
         total_ms = timed(args.steps, graph=graph)
     # per-kernel CUDA events: every launch of the timed region (eager), or the

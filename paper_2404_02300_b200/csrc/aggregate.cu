@@ -60,14 +60,25 @@ struct AggKernelArgs {
 __device__ __forceinline__ float4 ldg4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
-__device__ __forceinline__ void fma4(float4& a, float s, const float4& v) {
-  a.x = fmaf(s, v.x, a.x);
-  a.y = fmaf(s, v.y, a.y);
-  a.z = fmaf(s, v.z, a.z);
-  a.w = fmaf(s, v.w, a.w);
+// Packed fp32 pairs (sm_100 FADD2 / FFMA2): same IEEE round-to-nearest
+// arithmetic per element as two scalar ops, half the issue slots.
+__device__ __forceinline__ void add2(float& x, float& y, float u, float w) {
+  asm("{\n\t.reg .b64 a, b;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 b, {%2, %3};\n\t"
+      "add.rn.f32x2 a, a, b;\n\tmov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(x), "+f"(y) : "f"(u), "f"(w));
+}
+__device__ __forceinline__ void fma2(float& x, float& y, float s, float u, float w) {
+  asm("{\n\t.reg .b64 a, b, c;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 b, {%2, %3};\n\t"
+      "mov.b64 c, {%4, %4};\n\tfma.rn.f32x2 a, c, b, a;\n\tmov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(x), "+f"(y) : "f"(u), "f"(w), "f"(s));
+}
+__device__ __forceinline__ void fma4(float4& a, float s, const float4& v) {  // a += s * v
+  fma2(a.x, a.y, s, v.x, v.y);
+  fma2(a.z, a.w, s, v.z, v.w);
 }
 __device__ __forceinline__ void add4(float4& a, const float4& v) {
-  a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+  add2(a.x, a.y, v.x, v.y);
+  add2(a.z, a.w, v.z, v.w);
 }
 __device__ __forceinline__ float4 shfl_xor4(const float4& v, int m) {
   return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
@@ -137,15 +148,34 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
   }
 }
 
+// Lane base address of the gathered rows: row j's float4 column c4 = li +
+// LPN*q sits at base + j*ldb + q*LPN*16 (one IMAD.WIDE per neighbour, the q
+// offset an immediate).
+__device__ __forceinline__ const char* lane_base(const AggKernelArgs& p, int li) {
+  return reinterpret_cast<const char*>(p.in + p.in_col) + li * 16;
+}
+template <int VPL, int LPN>
+__device__ __forceinline__ float4 ld_nbr(const char* base, uint32_t ldb, int j, int q) {
+  return __ldg(reinterpret_cast<const float4*>(base + (uint64_t)(uint32_t)j * ldb + q * LPN * 16));
+}
+
 // Sum of pre[j]*in[j] over edges [e0, e1) into acc (reduced across groups).
+// Loads past the end of the range, and by lanes whose columns lie past the
+// row width, are skipped and contribute zeros.
 template <int VPL, int LPN, bool PRE>
 __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64_t e1,
                                        float4 (&acc)[VPL], int lane) {
   constexpr int G = 32 / LPN;  // neighbours processed side by side
   constexpr int UNROLL = VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8);
   const int g = lane / LPN, li = lane % LPN;
+  const char* base = lane_base(p, li);
+  const uint32_t ldb = p.in_ld * 4;
+  bool colok[VPL];
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < VPL; ++q) {
+    colok[q] = li + LPN * q < (int)p.w4;
+    acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   for (int64_t e = e0; e < e1; e += 32) {
     const int n = (int)((e1 - e) < 32 ? (e1 - e) : 32);
     const int myj = lane < n ? ld_col(p, e + lane) : 0;
@@ -154,17 +184,16 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
     for (int kb = 0; kb < n; kb += G * UNROLL) {
       float4 v[UNROLL][VPL];
       float s[UNROLL];
+      bool ok[UNROLL];
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const int kk = kb + u * G + g;
         const int j = __shfl_sync(0xffffffffu, myj, kk & 31);
         s[u] = PRE ? __shfl_sync(0xffffffffu, mys, kk & 31) : 1.0f;
-        const bool ok = kk < n;
+        ok[u] = kk < n;
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          const uint32_t c4 = li + LPN * q;
-          v[u][q] = (ok && c4 < p.w4) ? ldg4(p.in + (size_t)j * p.in_ld + p.in_col + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int q = 0; q < VPL; ++q)
+          v[u][q] = (ok[u] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u)
@@ -214,6 +243,11 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
     curs = (cb + lane < E1) ? __ldg(p.pre + cur) : 0.f;
     nxts = (cb + 32 + lane < E1) ? __ldg(p.pre + nxt) : 0.f;
   }
+  const char* base = lane_base(p, li);
+  const uint32_t ldb = p.in_ld * 4;
+  bool colok[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) colok[q] = li + LPN * q < (int)p.w4;
   for (int64_t rb = r0; rb < r1; rb += 32) {
     const int64_t rr = rb + lane;
     const int64_t rpa = rr < r1 ? __ldg(p.row_ptr + rr) : 0;
@@ -243,25 +277,51 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
         }
         float4 v[UNROLL][VPL];
         float s[UNROLL];
-#pragma unroll
-        for (int uu = 0; uu < UNROLL; ++uu) {
-          const int64_t ee = e + uu * G + g;
-          const int off = (int)(ee - cb);  // < 32 + B <= 64
-          const int ja = __shfl_sync(0xffffffffu, cur, off & 31);
-          const int jb = __shfl_sync(0xffffffffu, nxt, off & 31);
-          const int j = off < 32 ? ja : jb;
+        bool ok[UNROLL];
+        if constexpr (G == 1) {
+          // whole-warp rows: realign the window to this batch once (lane l <-
+          // edge e + l), then each neighbour is one shuffle of a constant lane
+          const int off = (int)(e - cb) + lane;  // < 64
+          const int wa = __shfl_sync(0xffffffffu, cur, off & 31);
+          const int wb = __shfl_sync(0xffffffffu, nxt, off & 31);
+          const int win = off < 32 ? wa : wb;
+          float wins = 1.f;
           if (PRE) {
             const float sa = __shfl_sync(0xffffffffu, curs, off & 31);
             const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
-            s[uu] = off < 32 ? sa : sb;
-          } else {
-            s[uu] = 1.f;
+            wins = off < 32 ? sa : sb;
           }
-          const bool ok = ee < e1;
+          const int rem = (int)((e1 - e) < B ? (e1 - e) : B);  // valid neighbours of the batch
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) {
-            const uint32_t c4 = li + LPN * q;
-            v[uu][q] = (ok && c4 < p.w4) ? ldg4(p.in + (size_t)j * p.in_ld + p.in_col + c4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int uu = 0; uu < UNROLL; ++uu) {
+            const int j = __shfl_sync(0xffffffffu, win, uu);
+            s[uu] = PRE ? __shfl_sync(0xffffffffu, wins, uu) : 1.f;
+            ok[uu] = uu < rem;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q)
+              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+          // lane groups: two shuffles per neighbour keep the register budget
+          // of the 4-CTA/SM narrow kernels
+#pragma unroll
+          for (int uu = 0; uu < UNROLL; ++uu) {
+            const int64_t ee = e + uu * G + g;
+            const int off = (int)(ee - cb);  // < 32 + B <= 64
+            const int ja = __shfl_sync(0xffffffffu, cur, off & 31);
+            const int jb = __shfl_sync(0xffffffffu, nxt, off & 31);
+            const int j = off < 32 ? ja : jb;
+            if (PRE) {
+              const float sa = __shfl_sync(0xffffffffu, curs, off & 31);
+              const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
+              s[uu] = off < 32 ? sa : sb;
+            } else {
+              s[uu] = 1.f;
+            }
+            ok[uu] = ee < e1;
+#pragma unroll
+            for (int q = 0; q < VPL; ++q)
+              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
 #pragma unroll
@@ -324,57 +384,62 @@ __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
   unit_loop<VPL, LPN, PRE, BITS>(p);
 }
 
-// One warp per split row: sum its chunk partials in chunk order, then the
-// same epilogue as a light row.
+// One CTA per split row.  Warp w sums the row's chunk partials c = w, w+8,
+// w+16, ... (two independent load chains per warp), the eight warp sums are
+// combined in warp order through shared memory, and warp 0 applies the same
+// epilogue as a light row.  The summation order is fixed by the plan, so the
+// result is deterministic run to run.  Hub rows with ~100 chunks finish in
+// ~7 dependent loads instead of ~25 with one warp per row.
+constexpr int kFixWarps = 8;
 template <int VPL>
 __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t h = wid; h < p.n_heavy; h += nw) {
+  __shared__ float4 part[kFixWarps][32 * VPL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t h = blockIdx.x; h < p.n_heavy; h += gridDim.x) {
     const int4 hv = __ldg(p.heavy + h);
     const int64_t r = hv.x;
-    // chunk c goes to partial sum c % 4 (4 independent load chains; a hub row
-    // has ~100 chunks), combined in a fixed order: deterministic
-    float4 acc[VPL], acc4[3][VPL];
+    float4 acc[VPL], acc2[VPL];
 #pragma unroll
-    for (int q = 0; q < VPL; ++q) {
-      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) acc4[k][q] = acc[q];
-    }
+    for (int q = 0; q < VPL; ++q) acc[q] = acc2[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     const float* base = p.partials + (size_t)hv.y * p.w4 * 4;
     const size_t cs = (size_t)p.w4 * 4;
-    int c = 0;
-    for (; c + 4 <= hv.z; c += 4) {
+    int c = warp;
+    for (; c + kFixWarps < hv.z; c += 2 * kFixWarps) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const uint32_t c4 = lane + 32 * q;
         if (c4 < p.w4) {
           const float* src = base + (size_t)c * cs + c4 * 4;
-          const float4 v0 = *reinterpret_cast<const float4*>(src);
-          const float4 v1 = *reinterpret_cast<const float4*>(src + cs);
-          const float4 v2 = *reinterpret_cast<const float4*>(src + 2 * cs);
-          const float4 v3 = *reinterpret_cast<const float4*>(src + 3 * cs);
-          add4(acc[q], v0); add4(acc4[0][q], v1); add4(acc4[1][q], v2); add4(acc4[2][q], v3);
+          add4(acc[q], __ldcg(reinterpret_cast<const float4*>(src)));
+          add4(acc2[q], __ldcg(reinterpret_cast<const float4*>(src + kFixWarps * cs)));
         }
       }
     }
-    for (; c < hv.z; ++c) {
+    if (c < hv.z) {
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
         const uint32_t c4 = lane + 32 * q;
-        if (c4 < p.w4) add4(acc[q], *reinterpret_cast<const float4*>(base + (size_t)c * cs + c4 * 4));
+        if (c4 < p.w4) add4(acc[q], __ldcg(reinterpret_cast<const float4*>(base + (size_t)c * cs + c4 * 4)));
       }
     }
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
-      add4(acc4[0][q], acc4[1][q]);
-      add4(acc4[0][q], acc4[2][q]);
-      add4(acc[q], acc4[0][q]);
+      add4(acc[q], acc2[q]);
+      part[warp][lane + 32 * q] = acc[q];
     }
-    const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
-    epilogue_row<VPL, 32, true>(p, r, deg, acc, lane);
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        float4 t = part[0][lane + 32 * q];
+#pragma unroll
+        for (int w = 1; w < kFixWarps; ++w) add4(t, part[w][lane + 32 * q]);
+        acc[q] = t;
+      }
+      const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
+      epilogue_row<VPL, 32, true>(p, r, deg, acc, lane);
+    }
+    __syncthreads();
   }
 }
 
@@ -505,7 +570,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     ctx->launches++;
     if (s->n_heavy) {
       AggFn fx = pick_fixup(w4);
-      const unsigned g2 = (unsigned)std::min<uint64_t>((s->n_heavy + 7) / 8, (uint64_t)ctx->num_sms * 8);
+      const unsigned g2 = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 16);
       fx<<<g2, 256, 0, ctx->stream>>>(p);
       CG_CHECK_LAUNCH();
       ctx->launches++;
