@@ -232,6 +232,12 @@ def main():
     ap.add_argument("--ref-edges", type=int, default=300_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lanes", type=int, default=int(os.environ.get("CATGNN_LANES", "1")),
+                    help="shard lanes: partitions of a rank trained on this many concurrent streams")
+    ap.add_argument("--agg-sms", type=int, default=int(os.environ.get("CATGNN_LANE_AGG_SMS", "0")),
+                    help="with lanes > 1: SMs a K2 grid covers (0 = all)")
+    ap.add_argument("--gemm-sms", type=int, default=int(os.environ.get("CATGNN_LANE_GEMM_SMS", "0")),
+                    help="with lanes > 1: SMs a K3 grid uses (0 = all)")
     ap.add_argument("--graph", type=int, default=int(os.environ.get("CATGNN_GRAPH", "1")),
                     help="replay the device-resident step as one CUDA graph (1) or enqueue it eagerly (0)")
     args = ap.parse_args()
@@ -273,14 +279,23 @@ def main():
     from paper_2404_02300_b200.gnn import ADAM, Comm, GNNModel, model_average, sync_weights
     stream = torch.cuda.Stream()
     ctx = gp.Context(local, stream.cuda_stream)
+    # shard lanes: partition k of this rank trains on lane k % L (own stream and
+    # scratch), so one partition's aggregation overlaps another's GEMMs
+    lanes = max(1, min(args.lanes, w.partitions // world))
+    lane_streams = [stream] + [torch.cuda.Stream() for _ in range(lanes - 1)]
+    ctxs = [ctx] + [gp.Context(local, st.cuda_stream) for st in lane_streams[1:]]
+    if lanes > 1:
+        for c in ctxs:
+            c.set_sm_budget(args.agg_sms, args.gemm_sms)
     mine = list(range(rank, w.partitions, world))
     X = np.load(os.path.join(prep["dir"], "features.npy"), mmap_mode="r")
     labels = np.load(os.path.join(prep["dir"], "labels.npy"))
     shards = []
     t0 = time.time()
-    for i in mine:
+    for k, i in enumerate(mine):
         p = W.load_part(prep, i, X, labels)
-        s = gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx)
+        s = gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"],
+                               ctxs[k % lanes])
         shards.append(s)
     # e2e input: the global feature matrix in pinned host memory, refreshed into
     # the device feature store every step; shards gather their rows from it
@@ -321,7 +336,8 @@ def main():
             store.allgather(feat_comm, rows_per_rank)
     kw = dict(optimizer=ADAM, lr=0.01, seed=0, ctx=ctx)
     shared = GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **kw)
-    reps = [GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **kw) for _ in shards]
+    reps = [GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, **dict(kw, ctx=ctxs[k % lanes]))
+            for k in range(len(shards))]
     for r in reps:
         r.copy_params_from(shared)
 
@@ -347,6 +363,8 @@ def main():
 
     def step(e2e=False, t=0, n=1):
         losses = []
+        for c in ctxs[1:]:  # fork the lanes off the main stream (graph capture needs it)
+            c.wait_for(ctx)
         if e2e:
             if t == 0:
                 refresh_features(stores[0])
@@ -361,6 +379,8 @@ def main():
         state["it"] += 1
         if state["it"] % args.sync == 0:
             average()
+        for c in ctxs[1:]:  # join the lanes back into the main stream
+            ctx.wait_for(c)
         return losses
 
     def timed(n, e2e=False, graph=None):
@@ -394,34 +414,51 @@ def main():
     # the step's ~180 launches replayed without host work between them
     # (not in the host-collective validation mode: its gloo all-reduce syncs the host)
     use_graph = bool(args.graph) and args.steps % args.sync == 0 and not host_coll
-    ctx.set_kernel_timing(True)  # warm the event pool before a capture
+    def timing(on):
+        for c in ctxs:
+            c.set_kernel_timing(on)
+
+    def launch_count():
+        return sum(c.launches for c in ctxs)
+
+    timing(True)  # warm the event pool before a capture
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    ctx.set_kernel_timing(True)
+    timing(True)
     graph = None
-    launches0 = ctx.launches
+    launches0 = launch_count()
     if use_graph:
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
                 for _ in range(args.sync):
                     step()
-            launches_per_replay = ctx.launches - launches0
+            launches_per_replay = launch_count() - launches0
         except Exception as ex:  # pragma: no cover - fall back to eager launches
             log(f"[rank {rank}] CUDA graph capture failed ({ex}); timing eager steps")
             graph = None
             torch.cuda.synchronize()
-            ctx.set_kernel_timing(True)
-            launches0 = ctx.launches
+            timing(True)
+            launches0 = launch_count()
     with ClockSampler(local) as clk:
         total_ms = timed(args.steps, graph=graph)
     # per-kernel CUDA events: every launch of the timed region (eager), or the
     # graph's event nodes as recorded by its last replay (one averaging period)
-    kt = ctx.kernel_time()
-    ctx.set_kernel_timing(False)
+    # (with lanes > 1 kernels of different lanes overlap: their event times add up
+    # to more than the step and each includes the time it shared the GPU)
+    kts = [c.kernel_time() for c in ctxs]
+    kt = {k: sum(x[k] for x in kts) for k in kts[0]}
     timed_steps = args.sync if graph is not None else args.steps
-    launches = launches_per_replay * (args.steps // args.sync) if graph is not None else ctx.launches - launches0
+    recs = {}
+    for c in ctxs:
+        for k, v in c.kernel_records().items():
+            a = recs.get(k, (0.0, 0))
+            recs[k] = (a[0] + v[0], a[1] + v[1])
+    breakdown = {k: {"ms_per_step": round(v[0] / timed_steps, 4), "launches_per_step": v[1] / timed_steps}
+                 for k, v in sorted(recs.items(), key=lambda kv: -kv[1][0])}
+    timing(False)
+    launches = launches_per_replay * (args.steps // args.sync) if graph is not None else launch_count() - launches0
     ms_step = total_ms / args.steps
 
     widths = w.passes()  # logical widths: algorithmic bytes exclude the row padding
@@ -499,7 +536,7 @@ def main():
                 "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 aggregation)",
                 "data": "synthetic (RMAT + reference SPRING partitions, random-init weights)",
                 "config": workload_config(w, prep, args), "roofline": roofline, "gemm": gemm,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "step_breakdown": breakdown,
                 "global_nnz_edges_per_s": meta["nnz"] * len(widths) * args.steps / (total_ms / 1e3),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -54,12 +54,28 @@ int catgnn_version(void);
 int catgnn_ctx_create(int device, void* stream, catgnn_ctx* out);
 int catgnn_ctx_destroy(catgnn_ctx ctx);
 int catgnn_ctx_synchronize(catgnn_ctx ctx);
+/* Stream ordering between contexts of one device: work enqueued on `waiter`
+ * after this call runs after everything enqueued on `producer` so far
+ * (event record + stream wait; capturable into a CUDA graph).  Library calls
+ * that read another context's objects (model averaging, parameter copies)
+ * order themselves this way. */
+int catgnn_ctx_wait(catgnn_ctx waiter, catgnn_ctx producer);
+/* Persistent-grid budgets of this context's kernels: K2 aggregation grids
+ * cover agg_sms SMs and K3 GEMM grids gemm_sms SMs (0 = all).  Budgets below
+ * the SM count let shard lanes on other contexts' streams run beside them. */
+int catgnn_ctx_set_sm_budget(catgnn_ctx ctx, int agg_sms, int gemm_sms);
 /* Number of CUDA kernels this library launched on ctx since creation (evidence
  * for bench.py's gpu_launches; counts launches, not graph replays). */
 uint64_t catgnn_ctx_launch_count(catgnn_ctx ctx);
 /* Device time (ms) accumulated by the aggregation kernel (K2) and the GEMM
  * kernel (K3) while timing is enabled (CUDA events on ctx's stream). */
 int catgnn_ctx_set_kernel_timing(catgnn_ctx ctx, int enable);
+/* Diagnostics: per-label totals of the launches timed since the last
+ * catgnn_ctx_set_kernel_timing (labels name the kernel and its shape).  Writes
+ * record i as "label<TAB>ms_total<TAB>launches" into buf and the number of
+ * records into *count (buf may be NULL to query the count).  No reference
+ * counterpart (the reference has no device kernels). */
+int catgnn_ctx_timing_record(catgnn_ctx ctx, uint32_t i, char* buf, uint32_t cap, uint32_t* count);
 int catgnn_ctx_kernel_time(catgnn_ctx ctx, double* agg_ms, uint64_t* agg_launches,
                            double* gemm_ms, uint64_t* gemm_launches);
 

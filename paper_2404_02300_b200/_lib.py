@@ -47,7 +47,10 @@ def _load():
         "catgnn_ctx_synchronize": (C.c_int, [vp]),
         "catgnn_ctx_launch_count": (u64, [vp]),
         "catgnn_ctx_set_kernel_timing": (C.c_int, [vp, C.c_int]),
+        "catgnn_ctx_wait": (C.c_int, [vp, vp]),
+        "catgnn_ctx_set_sm_budget": (C.c_int, [vp, C.c_int, C.c_int]),
         "catgnn_ctx_kernel_time": (C.c_int, [vp, P(f64), P(u64), P(f64), P(u64)]),
+        "catgnn_ctx_timing_record": (C.c_int, [vp, u32, C.c_char_p, u32, P(u32)]),
         "catgnn_artifact_open": (C.c_int, [C.c_char_p, P(vp)]),
         "catgnn_artifact_close": (C.c_int, [vp]),
         "catgnn_artifact_get_info": (C.c_int, [vp, vp]),

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <string>
 
 #include "shard.hpp"
 
@@ -560,11 +561,15 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     int lpn = 32;
     AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
-    int t = ctx->begin_timed(0);
+    int t = ctx->begin_timed(0, ctx->timing ? "K2 agg w" + std::to_string(w4 * 4) + (a.pre ? " pre" : "") +
+                                                   (a.mask_bits || a.bits_out ? " bits" : "")
+                                             : std::string());
     const int bps = blocks_per_sm(fn);
+    static const int sms_env = env_int("CATGNN_AGG_SMS", 0);  // A/B knob: SMs the persistent grid covers
     const uint64_t warps_needed = std::max<uint64_t>(1, s->n_units);
     const unsigned grid = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)ctx->num_sms * bps, (warps_needed + 7) / 8));
+        1, std::min<uint64_t>((uint64_t)(sms_env > 0 ? sms_env : (ctx->agg_sms ? ctx->agg_sms : ctx->num_sms)) * bps,
+                              (warps_needed + 7) / 8));
     fn<<<grid, 256, 0, ctx->stream>>>(p);
     CG_CHECK_LAUNCH();
     ctx->launches++;

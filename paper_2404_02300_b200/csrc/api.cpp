@@ -33,6 +33,19 @@ cudaEvent_t catgnn_ctx_s::take_event() {
   CG_CUDA(cudaEventCreate(&e));
   return e;
 }
+void catgnn_ctx_s::wait_for(const catgnn_ctx_s* other) {
+  if (!other || other->stream == stream) return;
+  // a small ring of timing-disabled events recorded on the other stream; an
+  // event may be re-recorded once the wait that used it has been enqueued
+  if (order_events.empty()) {
+    order_events.resize(64);
+    for (auto& e : order_events) CG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t e = order_events[order_next++ % order_events.size()];
+  CG_CUDA(cudaEventRecord(e, other->stream));
+  CG_CUDA(cudaStreamWaitEvent(stream, e, 0));
+}
+
 // Under stream capture the timing events become event-record nodes of the
 // graph (cudaEventRecordExternal), re-recorded by every replay.
 static void record_timing_event(cudaEvent_t e, cudaStream_t st) {
@@ -41,9 +54,9 @@ static void record_timing_event(cudaEvent_t e, cudaStream_t st) {
   if (cs == cudaStreamCaptureStatusActive) CG_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
   else CG_CUDA(cudaEventRecord(e, st));
 }
-int catgnn_ctx_s::begin_timed(int kind) {
+int catgnn_ctx_s::begin_timed(int kind, std::string label) {
   if (!timing) return -1;
-  Pending p{take_event(), take_event(), kind};
+  Pending p{take_event(), take_event(), kind, std::move(label)};
   record_timing_event(p.a, stream);
   pending.push_back(p);
   return (int)pending.size() - 1;
@@ -59,6 +72,11 @@ void catgnn_ctx_s::drain_timing() {
     CG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     if (p.kind == 0) { agg_ms += ms; agg_n++; }
     else { gemm_ms += ms; gemm_n++; }
+    if (!p.label.empty()) {
+      auto& l = by_label[p.label];
+      l.first += ms;
+      l.second++;
+    }
     event_pool.push_back(p.a);
     event_pool.push_back(p.b);
   }
@@ -67,6 +85,7 @@ void catgnn_ctx_s::drain_timing() {
 catgnn_ctx_s::~catgnn_ctx_s() {
   for (auto& p : pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : event_pool) cudaEventDestroy(e);
+  for (auto e : order_events) cudaEventDestroy(e);
   scratch.clear();
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -271,6 +290,25 @@ int catgnn_ctx_destroy(catgnn_ctx ctx) {
   });
 }
 
+int catgnn_ctx_wait(catgnn_ctx waiter, catgnn_ctx producer) {
+  return guarded([&] {
+    check_ctx(waiter);
+    check_ctx(producer);
+    if (waiter->device != producer->device) throw ConfigError("contexts are on different devices");
+    waiter->wait_for(producer);
+  });
+}
+
+int catgnn_ctx_set_sm_budget(catgnn_ctx ctx, int agg_sms, int gemm_sms) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (agg_sms < 0 || gemm_sms < 0 || agg_sms > ctx->num_sms || gemm_sms > ctx->num_sms)
+      throw ConfigError("SM budget out of range");
+    ctx->agg_sms = agg_sms;
+    ctx->gemm_sms = gemm_sms;
+  });
+}
+
 int catgnn_ctx_synchronize(catgnn_ctx ctx) {
   return guarded([&] {
     check_ctx(ctx);
@@ -286,7 +324,24 @@ int catgnn_ctx_set_kernel_timing(catgnn_ctx ctx, int enable) {
     ctx->drain_timing();
     ctx->timing = enable != 0;
     ctx->agg_ms = ctx->gemm_ms = 0;
+    ctx->by_label.clear();
     ctx->agg_n = ctx->gemm_n = 0;
+  });
+}
+
+// Per-label breakdown of the timed launches: record i (0 <= i < count) as
+// "label\tms_total\tlaunches"; returns the record count in *count.
+int catgnn_ctx_timing_record(catgnn_ctx ctx, uint32_t i, char* buf, uint32_t cap, uint32_t* count) {
+  return guarded([&] {
+    check_ctx(ctx);
+    ctx->drain_timing();
+    if (count) *count = (uint32_t)ctx->by_label.size();
+    if (!buf || cap == 0) return;
+    if (i >= ctx->by_label.size()) throw ConfigError("timing record index out of range");
+    auto it = ctx->by_label.begin();
+    std::advance(it, i);
+    std::snprintf(buf, cap, "%s\t%.6f\t%llu", it->first.c_str(), it->second.first,
+                  (unsigned long long)it->second.second);
   });
 }
 

@@ -106,10 +106,15 @@ struct catgnn_ctx_s {
   struct Pending {
     cudaEvent_t a, b;
     int kind;  // 0 agg, 1 gemm
+    std::string label;
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  std::vector<cudaEvent_t> order_events;  // ring of events for wait_for
+  size_t order_next = 0;
   double agg_ms = 0, gemm_ms = 0;
+  // per-label totals of the timed launches (step breakdown diagnostics)
+  std::map<std::string, std::pair<double, uint64_t>> by_label;
   uint64_t agg_n = 0, gemm_n = 0;
   // named grow-only scratch buffers
   std::map<std::string, catgnn::DevBuf<unsigned char>> scratch;
@@ -123,8 +128,15 @@ struct catgnn_ctx_s {
     return reinterpret_cast<T*>(b.p);
   }
   cudaEvent_t take_event();
+  // SMs the persistent K2 grid covers and CTAs (SMs) the persistent K3 grid
+  // uses; 0 = all.  Budgets < num_sms let kernels of contexts on other
+  // streams run beside them (shard lanes, catgnn_ctx_set_sm_budget).
+  int agg_sms = 0, gemm_sms = 0;
+  // Make this context's stream wait for the work enqueued so far on `other`'s
+  // stream (no-op for the same stream); capturable.
+  void wait_for(const catgnn_ctx_s* other);
   // Bracket a kernel for timing; returns an index to close with end_timed.
-  int begin_timed(int kind);
+  int begin_timed(int kind, std::string label = std::string());
   void end_timed(int idx);
   void drain_timing();
   ~catgnn_ctx_s();

@@ -50,6 +50,7 @@ struct GemmArgs {
   uint32_t mt, nt, splits, tiles;
   uint32_t a_mn, b_mn;  // operand stored MN-major ([K rows][M or N cols] row-major)
   uint32_t bm;          // tile rows: BM x CTAs per tile
+  uint32_t a_stream, b_stream;  // operand read once per GEMM (row-sized): L2 evict-first loads
   GemmEpi epi;
 };
 
@@ -95,6 +96,23 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// Same with an L2 eviction policy (createpolicy): row-sized activation
+// operands are streamed once per GEMM and loaded evict-first, so the output
+// the next kernel consumes stays in L2.
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // UMMA shared-memory descriptor, K-major, SWIZZLE_128B: rows of 128 bytes,
 // 8-row core groups 1024 bytes apart (SBO), LBO unused (1), version 1.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
@@ -119,12 +137,17 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks, bool mn) {
 
 // TMA fill of one operand stage: K-major = one {32 x rows} box; MN-major =
 // rows/32 boxes of {32 (M/N) x 32 (K)} placed 4 KB apart.
+// policy != 0: load with that L2 cache hint.
 __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* map, bool mn, int k0, int r0,
-                                             uint32_t rows, uint32_t bar) {
+                                             uint32_t rows, uint32_t bar, uint64_t policy) {
   if (!mn) {
-    tma_load_2d(dst, map, k0, r0, bar);
+    if (policy) tma_load_2d_hint(dst, map, k0, r0, bar, policy);
+    else tma_load_2d(dst, map, k0, r0, bar);
   } else {
-    for (uint32_t a = 0; a < rows / 32; ++a) tma_load_2d(dst + a * 4096, map, r0 + (int)(32 * a), k0, bar);
+    for (uint32_t a = 0; a < rows / 32; ++a) {
+      if (policy) tma_load_2d_hint(dst + a * 4096, map, r0 + (int)(32 * a), k0, bar, policy);
+      else tma_load_2d(dst + a * 4096, map, r0 + (int)(32 * a), k0, bar);
+    }
   }
 }
 
@@ -337,6 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t bytes = A_STAGE + B_STAGE;
+      const uint64_t ef = policy_evict_first();
+      const uint64_t pol_a = args.a_stream ? ef : 0, pol_b = args.b_stream ? ef : 0;
       uint32_t it = 0;
       for (uint32_t t = cid; t < args.tiles; t += ncl) {
         uint32_t m0, n0, kb0, nkb;
@@ -348,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(empty + s), ph ^ 1);
           mbar_expect_tx(smem_u32(full + s), bytes);
           const int kx = (int)((kb0 + i) * BK);
-          load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s));
-          load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s));
+          load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s), pol_a);
+          load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), pol_b);
         }
       }
     }
@@ -446,7 +471,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4* T = epi_tiles + q * (32 * kTileLd4);
       const uint32_t r8 = lane >> 3, c4 = lane & 7;
       const uint32_t rbase = m0 + q * 32;
+      // ReLU-backward mask words are fetched one 32-column chunk ahead, so the
+      // global load latency overlaps the previous chunk's TMEM drain and stores
+      // (a whole-tile prefetch with the chunk loop unrolled measured slower)
+      const uint32_t* mrow = (e.mask_bits && row_ok) ? e.mask_bits + (size_t)row * e.mask_words : nullptr;
+      uint32_t mw_next = (mrow && n0 < args.N) ? __ldg(mrow + n0 / 32) : 0xffffffffu;
       for (uint32_t c = 0; c < BN; c += 32) {
+        const uint32_t mw_cur = mw_next;
+        if (mrow && n0 + c + 32 < args.N && c + 32 < BN) mw_next = __ldg(mrow + (n0 + c + 32) / 32);
         float v[32];
         if (nkb) {
           tmem_ld32(tmem + b * acc_cols + ((q * 32u) << 16) + c, v);
@@ -461,8 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // mask is one 32-bit word per row and chunk, and ReLU layers emit the
         // same word for their own backward (bits_out).
         if (col0 + 32 <= args.N && !e.partial) {
-          const uint32_t mw = (e.mask_bits && row_ok) ? __ldg(e.mask_bits + (size_t)row * e.mask_words + col0 / 32)
-                                                     : 0xffffffffu;
+          const uint32_t mw = mrow ? mw_cur : 0xffffffffu;
           uint32_t bw = 0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -654,7 +685,8 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   const uint32_t nkb = (K + BK - 1) / BK;
   const uint32_t bm = BM * ncta;
   const uint32_t mt = (M + bm - 1) / bm, nt = (N + BN - 1) / BN;
-  const uint32_t units = (uint32_t)ctx->num_sms / ncta;  // persistent CTAs (pairs)
+  const uint32_t gsms = ctx->gemm_sms ? std::max<uint32_t>(ncta, (uint32_t)ctx->gemm_sms) : (uint32_t)ctx->num_sms;
+  const uint32_t units = gsms / ncta;  // persistent CTAs (pairs)
   uint32_t splits = 1;
   if (split_k == 0) {
     // fill the SMs when the tile grid is small and K is long
@@ -694,6 +726,16 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   args.a_mn = a.mn_major ? 1u : 0u;
   args.b_mn = b.mn_major ? 1u : 0u;
   args.bm = bm;
+  {
+    static const int ef_env = [] {
+      const char* v = std::getenv("CATGNN_GEMM_EVICT_FIRST");
+      return v ? std::atoi(v) : 0;  // measured slower on the reddit step (off by default)
+    }();
+    // an operand is streamed when its row extent (M for A, N for B) is row-sized
+    // or it is the long contraction side of a split-K weight gradient
+    args.a_stream = ef_env && (M > 4096 || K > 4096) ? 1u : 0u;
+    args.b_stream = ef_env && (N > 4096 || K > 4096) ? 1u : 0u;
+  }
   // instruction descriptor: D f32, A/B tf32, A/B major (bit 15/16), N>>3, M>>4
   args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (args.a_mn << 15) | (args.b_mn << 16) | ((BN >> 3) << 17) |
                ((bm >> 4) << 24);
@@ -714,7 +756,11 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set[ncta - 1] = true;
   }
-  int t = ctx->begin_timed(1);
+  // timing label: the GEMM's shape class (row-sized extents as "rows")
+  auto dim = [](uint32_t x) { return x > 4096 ? std::string("rows") : std::to_string(x); };
+  int t = ctx->begin_timed(1, ctx->timing ? "K3 gemm M=" + dim(M) + " N=" + dim(N) + " K=" + dim(K) +
+                                             (pair ? " pair" : "") + (splits > 1 ? " split-K" : "")
+                                       : std::string());
   const unsigned grid = std::min<unsigned>(args.tiles, units) * ncta;  // persistent
   if (pair) {
     cudaLaunchConfig_t cfg = {};

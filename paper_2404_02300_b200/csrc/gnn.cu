@@ -746,6 +746,8 @@ int catgnn_model_copy_params(catgnn_model dst, catgnn_model src) {
     check_model(dst);
     check_model(src);
     if (dst->n_params != src->n_params) throw DataError("model shapes differ across replicas");
+    if (dst->ctx->device != src->ctx->device) throw ConfigError("models are on different devices");
+    dst->ctx->wait_for(src->ctx);  // src's pending updates first (contexts on other streams)
     CG_CUDA(cudaMemcpyAsync(dst->params.p, src->params.p, dst->n_params * 4, cudaMemcpyDeviceToDevice,
                             dst->ctx->stream));
   });
@@ -858,8 +860,9 @@ int catgnn_model_average(uint32_t n, const catgnn_model* src, const uint64_t* tr
     std::vector<const float*> ptrs(n);
     for (uint32_t i = 0; i < n; ++i) {
       check_model(src[i]);
-      if (src[i]->n_params != dst->n_params || src[i]->ctx != dst->ctx)
-        throw DataError("model shapes differ across replicas");
+      if (src[i]->n_params != dst->n_params) throw DataError("model shapes differ across replicas");
+      if (src[i]->ctx->device != dst->ctx->device) throw ConfigError("models are on different devices");
+      dst->ctx->wait_for(src[i]->ctx);  // replicas trained on other contexts' streams finish first
       ptrs[i] = src[i]->params.p;
     }
     float* tmp = dst->ctx->scratch_buf<float>("avg_tmp", dst->n_params);

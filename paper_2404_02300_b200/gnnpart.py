@@ -61,6 +61,14 @@ class Context:
     def launches(self) -> int:
         return int(lib.catgnn_ctx_launch_count(self.handle))
 
+    def wait_for(self, other: "Context"):
+        """Order this context's later work after `other`'s work enqueued so far."""
+        check(lib.catgnn_ctx_wait(self.handle, other.handle))
+
+    def set_sm_budget(self, agg_sms: int = 0, gemm_sms: int = 0):
+        """Persistent-grid SM budgets of this context's K2 / K3 launches (0 = all SMs)."""
+        check(lib.catgnn_ctx_set_sm_budget(self.handle, int(agg_sms), int(gemm_sms)))
+
     def set_kernel_timing(self, enable: bool):
         check(lib.catgnn_ctx_set_kernel_timing(self.handle, int(enable)))
 
@@ -68,6 +76,18 @@ class Context:
         a = C.c_double(); an = C.c_uint64(); g = C.c_double(); gn = C.c_uint64()
         check(lib.catgnn_ctx_kernel_time(self.handle, C.byref(a), C.byref(an), C.byref(g), C.byref(gn)))
         return dict(agg_ms=a.value, agg_launches=an.value, gemm_ms=g.value, gemm_launches=gn.value)
+
+    def kernel_records(self):
+        """Per-label totals of the timed launches: {label: (ms_total, launches)}."""
+        n = C.c_uint32()
+        check(lib.catgnn_ctx_timing_record(self.handle, 0, None, 0, C.byref(n)))
+        out = {}
+        buf = C.create_string_buffer(512)
+        for i in range(n.value):
+            check(lib.catgnn_ctx_timing_record(self.handle, i, buf, 512, C.byref(n)))
+            label, ms, cnt = buf.value.decode().split("\t")
+            out[label] = (float(ms), int(cnt))
+        return out
 
     def close(self):
         if getattr(self, "handle", None):
