@@ -422,6 +422,66 @@ def main():
         return sum(c.launches for c in ctxs)
 
     timing(True)  # warm the event pool before a capture
+    def timed_e2e_graph(n, diag=False):
+        """End-to-end steps as replays of one CUDA graph holding two steps: step
+        2i gathers from store 0 while store 1 receives step 2i+1's features on
+        the copy stream, step 2i+1 gathers from store 1 while store 0 receives
+        the next replay's; every step's losses are copied into pinned host
+        memory and read after the replay.  The first step's upload runs eagerly
+        inside the timed region."""
+        R = len(reps)
+        host_loss = torch.zeros(2 * R, dtype=torch.float64).pin_memory()
+        base = host_loss.data_ptr()
+        rows = [0] * (2 * R)
+        torch.cuda.synchronize()
+        for st in stores:
+            st.reset_deps()
+        if diag:
+            timing(True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+            copy_ctx.wait_for(ctx)
+            for c in ctxs[1:]:
+                c.wait_for(ctx)
+            for sub in (0, 1):
+                refresh_features(stores[1 - sub])  # the next step's inputs (copy stream)
+                for k, (r, s) in enumerate(zip(reps, shards)):
+                    s.gather_features(stores[sub])
+                    r.train_step(s, want_loss=False)
+                    rows[sub * R + k] = r.last_loss_async(base + 8 * (sub * R + k))
+                average()
+            ctx.wait_for(copy_ctx)
+            for c in ctxs[1:]:
+                ctx.wait_for(c)
+        for st in stores:
+            st.reset_deps()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        wall0 = time.perf_counter()
+        refresh_features(stores[0])  # step 0's inputs
+        ctx.wait_for(copy_ctx)
+        losses = []
+        with torch.cuda.stream(stream):
+            for _ in range(n // 2):
+                g.replay()
+                stream.synchronize()  # both steps' losses are on the host now
+                hl = host_loss.tolist()
+                losses.append([hl[j] / rows[j] if rows[j] else 0.0 for j in range(2 * R)])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = max(ev0.elapsed_time(ev1), (time.perf_counter() - wall0) * 1e3)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        if not all(np.isfinite(x).all() for x in losses):
+            raise RuntimeError("non-finite loss in the e2e steps")
+        return ms
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -515,15 +575,37 @@ def main():
     if not args.no_e2e:
         for t in range(2):
             step(True, t, 2)
-        e2e_ms = timed(args.steps, e2e=True) / args.steps
+        diag = os.environ.get("CATGNN_E2E_BREAKDOWN") == "1"  # per-kernel times of the e2e steps
+        e2e_graph = use_graph and graph is not None and args.sync == 1 and args.steps % 2 == 0
+        if e2e_graph:
+            try:
+                e2e_ms = timed_e2e_graph(args.steps, diag) / args.steps
+            except Exception as ex:  # pragma: no cover - fall back to eager steps
+                log(f"[rank {rank}] e2e graph failed ({ex}); timing eager e2e steps")
+                torch.cuda.synchronize()
+                for st in stores:
+                    st.reset_deps()
+                e2e_graph = False
+        if not e2e_graph:
+            if diag:
+                timing(True)
+            e2e_ms = timed(args.steps, e2e=True) / args.steps
+        if diag:
+            for c in ctxs:
+                for k, v in sorted(c.kernel_records().items(), key=lambda kv: -kv[1][0]):
+                    log(f"[e2e] {k}: {v[0] / (2 if e2e_graph else args.steps):.3f} ms/step, "
+                        f"{v[1] / (2 if e2e_graph else args.steps):.1f} launches/step")
+            timing(False)
         h2d = int(host_X.numel()) * 4 * (1 if feat_comm is not None else world)
         e2e = {"value": edges_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
+               "graph": "two steps per CUDA graph replay (device stores alternate)" if e2e_graph else None,
                "path": "catgnn_features_upload (global features, pinned H2D on a copy stream, double-buffered; "
                        "N > 1: 1/N of the rows per rank + catgnn_features_allgather over NVLink; "
                        "step t+1's copy overlaps step t) + per partition catgnn_shard_gather_features + "
-                       "catgnn_model_train_step; every partition's loss D2H once per step "
-                       "(catgnn_model_last_loss); model averaging"}
+                       "catgnn_model_train_step; every partition's loss D2H every step "
+                       "(catgnn_model_last_loss_async into pinned memory, read on the host after each replay); "
+                       "model averaging"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

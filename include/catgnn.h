@@ -144,6 +144,10 @@ int catgnn_shard_upload_features(catgnn_shard s, const float* features, uint32_t
 int catgnn_features_create(catgnn_ctx ctx, uint64_t rows, uint32_t dim, catgnn_features* out);
 int catgnn_features_destroy(catgnn_features f);
 int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_begin, uint64_t nrows);
+/* Forget the store's recorded upload / gather events; the caller orders its
+ * producers and consumers by stream order from then on (before capturing a
+ * CUDA graph that uploads into and gathers from the store). */
+int catgnn_features_reset_deps(catgnn_features f);
 int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f);
 /* Multi-GPU refresh of a feature store: rank r uploads rows [r*R, (r+1)*R)
  * (catgnn_features_upload with row_begin = r*R), then this in-place NCCL
@@ -291,6 +295,10 @@ int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss);
 /* Loss of the last train_step (computed on the device either way); lets a
  * caller run several replicas' steps back to back and sync once. */
 int catgnn_model_last_loss(catgnn_model m, double* loss);
+/* Same, asynchronous: enqueues the copy of the loss sum into host_sum (pinned
+ * host memory; capturable into a CUDA graph) and returns the train-row count
+ * in *rows; the mean is *host_sum / *rows after the context synchronises. */
+int catgnn_model_last_loss_async(catgnn_model m, double* host_sum, uint64_t* rows);
 /* Forward + backward only (no update); gradients readable by get_grads. */
 int catgnn_model_forward_backward(catgnn_model m, catgnn_shard s, double* loss);
 /* Forward only; logits rows x classes into out (host) when out != NULL;

@@ -561,8 +561,10 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     int lpn = 32;
     AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
+    static const int detail = env_int("CATGNN_TIMING_DETAIL", 0);  // label per shard (rows)
     int t = ctx->begin_timed(0, ctx->timing ? "K2 agg w" + std::to_string(w4 * 4) + (a.pre ? " pre" : "") +
-                                                   (a.mask_bits || a.bits_out ? " bits" : "")
+                                                   (a.mask_bits || a.bits_out ? " bits" : "") +
+                                                   (detail ? " rows=" + std::to_string(s->rows) : std::string())
                                              : std::string());
     const int bps = blocks_per_sm(fn);
     static const int sms_env = env_int("CATGNN_AGG_SMS", 0);  // A/B knob: SMs the persistent grid covers

@@ -71,7 +71,7 @@ void catgnn_ctx_s::drain_timing() {
     float ms = 0;
     CG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     if (p.kind == 0) { agg_ms += ms; agg_n++; }
-    else { gemm_ms += ms; gemm_n++; }
+    else if (p.kind == 1) { gemm_ms += ms; gemm_n++; }
     if (!p.label.empty()) {
       auto& l = by_label[p.label];
       l.first += ms;

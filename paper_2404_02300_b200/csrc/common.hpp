@@ -105,7 +105,7 @@ struct catgnn_ctx_s {
   bool timing = false;
   struct Pending {
     cudaEvent_t a, b;
-    int kind;  // 0 agg, 1 gemm
+    int kind;  // 0 agg, 1 gemm, 2 other (label only)
     std::string label;
   };
   std::vector<Pending> pending;

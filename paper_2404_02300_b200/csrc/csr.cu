@@ -116,6 +116,10 @@ uint32_t env_unit_cost() {
 // result is deterministic run to run.
 void build_plan(catgnn_shard_s* s, const std::vector<int64_t>& rp) {
   const uint32_t U = env_unit_cost();
+  static const uint64_t row_cost = [] {  // per-row overhead in edge units (A/B knob)
+    const char* v = std::getenv("CATGNN_ROW_COST");
+    return (uint64_t)(v && *v ? std::max(1L, std::strtol(v, nullptr, 10)) : 16L);  // 16: measured best on the reddit shards
+  }();
   std::vector<int4> units, heavy;
   uint64_t chunks = 0, cost = 0, begin = 0;
   for (uint64_t r = 0; r < s->rows; ++r) {
@@ -130,7 +134,7 @@ void build_plan(catgnn_shard_s* s, const std::vector<int64_t>& rp) {
       begin = r + 1;
       cost = 0;
     } else {
-      cost += deg + 2;
+      cost += deg + row_cost;
       if (cost >= U) {
         units.push_back(make_int4((int)begin, (int)(r + 1), -1, 0));
         begin = r + 1;

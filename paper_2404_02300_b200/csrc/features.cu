@@ -26,6 +26,7 @@ struct catgnn_features_s {
   uint32_t dim = 0;
   catgnn::DevBuf<float> x;  // rows x dim, dense
   cudaEvent_t uploaded = nullptr;
+  bool has_upload = false;  // `uploaded` marks an upload consumers must wait for
   std::map<cudaStream_t, cudaEvent_t> consumed;  // per consumer stream: last gather
   ~catgnn_features_s() {
     if (uploaded) cudaEventDestroy(uploaded);
@@ -112,6 +113,7 @@ int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_be
     CG_CUDA(cudaMemcpyAsync(f->x.p + row_begin * f->dim, host, nrows * f->dim * sizeof(float),
                             cudaMemcpyHostToDevice, st));
     CG_CUDA(cudaEventRecord(f->uploaded, st));
+    f->has_upload = true;
   });
 }
 
@@ -129,6 +131,19 @@ int catgnn_features_allgather(catgnn_features f, catgnn_comm c, uint64_t rows_pe
     const ncclResult_t r = ncclAllGather(mine, f->x.p, count, ncclFloat32, c->comm, st);  // in place
     if (r != ncclSuccess) throw InternalError(std::string("ncclAllGather: ") + ncclGetErrorString(r));
     CG_CUDA(cudaEventRecord(f->uploaded, st));
+    f->has_upload = true;
+  });
+}
+
+// Forget the recorded upload / gather events: the caller orders the store's
+// producers and consumers by stream order from here on (e.g. before capturing
+// a CUDA graph whose replays must not wait on events of uncaptured work).
+int catgnn_features_reset_deps(catgnn_features f) {
+  return guarded([&] {
+    check_features(f);
+    for (auto& kv : f->consumed) CG_CUDA(cudaEventDestroy(kv.second));
+    f->consumed.clear();
+    f->has_upload = false;
   });
 }
 
@@ -157,8 +172,9 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
     }
     s->xprop.release();
     if (!s->rows) return;
-    if (f->ctx->stream != st) CG_CUDA(cudaStreamWaitEvent(st, f->uploaded, 0));
+    if (f->ctx->stream != st && f->has_upload) CG_CUDA(cudaStreamWaitEvent(st, f->uploaded, 0));
     const unsigned grid = (unsigned)std::min<uint64_t>((s->rows + 7) / 8, (uint64_t)s->ctx->num_sms * 8);
+    const int t = s->ctx->begin_timed(2, s->ctx->timing ? "K6 feature gather d" + std::to_string(f->dim) : std::string());
     if (f->dim % 4 == 0)
       gather_rows_kernel<4><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
     else if (f->dim % 2 == 0)
@@ -166,6 +182,7 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
     else
       gather_rows_kernel<1><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
     CG_CHECK_LAUNCH();
+    s->ctx->end_timed(t);
     s->ctx->launches++;
     if (f->ctx->stream != st) {
       cudaEvent_t& ev = f->consumed[st];

@@ -790,6 +790,22 @@ int catgnn_model_last_loss(catgnn_model m, double* loss) {
   });
 }
 
+// Asynchronous form: enqueues the D2H copy of the last step's loss sum into
+// host_sum (pinned memory; capturable) and returns its train-row count, so
+// the mean is *host_sum / *rows once the context's stream has synchronised.
+int catgnn_model_last_loss_async(catgnn_model m, double* host_sum, uint64_t* rows) {
+  return guarded([&] {
+    check_model(m);
+    if (!host_sum || !rows) throw ConfigError("null argument");
+    *rows = m->loss_rows;
+    if (!m->loss_dev.p || m->loss_rows == 0) {
+      *host_sum = 0.0;
+      return;
+    }
+    CG_CUDA(cudaMemcpyAsync(host_sum, m->loss_dev.p, 8, cudaMemcpyDeviceToHost, m->ctx->stream));
+  });
+}
+
 int catgnn_model_forward(catgnn_model m, catgnn_shard s, float* logits, int role, double* f1) {
   return guarded([&] {
     check_pair(m, s);

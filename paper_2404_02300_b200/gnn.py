@@ -87,6 +87,14 @@ class GNNModel:
         check(lib.catgnn_model_last_loss(self.handle, C.byref(loss)))
         return loss.value
 
+    def last_loss_async(self, host_sum) -> int:
+        """Enqueue the D2H copy of the last step's loss sum into host_sum (a
+        pinned float64 buffer's address); returns the train-row count."""
+        rows = C.c_uint64()
+        check(lib.catgnn_model_last_loss_async(self.handle, C.cast(host_sum, C.POINTER(C.c_double)),
+                                               C.byref(rows)))
+        return int(rows.value)
+
     def forward_backward(self, shard: Shard) -> float:
         loss = C.c_double()
         check(lib.catgnn_model_forward_backward(self.handle, shard.handle, C.byref(loss)))

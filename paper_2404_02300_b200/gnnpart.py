@@ -401,6 +401,10 @@ class FeatureStore:
             raise ConfigError(f"feature rows must be {self.dim} wide")
         check(lib.catgnn_features_upload(self.handle, _ptr(f), row_begin, f.shape[0]))
 
+    def reset_deps(self):
+        """Forget recorded upload / gather events (stream order from here on)."""
+        check(lib.catgnn_features_reset_deps(self.handle))
+
     def allgather(self, comm, rows_per_rank: int):
         """In-place NCCL all-gather of every rank's row slice (see catgnn.h)."""
         check(lib.catgnn_features_allgather(self.handle, comm.handle, int(rows_per_rank)))
