@@ -213,9 +213,21 @@ __global__ void colsum_reduce_kernel(const float* __restrict__ partial, uint32_t
 }
 
 // K5: fused optimizer over the flat parameter vector.
+// The step count lives on the device (step[0] = completed updates, step[1] =
+// block ticket), so a CUDA graph replaying train steps applies the right bias
+// correction every replay: each block reads t = step[0] + 1, and the last
+// block to finish advances step[0].
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, uint64_t n, float lr, float b1, float b2, float eps,
-                            float bc1, float bc2) {
+                            double b1d, double b2d, unsigned long long* step) {
+  __shared__ float bc[2];
+  if (threadIdx.x == 0) {
+    const double t = (double)(*(volatile unsigned long long*)step + 1);
+    bc[0] = (float)(1.0 - pow(b1d, t));
+    bc[1] = (float)(1.0 - pow(b2d, t));
+  }
+  __syncthreads();
+  const float bc1 = bc[0], bc2 = bc[1];
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
@@ -224,6 +236,13 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     m[i] = mi;
     v[i] = vi;
     p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(step + 1, 1ull) == gridDim.x - 1) {  // every block has read step[0]
+      step[0] += 1;
+      step[1] = 0;
+    }
   }
 }
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, uint64_t n, float lr) {
@@ -264,7 +283,8 @@ struct catgnn_model_s {
   std::vector<Layer> layers;
   uint64_t n_params = 0;
   DevBuf<float> params, grads, m, v;
-  uint64_t step = 0;
+  uint64_t step = 0;                       // updates issued (host count)
+  DevBuf<unsigned long long> step_dev;     // [completed updates, block ticket] (Adam bias correction)
   uint64_t last_rows = 0;
   catgnn_shard last_shard = nullptr;
   double last_loss = 0.0;
@@ -611,11 +631,10 @@ void optimizer_step(catgnn_model_s* M) {
   M->step++;
   const auto& c = M->cfg;
   if (c.optimizer == CATGNN_OPT_ADAM) {
-    const float bc1 = (float)(1.0 - std::pow(c.beta1, (double)M->step));
-    const float bc2 = (float)(1.0 - std::pow(c.beta2, (double)M->step));
     adam_kernel<<<grid1d(M->n_params), 256, 0, ctx->stream>>>(M->params.p, M->grads.p, M->m.p, M->v.p,
                                                              M->n_params, (float)c.lr, (float)c.beta1,
-                                                             (float)c.beta2, (float)c.eps, bc1, bc2);
+                                                             (float)c.beta2, (float)c.eps, c.beta1, c.beta2,
+                                                             M->step_dev.p);
   } else {
     sgd_kernel<<<grid1d(M->n_params), 256, 0, ctx->stream>>>(M->params.p, M->grads.p, M->n_params, (float)c.lr);
   }
@@ -658,6 +677,8 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
     CG_CUDA(cudaMemsetAsync(M->grads.p, 0, M->n_params * 4, ctx->stream));
     CG_CUDA(cudaMemsetAsync(M->m.p, 0, M->n_params * 4, ctx->stream));
     CG_CUDA(cudaMemsetAsync(M->v.p, 0, M->n_params * 4, ctx->stream));
+    M->step_dev.alloc(2);
+    CG_CUDA(cudaMemsetAsync(M->step_dev.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     // Glorot-uniform init: W[i] = (2u-1)*sqrt(6/(d_in+d_out)), u from
     // splitmix64(seed_for(seed, layer) + i) over the logical row-major index;
     // biases zero.  (The reference's SGC model is zero-initialised,

@@ -236,3 +236,135 @@ def test_edge_cases_no_edges_no_train_rows(kind):
     assert m2.train_step(s2, want_loss=True) == 0.0
     assert np.all(m2.get_grads() == 0)
     assert np.array_equal(m2.get_params(), p0)
+
+
+def test_last_loss_async_matches(graph):
+    import torch
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    s, _ = make(gp, graph, 16, 4)
+    a = GNNModel("gcn", 2, 16, 32, 4, seed=1)
+    buf = torch.zeros(1, dtype=torch.float64).pin_memory()
+    la = a.train_step(s, want_loss=True)
+    rows = a.last_loss_async(buf.data_ptr())
+    a.ctx.synchronize()
+    assert rows == int(s.info.n_train) and buf.item() / rows == la
+
+
+def test_replicas_on_other_contexts_average_identically(graph):
+    """Replicas trained on other contexts' streams (shard lanes) and averaged /
+    copied across contexts give bit-identical parameters (catgnn_ctx_wait
+    ordering inside catgnn_model_average / catgnn_model_copy_params); SM budgets
+    change only the persistent grid sizes, not the results."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel, model_average
+    main = gp.Context(0)
+    lanes = [gp.Context(0), gp.Context(0)]
+    lanes[1].set_sm_budget(100, 32)
+    out = []
+    for mode in ("one", "lanes"):
+        ctxs = [main, main] if mode == "one" else lanes
+        shards, reps = [], []
+        for k in range(2):
+            rng = np.random.default_rng(10 + k)
+            X = rng.normal(size=(graph["n"], 16)).astype(np.float32)
+            labels = rng.integers(0, 4, graph["n"]).astype(np.int32)
+            train = np.sort(rng.choice(graph["n"], size=graph["n"] // 2, replace=False)).astype(np.uint32)
+            s = gp.Shard.from_edges(graph["n"], graph["pairs"], X, ctx=ctxs[k])
+            s.set_labels(labels, train)
+            shards.append(s)
+            reps.append(GNNModel("gcn", 2, 16, 32, 4, seed=3, ctx=ctxs[k]))
+        shared = GNNModel("gcn", 2, 16, 32, 4, seed=3, ctx=main)
+        for _ in range(3):
+            for c in ctxs:
+                c.wait_for(main)
+            for r, s in zip(reps, shards):
+                r.train_step(s, want_loss=False)
+            model_average(reps, [3, 5], shared)
+            for r in reps:
+                r.copy_params_from(shared)
+        main.synchronize()
+        out.append(shared.get_params())
+    assert np.array_equal(out[0], out[1])
+
+
+def test_graph_captured_e2e_steps_match_eager(tmp_path_factory):
+    """bench.py's graph-captured e2e pipeline (upload into one store on a copy
+    stream while the other feeds the gathers; stores reset to stream order
+    before capture) trains exactly like eager steps."""
+    import torch
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    ds = make_dataset(tmp_path_factory.mktemp("e2eg"), scale=10, edges=4000, dim=20, classes=5, seed=9)
+    art = make_artifact(ds, p=2)
+    X = ds["X"]
+    Xs = []  # two different per-step inputs, pinned (graph-captured H2D copies)
+    for a in (X, X * 0.5 + 1.0):
+        t = torch.empty(a.shape, dtype=torch.float32).pin_memory()
+        t.numpy()[:] = a
+        Xs.append(t.numpy())
+    results = []
+    for mode in ("eager", "graph"):
+        stream = torch.cuda.Stream()
+        ctx = gp.Context(0, stream.cuda_stream)
+        copy_ctx = gp.Context(0)
+        data = gp.load_training_data(art, ctx=ctx)
+        stores = [gp.FeatureStore(X.shape[0], X.shape[1], copy_ctx) for _ in range(2)]
+        reps = [GNNModel("gcn", 2, X.shape[1], 16, 5, seed=7, ctx=ctx) for _ in data.shards]
+        host = torch.zeros(4, dtype=torch.float64).pin_memory()
+        # one eager step in both modes first (allocates the lazily sized buffers)
+        stores[1].upload(Xs[1])
+        for r, s in zip(reps, data.shards):
+            s.gather_features(stores[1])
+            r.train_step(s, want_loss=False)
+        losses = []
+        if mode == "eager":
+            for t in range(4):
+                stores[t % 2].upload(Xs[t % 2])
+                for r, s in zip(reps, data.shards):
+                    s.gather_features(stores[t % 2])
+                    r.train_step(s, want_loss=False)
+                losses += [r.last_loss() for r in reps]
+        else:
+            torch.cuda.synchronize()
+            for st in stores:
+                st.reset_deps()
+            rows = [0] * 4
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+                copy_ctx.wait_for(ctx)
+                for sub in (0, 1):
+                    stores[1 - sub].upload(Xs[1 - sub])
+                    for k, (r, s) in enumerate(zip(reps, data.shards)):
+                        s.gather_features(stores[sub])
+                        r.train_step(s, want_loss=False)
+                        rows[2 * sub + k] = r.last_loss_async(host.data_ptr() + 8 * (2 * sub + k))
+                ctx.wait_for(copy_ctx)
+            for st in stores:
+                st.reset_deps()
+            stores[0].upload(Xs[0])
+            ctx.wait_for(copy_ctx)
+            with torch.cuda.stream(stream):
+                for _ in range(2):
+                    g.replay()
+                    stream.synchronize()
+                    losses += [host[j].item() / rows[j] for j in range(4)]
+        results.append((losses, [r.get_params() for r in reps]))
+    assert results[0][0] == results[1][0]
+    for a, b in zip(results[0][1], results[1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_timing_records_label_kernels(graph):
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    ctx = gp.Context(0)
+    s2 = gp.Shard.from_edges(graph["n"], graph["pairs"], np.ones((graph["n"], 16), np.float32), ctx=ctx)
+    s2.set_labels(np.zeros(graph["n"], np.int32), np.arange(10, dtype=np.uint32))
+    m = GNNModel("gcn", 2, 16, 32, 4, seed=1, ctx=ctx)
+    ctx.set_kernel_timing(True)
+    m.train_step(s2, want_loss=False)
+    rec = ctx.kernel_records()
+    ctx.set_kernel_timing(False)
+    assert any(k.startswith("K2 agg w") for k in rec) and any(k.startswith("K3 gemm") for k in rec)
+    assert all(v[0] > 0 and v[1] >= 1 for v in rec.values())
