@@ -118,7 +118,7 @@ void build_plan(catgnn_shard_s* s, const std::vector<int64_t>& rp) {
   const uint32_t U = env_unit_cost();
   static const uint64_t row_cost = [] {  // per-row overhead in edge units (A/B knob)
     const char* v = std::getenv("CATGNN_ROW_COST");
-    return (uint64_t)(v && *v ? std::max(1L, std::strtol(v, nullptr, 10)) : 16L);  // 16: measured best on the reddit shards
+    return (uint64_t)(v && *v ? std::max(1L, std::strtol(v, nullptr, 10)) : 32L);  // 32: measured best on the reddit shards (scripts/plan_sweep.sh)
   }();
   std::vector<int4> units, heavy;
   uint64_t chunks = 0, cost = 0, begin = 0;
