@@ -13,9 +13,11 @@
 //               .cta_group::1.kind::tf32 (M=128, N=BN, K=8 per instruction)
 //               into one of two TMEM accumulators, so the epilogue of tile i
 //               overlaps the MMAs of tile i+1; tcgen05.commit frees stages
-//   warps 2..5  3xTF32 converters: lo = x - tf32(x) tiles next to each stage,
+//   warps 2..5  3xTF32 converters: lo = x - tf32(x) tiles into a ring of L
+//               residual slots (slot it % L, freed by the MMAs of stage it - L),
 //               MMA issues lo*hi + hi*lo + hi*hi (~fp32 accuracy)
-//   warps 6..9  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
+//   warps 6..   epilogue (4 warps, or 8 for short K loops — two per TMEM lane
+//               quarter splitting the 32-column chunks): tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
 //               32*(w%4)..+31 = tile rows), fused row-scale / bias / ReLU /
 //               ReLU-backward bit mask, staged line-coalesced stores — or raw split-K partials
 //               that gemm_reduce_kernel sums in split order (deterministic).
@@ -35,14 +37,28 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;              // fp32 elements per k-block row = 128 bytes
 constexpr int A_STAGE = BM * BK * 4;  // 16 KB
-constexpr int kThreads = 320;  // 10 warps: TMA, MMA, 4 converters, 4 epilogue
-constexpr uint32_t kTileLd4 = 9;  // epilogue staging tile row stride in float4 (144 B)
-constexpr size_t kEpiSmem = 4 * 32 * kTileLd4 * 16;
+#ifndef GEMM_CONV_WARPS
+#define GEMM_CONV_WARPS 4
+#endif
+constexpr int kConvWarps = GEMM_CONV_WARPS;  // 3xTF32 converter warps (8 measured no faster)
+constexpr int kEpiWarp0 = 2 + kConvWarps;    // first epilogue warp
+// Epilogue warps per CTA (template EPIW): 4, one per TMEM lane quarter, or 8,
+// two per quarter splitting the 32-column chunks — for GEMMs with a short K
+// loop, which are bound by draining and storing the accumulator.
+template <int EPIW>
+constexpr int threads_for() { return 32 * (kEpiWarp0 + EPIW); }  // TMA, MMA, converters, epilogue
+constexpr uint32_t kTileLd4 = 9;
+constexpr uint32_t kMaxLo = 8;     // residual-slot barriers reserved (>= stages for CATGNN_GEMM_LO_SLOTS=0)
+constexpr uint32_t kMaxStages = 8;
+// barrier block: full/empty/conv per stage, tfull/tempty x2, lo_empty x kMaxLo, TMEM holder
+__host__ __device__ constexpr uint32_t kBarBytes(uint32_t S) { return ((3 * S + 4 + kMaxLo) * 8 + 8 + 15) / 16 * 16; }  // epilogue staging tile row stride in float4 (144 B)
+constexpr size_t epi_smem(int epiw) { return (size_t)epiw * 32 * kTileLd4 * 16; }
 
 struct GemmArgs {
   uint32_t M, N, K;
   uint32_t BN;
   uint32_t stages;
+  uint32_t lo_slots;  // 3xTF32: ring of lo (residual) tile slots, decoupled from the TMA stages
   uint32_t kb_per_split;
   uint32_t tmem_cols;
   uint32_t idesc;
@@ -69,10 +85,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 
 // Parity wait with a watchdog: a pipeline bug traps (kernel error) instead of
 // hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+#ifdef GEMM_WAIT_PROFILE
+// diagnostics build: nanoseconds each wait site spent blocked, summed over CTAs
+__device__ unsigned long long g_gemm_wait_ns[8];
+#endif
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase, int site = -1) {
   uint32_t done = 0;
   uint64_t t0 = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#ifdef GEMM_WAIT_PROFILE
+  struct Acc {
+    uint64_t t0; int site;
+    __device__ ~Acc() {
+      uint64_t t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (site >= 0 && (threadIdx.x & 31) == 0) atomicAdd(&g_gemm_wait_ns[site], (unsigned long long)(t1 - t0));
+    }
+  } acc{t0, site};
+#endif
   while (true) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -261,16 +291,17 @@ __device__ __forceinline__ void sts4(uint32_t a, float4 v) {
 // threads, 8 words in flight per thread (element-wise, so the SW128 layout of
 // the source carries over to the residual tile).
 __device__ __forceinline__ void convert_tile(uint32_t src, uint32_t dst, uint32_t n16, uint32_t t) {
-  for (uint32_t k0 = t; k0 < n16; k0 += 128 * 8) {
+  constexpr uint32_t NT = 32 * kConvWarps;
+  for (uint32_t k0 = t; k0 < n16; k0 += NT * 8) {
     float4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const uint32_t k = k0 + u * 128;
+      const uint32_t k = k0 + u * NT;
       if (k < n16) v[u] = lds4(src + k * 16);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const uint32_t k = k0 + u * 128;
+      const uint32_t k = k0 + u * NT;
       if (k < n16) sts4(dst + k * 16, tf32_residual4(v[u]));
     }
   }
@@ -289,12 +320,12 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 //              tile i's epilogue overlaps tile i+1's MMAs
 //   warps 2-5  3xTF32 converters (lo = x - tf32(x) tiles); in a pair they also
 //              relay "stage ready" to the rank-0 CTA's barrier
-//   warps 6-9  epilogue: tcgen05.ld -> fused epilogue -> 128-bit stores
+//   warps 6-9 (6-13) epilogue: tcgen05.ld -> fused epilogue -> 128-bit stores
 // Pair protocol: full[s] / empty[s] are per CTA (local TMA, multicast MMA
 // commit); conv[s] and tempty[b] live in the rank-0 CTA and count the arrivals
 // of both CTAs' converter / epilogue warps; tfull[b] is multicast.
-template <int NCTA>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NCTA, int EPIW>
+__global__ void __launch_bounds__(threads_for<EPIW>(), 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -306,18 +337,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool split3 = args.split3 != 0;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)S * A_STAGE;
-  uint8_t* sAl = sB + (size_t)S * B_STAGE;  // 3xTF32 residual tiles (same swizzled layout)
-  uint8_t* sBl = sAl + (split3 ? (size_t)S * A_STAGE : 0);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (split3 ? (size_t)S * B_STAGE : 0));
+  // 3xTF32 residual tiles (same swizzled layout) in a ring of L slots: the
+  // converters of stage `it` write slot it % L once the MMAs of stage it - L
+  // have drained it, so the TMA ring keeps S full stages in flight with only L
+  // residual copies (the skinny GEMMs are bound by that TMA round trip)
+  const uint32_t L = split3 ? args.lo_slots : 0;
+  uint8_t* sAl = sB + (size_t)S * B_STAGE;
+  uint8_t* sBl = sAl + (size_t)L * A_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (size_t)L * B_STAGE);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* conv = bars + 2 * S;
   uint64_t* tfull = bars + 3 * S;    // [2] accumulator ready
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* lo_empty = bars + 3 * S + 4;  // [L] residual slot drained by the MMAs
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 3 * S + 4 + kMaxLo);
   // epilogue staging: per epilogue warp a 32-row x 32-column tile, rows 144 B
   // apart (conflict-free 128-bit row and column-chunk accesses)
-  float4* epi_tiles = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(bars) + ((3 * S + 5) * 8 + 15) / 16 * 16);
+  float4* epi_tiles = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes(S));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = NCTA == 2 ? cluster_rank() : 0;
   const uint32_t cid = blockIdx.x / NCTA, ncl = gridDim.x / NCTA;  // pair index / count
@@ -329,12 +366,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t i = 0; i < S; ++i) {
       mbar_init(smem_u32(full + i), 1);
       mbar_init(smem_u32(empty + i), 1);
-      mbar_init(smem_u32(conv + i), 4 * NCTA);
+      mbar_init(smem_u32(conv + i), kConvWarps * NCTA);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(tfull + b), 1);
-      mbar_init(smem_u32(tempty + b), 4 * NCTA);
+      mbar_init(smem_u32(tempty + b), EPIW * NCTA);
     }
+    for (uint32_t j = 0; j < L; ++j) mbar_init(smem_u32(lo_empty + j), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -370,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         n0 += crank * BNh;
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
-          mbar_wait(smem_u32(empty + s), ph ^ 1);
+          mbar_wait(smem_u32(empty + s), ph ^ 1, 0);
           mbar_expect_tx(smem_u32(full + s), bytes);
           const int kx = (int)((kb0 + i) * BK);
           load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s), pol_a);
@@ -385,18 +423,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t m0, n0, kb0, nkb;
         tile_coords(args, t, m0, n0, kb0, nkb);
         const uint32_t b = j & 1;
-        mbar_wait(smem_u32(tempty + b), ((j >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(tempty + b), ((j >> 1) & 1) ^ 1, 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + b * acc_cols;
         const bool amn = args.a_mn != 0, bmn = args.b_mn != 0;
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
-          mbar_wait(smem_u32(via_conv ? conv + s : full + s), ph);
+          mbar_wait(smem_u32(via_conv ? conv + s : full + s), ph, 2);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
           const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
-          const uint32_t al = smem_u32(sAl + (size_t)s * A_STAGE);
-          const uint32_t bl = smem_u32(sBl + (size_t)s * B_STAGE);
+          const uint32_t lj = split3 ? it % L : 0;
+          const uint32_t al = smem_u32(sAl + (size_t)lj * A_STAGE);
+          const uint32_t bl = smem_u32(sBl + (size_t)lj * B_STAGE);
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
             const uint32_t first = (i > 0 || ks > 0) ? 1u : 0u;
@@ -419,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           commit_to<NCTA>(smem_u32(empty + s));
+          if (split3) commit_to<NCTA>(smem_u32(lo_empty + lj));
         }
         if (nkb) {
           commit_to<NCTA>(smem_u32(tfull + b));
@@ -429,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp < 6) {
+  } else if (warp < kEpiWarp0) {
     if (via_conv) {
       const uint32_t tt = threadIdx.x - 64;
       const uint32_t a4 = A_STAGE / 16, b4 = B_STAGE / 16;
@@ -439,10 +479,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(args, t, m0, n0, kb0, nkb);
         for (uint32_t i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % S, ph = (it / S) & 1;
-          mbar_wait(smem_u32(full + s), ph);
+          mbar_wait(smem_u32(full + s), ph, 3);
           if (split3) {
-            convert_tile(smem_u32(sA + (size_t)s * A_STAGE), smem_u32(sAl + (size_t)s * A_STAGE), a4, tt);
-            convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)s * B_STAGE), b4, tt);
+            const uint32_t lj = it % L, lph = (it / L) & 1;
+            mbar_wait(smem_u32(lo_empty + lj), lph ^ 1, 4);  // the MMAs of stage it - L are done with slot lj
+            convert_tile(smem_u32(sA + (size_t)s * A_STAGE), smem_u32(sAl + (size_t)lj * A_STAGE), a4, tt);
+            convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)lj * B_STAGE), b4, tt);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           }
           __syncwarp();
@@ -455,6 +497,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t ew = warp - kEpiWarp0;  // epilogue warp index
+    const uint32_t chalf = ew / 4;          // with 8 warps: chunks c = 32*(chalf + 2i)
+    constexpr uint32_t kCStep = 32 * (EPIW / 4);
     const GemmEpi& e = args.epi;
     uint32_t j = 0;
     for (uint32_t t = cid; t < args.tiles; t += ncl, ++j) {
@@ -462,23 +507,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(args, t, m0, n0, kb0, nkb);
       m0 += crank * BM;
       const uint32_t b = j & 1;
-      mbar_wait(smem_u32(tfull + b), (j >> 1) & 1);
+      mbar_wait(smem_u32(tfull + b), (j >> 1) & 1, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t row = m0 + q * 32 + lane;
       const bool row_ok = row < args.M;
       const float rs = (row_ok && e.rowscale) ? __ldg(e.rowscale + row) : 1.f;
       const uint32_t z = t / (args.nt * args.mt);
-      float4* T = epi_tiles + q * (32 * kTileLd4);
+      float4* T = epi_tiles + ew * (32 * kTileLd4);
       const uint32_t r8 = lane >> 3, c4 = lane & 7;
       const uint32_t rbase = m0 + q * 32;
       // ReLU-backward mask words are fetched one 32-column chunk ahead, so the
       // global load latency overlaps the previous chunk's TMEM drain and stores
       // (a whole-tile prefetch with the chunk loop unrolled measured slower)
       const uint32_t* mrow = (e.mask_bits && row_ok) ? e.mask_bits + (size_t)row * e.mask_words : nullptr;
-      uint32_t mw_next = (mrow && n0 < args.N) ? __ldg(mrow + n0 / 32) : 0xffffffffu;
-      for (uint32_t c = 0; c < BN; c += 32) {
+      const uint32_t cfirst = 32 * chalf;
+      uint32_t mw_next = (mrow && cfirst < BN && n0 + cfirst < args.N) ? __ldg(mrow + (n0 + cfirst) / 32) : 0xffffffffu;
+      for (uint32_t c = cfirst; c < BN; c += kCStep) {
         const uint32_t mw_cur = mw_next;
-        if (mrow && n0 + c + 32 < args.N && c + 32 < BN) mw_next = __ldg(mrow + (n0 + c + 32) / 32);
+        if (mrow && n0 + c + kCStep < args.N && c + kCStep < BN) mw_next = __ldg(mrow + (n0 + c + kCStep) / 32);
         float v[32];
         if (nkb) {
           tmem_ld32(tmem + b * acc_cols + ((q * 32u) << 16) + c, v);
@@ -704,11 +750,33 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
   const uint32_t b_stage = BNh * BK * 4;
-  const size_t stage_bytes = (size_t)(A_STAGE + b_stage) * (split3 ? 2 : 1);
-  const size_t budget = 227 * 1024 - 1024 - 512 - kEpiSmem;
-  uint32_t stages = (uint32_t)std::min<size_t>(6, budget / stage_bytes);
+  const size_t stage_bytes = (size_t)(A_STAGE + b_stage);
+  static const int lo_env = [] {
+    const char* v = std::getenv("CATGNN_GEMM_LO_SLOTS");
+    return v ? std::atoi(v) : 2;
+  }();
+  // short K loops (<= 4 k-blocks per tile, no split-K partials) are bound by the
+  // accumulator drain: 8 epilogue warps; otherwise 4 (more warps slow the
+  // compute-bound GEMMs through issue contention)
+  static const int epi_env = [] {
+    const char* v = std::getenv("CATGNN_GEMM_EPI_WARPS");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int epiw = epi_env == 4 || epi_env == 8 ? epi_env : (nkb <= 4 && splits == 1 ? 8 : 4);
+  const size_t kEpiSmem = epi_smem(epiw);
+  const size_t budget = 227 * 1024 - 1024 - kBarBytes(kMaxStages) - kEpiSmem;
+  uint32_t stages, lo_slots = 0;
+  if (split3 && lo_env > 0) {
+    lo_slots = (uint32_t)std::min<int>(lo_env, (int)kMaxLo);
+    stages = (uint32_t)std::min<size_t>(kMaxStages, (budget - lo_slots * stage_bytes) / stage_bytes);
+  } else if (split3) {  // CATGNN_GEMM_LO_SLOTS=0: one residual copy per stage (previous layout)
+    stages = (uint32_t)std::min<size_t>(6, budget / (2 * stage_bytes));
+    lo_slots = stages;
+  } else {
+    stages = (uint32_t)std::min<size_t>(kMaxStages, budget / stage_bytes);
+  }
   if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + ((3 * stages + 5) * 8 + 15) / 16 * 16 + kEpiSmem;
+  const size_t smem = 1024 + (size_t)(stages + lo_slots) * stage_bytes + kBarBytes(stages) + kEpiSmem;
 
   GemmArgs args{};
   args.M = M;
@@ -716,6 +784,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   args.K = K;
   args.BN = BN;
   args.stages = stages;
+  args.lo_slots = lo_slots;
   args.kb_per_split = kbps;
   args.tmem_cols = pow2_cols(2 * round_up(BN, 32));  // two accumulator buffers
   args.split3 = split3 ? 1u : 0u;
@@ -750,11 +819,13 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   }
   CUtensorMap ta = a.mn_major ? make_map_mn(A, M, K, lda) : make_map(A, M, K, lda, BM);
   CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BNh);
-  static bool attr_set[2] = {false, false};
-  auto kern = pair ? gemm_tf32_kernel<2> : gemm_tf32_kernel<1>;
-  if (!attr_set[ncta - 1]) {
+  static bool attr_set[2][2] = {{false, false}, {false, false}};
+  auto kern = pair ? (epiw == 8 ? gemm_tf32_kernel<2, 8> : gemm_tf32_kernel<2, 4>)
+                   : (epiw == 8 ? gemm_tf32_kernel<1, 8> : gemm_tf32_kernel<1, 4>);
+  const int kThreads = epiw == 8 ? threads_for<8>() : threads_for<4>();
+  if (!attr_set[ncta - 1][epiw == 8]) {
     CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set[ncta - 1] = true;
+    attr_set[ncta - 1][epiw == 8] = true;
   }
   // timing label: the GEMM's shape class (row-sized extents as "rows")
   auto dim = [](uint32_t x) { return x > 4096 ? std::string("rows") : std::to_string(x); };
@@ -792,6 +863,24 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
 }
 
 }  // namespace catgnn
+
+// Diagnostics (GEMM_WAIT_PROFILE builds): per wait site, the nanoseconds
+// warps spent blocked since the last call (0 producer empty, 1 MMA tempty,
+// 2 MMA conv/full, 3 converter full, 4 converter lo slot, 5 epilogue tfull).
+extern "C" int catgnn_debug_gemm_waits(unsigned long long* out8) {
+  using namespace catgnn;
+  return guarded([&] {
+#ifdef GEMM_WAIT_PROFILE
+    CG_CUDA(cudaDeviceSynchronize());
+    CG_CUDA(cudaMemcpyFromSymbol(out8, g_gemm_wait_ns, 8 * sizeof(unsigned long long)));
+    const unsigned long long z[8] = {0};
+    CG_CUDA(cudaMemcpyToSymbol(g_gemm_wait_ns, z, sizeof(z)));
+#else
+    (void)out8;
+    throw ConfigError("library built without GEMM_WAIT_PROFILE");
+#endif
+  });
+}
 
 // General test hook: A is M x K (a_mn = 0) or K x M (a_mn = 1), B is N x K or
 // K x N, all host row-major; C = A . B^T in the logical (M x K).(N x K)^T sense.
