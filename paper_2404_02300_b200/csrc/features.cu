@@ -50,14 +50,36 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const float* __restric
   for (uint64_t r = warp; r < rows; r += nwarps) {
     const float* s = src + __ldg(ext + r) * dim;
     float* d = dst + r * ld;
-    if (V == 4) {
-      for (uint32_t c = lane * 4; c < dim; c += 128)
-        *reinterpret_cast<float4*>(d + c) = __ldg(reinterpret_cast<const float4*>(s + c));
-    } else if (V == 2) {
-      for (uint32_t c = lane * 2; c < dim; c += 64)
-        *reinterpret_cast<float2*>(d + c) = __ldg(reinterpret_cast<const float2*>(s + c));
-    } else {
-      for (uint32_t c = lane; c < dim; c += 32) d[c] = __ldg(s + c);
+    // U vector loads in flight per lane before their stores (a 602-wide row is
+    // 10 float2 per lane: one round trip instead of ten)
+    constexpr int U = 8;
+    constexpr uint32_t step = 32 * V;
+    for (uint32_t c0 = lane * V; c0 < dim; c0 += step * U) {
+      if (V == 4) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * step < dim) v[u] = __ldg(reinterpret_cast<const float4*>(s + c0 + u * step));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * step < dim) *reinterpret_cast<float4*>(d + c0 + u * step) = v[u];
+      } else if (V == 2) {
+        float2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * step < dim) v[u] = __ldg(reinterpret_cast<const float2*>(s + c0 + u * step));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * step < dim) *reinterpret_cast<float2*>(d + c0 + u * step) = v[u];
+      } else {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * step < dim) v[u] = __ldg(s + c0 + u * step);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (c0 + u * step < dim) d[c0 + u * step] = v[u];
+      }
     }
   }
 }
