@@ -368,3 +368,37 @@ def test_timing_records_label_kernels(graph):
     ctx.set_kernel_timing(False)
     assert any(k.startswith("K2 agg w") for k in rec) and any(k.startswith("K3 gemm") for k in rec)
     assert all(v[0] > 0 and v[1] >= 1 for v in rec.values())
+
+
+def test_nccl_collectives_inside_cuda_graph(graph):
+    """The N > 1 step captured as a CUDA graph (bench.py) holds the C1
+    all-reduce and the feature all-gather: with a 1-rank communicator the
+    captured collectives must replay (sum over one rank = identity)."""
+    import torch
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import Comm, GNNModel
+    stream = torch.cuda.Stream()
+    ctx = gp.Context(0, stream.cuda_stream)
+    comm = Comm(ctx, 1, 0, Comm.unique_id())
+    m = GNNModel("gcn", 2, 16, 32, 4, seed=1, ctx=ctx)
+    store = gp.FeatureStore(64, 8, ctx)
+    feats = torch.empty((64, 8), dtype=torch.float32).pin_memory()
+    feats.numpy()[:] = np.arange(512, dtype=np.float32).reshape(64, 8)
+    p0 = m.get_params()
+    m.scale(2.0)
+    m.allreduce(comm)  # eager warm-up
+    torch.cuda.synchronize()
+    store.reset_deps()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        m.scale(0.5)
+        m.allreduce(comm)
+        store.upload(feats.numpy())
+        store.allgather(comm, 64)
+    store.reset_deps()
+    with torch.cuda.stream(stream):
+        g.replay()
+        g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(m.get_params(), (p0 * 2.0 * 0.5 * 0.5).astype(np.float32))
+    comm.close()
