@@ -48,6 +48,7 @@ struct Layer {
   uint32_t d_in = 0, d_out = 0;
   uint32_t K_in = 0;    // round4(d_in): activation row stride of the input
   uint32_t D_out = 0;   // round4(d_out)
+  uint32_t ld_act = 0;  // row stride of this layer's output activations (>= D_out)
   bool agg_first = false;
   // internal weight matrix (GEMM B operand): w_rows x w_cols
   uint32_t w_rows = 0, w_cols = 0;
@@ -323,6 +324,10 @@ const uint32_t kPadNarrow = [] {
   return v ? (uint32_t)std::atoi(v) : 16u;
 }();
 uint32_t act_width(uint32_t d) { return d < 128 ? round_up(d, kPadNarrow) : round_up(d, 4); }
+const bool kNarrowLd64 = [] {  // A/B knob; measured no faster on reddit (off)
+  const char* v = std::getenv("CATGNN_NARROW_LD64");
+  return v ? v[0] != '0' : false;
+}();
 
 void plan_layers(catgnn_model_s* M) {
   const auto& c = M->cfg;
@@ -334,6 +339,11 @@ void plan_layers(catgnn_model_s* M) {
     L.d_out = l + 1 == c.layers ? c.classes : c.hidden;
     L.K_in = l == 0 ? round_up(L.d_in, 4) : act_width(L.d_in);  // layer 0 reads the shard's x
     L.D_out = act_width(L.d_out);
+    // CATGNN_NARROW_LD64=1: narrow GCN/GIN activations (33-64 floats, e.g. the
+    // 41 classes padded to 48) stored 64 floats apart, so every gathered row
+    // starts on a 128-byte line (two L1 wavefronts per 48-float row instead of
+    // 2.5); measured no faster, the 48-wide pass is not wavefront-bound
+    L.ld_act = (kNarrowLd64 && c.kind != CATGNN_MODEL_SAGE && L.D_out > 32 && L.D_out <= 64) ? 64 : L.D_out;
     if (c.kind == CATGNN_MODEL_SAGE) {
       L.agg_first = L.d_in <= L.d_out;
       if (L.agg_first) {
@@ -445,7 +455,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
     Bufs& b = B[l];
     b.in = in;
     b.in_ld = in_ld;
-    b.out_ld = L.D_out;
+    b.out_ld = L.ld_act;
     b.out = act(ctx, nm("H", l), rows, b.out_ld, fresh);
     if (!last) {
       b.bits_words = (L.D_out + 31) / 32;
@@ -486,7 +496,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       e.bits_out = b.bits; e.bits_words = b.bits_words;
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN transform-first
-      b.mid_ld = L.D_out;
+      b.mid_ld = L.ld_act;
       b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
       GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld; e.rowscale = gcn ? S->dinv.p : nullptr;
       gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
@@ -514,8 +524,8 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   const size_t nl = M->layers.size();
   // K4: dZ of the last layer
   const Layer& LL = M->layers[nl - 1];
-  float* dZ = act(ctx, nm("dZ", nl - 1), rows, LL.D_out, false);
-  CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.D_out * 4, st));
+  float* dZ = act(ctx, nm("dZ", nl - 1), rows, LL.ld_act, false);
+  CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   const uint64_t ntr = S->h_train.size();
   double loss = 0.0;
   double* row_loss = ctx->scratch_buf<double>("row_loss", std::max<uint64_t>(1, ntr));
@@ -527,19 +537,19 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   // dinv * dZ, produced here by K4 instead of per edge in K2
   float* dZs = nullptr;
   if (gcn && !LL.agg_first) {
-    dZs = act(ctx, "dZs", rows, LL.D_out, false);
-    CG_CUDA(cudaMemsetAsync(dZs, 0, std::max<uint64_t>(1, rows) * LL.D_out * 4, st));
+    dZs = act(ctx, "dZs", rows, LL.ld_act, false);
+    CG_CUDA(cudaMemsetAsync(dZs, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   }
   if (ntr) {
     softmax_ce_kernel<<<grid1d(ntr * 32), 256, 0, st>>>(B[nl - 1].out, B[nl - 1].out_ld, LL.d_out,
-                                                      S->labels.p, S->d_train.p, ntr, dZ, LL.D_out, row_loss,
+                                                      S->labels.p, S->d_train.p, ntr, dZ, LL.ld_act, row_loss,
                                                       dZs ? S->dinv.p : nullptr, dZs);
     CG_CHECK_LAUNCH();
     sum_doubles_kernel<<<1, 1024, 0, st>>>(row_loss, ntr, loss_dev);
     CG_CHECK_LAUNCH();
     ctx->launches += 2;
   }
-  uint32_t dZ_ld = LL.D_out;
+  uint32_t dZ_ld = LL.ld_act;
   for (size_t li = nl; li-- > 0;) {
     const Layer& L = M->layers[li];
     const Bufs& b = B[li];
@@ -600,18 +610,18 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         aggregate(S, a);
       }
     } else {  // GCN / GIN transform-first
-      float* dT = act(ctx, "dmid", rows, L.D_out, false);
+      float* dT = act(ctx, "dmid", rows, L.ld_act, false);
       AggArgs a;
       a.in = dZ; a.in_ld = dZ_ld; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
       if (li == nl - 1 && dZs) { a.in = dZs; a.pre = nullptr; }  // pre-scaled by K4
-      a.out = dT; a.out_ld = L.D_out; a.width = L.D_out;
+      a.out = dT; a.out_ld = L.ld_act; a.width = L.D_out;
       aggregate(S, a);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
-      gemm(ctx, GemmOperand{dT, L.D_out, true}, GemmOperand{b.in, b.in_ld, true}, L.d_out, L.w_cols,
+      gemm(ctx, GemmOperand{dT, L.ld_act, true}, GemmOperand{b.in, b.in_ld, true}, L.d_out, L.w_cols,
            (uint32_t)rows, e, 0, kBwdPrecision);
       if (need_dx) {
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
-        gemm(ctx, GemmOperand{dT, L.D_out, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true},
+        gemm(ctx, GemmOperand{dT, L.ld_act, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true},
              (uint32_t)rows, L.w_cols, L.d_out, e2, 1, kBwdPrecision);
       }
     }
@@ -868,8 +878,8 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
     const Layer& L = m->layers[layer];
     const float* src = nullptr;
     uint32_t ld = 0, w = L.d_out;
-    if (what == 0) { src = m->ctx->scratch_buf<float>(nm("H", layer), 1); ld = L.D_out; }
-    else if (what == 2) { src = m->ctx->scratch_buf<float>(nm("dZ", layer), 1); ld = L.D_out; }
+    if (what == 0) { src = m->ctx->scratch_buf<float>(nm("H", layer), 1); ld = L.ld_act; }
+    else if (what == 2) { src = m->ctx->scratch_buf<float>(nm("dZ", layer), 1); ld = L.ld_act; }
     else throw ConfigError("export: what must be 0 (H) or 2 (dZ)");
     if (width) *width = w;
     if (out && s->rows)
