@@ -475,6 +475,10 @@ AggFn pick_kernel(uint32_t w4, bool pre, bool bits, int* lpn_out) {
   if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre, bits); }
   if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre, bits); }
   if (w4 <= 16) { *lpn_out = 8; return pick_pre<2, 8>(pre, bits); }
+  // 129-192 floats (e.g. 172 classes): 16 lanes x 3 float4, two neighbours per
+  // load instruction (48 float4 slots instead of 64)
+  static const int mid16 = env_int("CATGNN_AGG_MID16", 1);
+  if (mid16 && w4 > 32 && w4 <= 48) { *lpn_out = 16; return pick_pre<3, 16>(pre, bits); }
   *lpn_out = 32;
   switch ((w4 + 31) / 32) {
     case 1: return pick_pre<1, 32>(pre, bits);

@@ -5,6 +5,7 @@ algorithmic GB/s per SURVEY §8(d).  Env: WIDTHS=256,44,48 REPS=10."""
 import json
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -24,15 +25,23 @@ for width in widths:
     inf = s.info
     gp.sgc_propagate(s, 1)
     flush = os.environ.get("FLUSH") == "1"  # evict L2 before every pass (cold-input case)
-    if flush:
+    load = os.environ.get("TENSOR_LOAD") == "1"  # a tensor-core burst before every pass (power state)
+    if flush or load:
         import torch
         junk = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        ma = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
     ctx.set_kernel_timing(True)
     for _ in range(reps):
         if flush:
             torch.cuda.synchronize()
             junk.fill_(1)
             torch.cuda.synchronize()
+        if load:
+            for _ in range(int(os.environ.get("LOAD_N", "20"))):
+                ma2 = ma @ ma
+            torch.cuda.synchronize()
+            if os.environ.get("LOAD_GAP_MS"):
+                time.sleep(float(os.environ["LOAD_GAP_MS"]) / 1e3)
         gp.lib.catgnn_sgc_propagate(s.handle, 1)
     kt = ctx.kernel_time()
     ctx.set_kernel_timing(False)

@@ -19,6 +19,8 @@ CASES = [  # kind, in_dim, hidden, classes, layers  (covers aggregate-first and 
     ("sage", 64, 256, 8, 2),   # config-1 shape: aggregate-first then transform-first
     ("sage", 100, 32, 47, 3),  # transform-first, 3 layers, odd class count
     ("gin", 12, 48, 6, 2),
+    ("gin", 140, 256, 172, 2),  # 129-192-wide aggregations (16 lanes x 3 float4): 140 fwd, 172 fwd/bwd
+    ("gcn", 150, 160, 12, 2),   # 152-wide aggregate-first with the GCN source scale and ReLU bits
 ]
 
 

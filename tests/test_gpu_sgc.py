@@ -144,7 +144,7 @@ def test_sgc_propagate_star_kat(gp):
     np.testing.assert_array_equal(gp.sgc_propagate(s, 0).ravel(), [0.0, 3.0, 3.0])
 
 
-@pytest.mark.parametrize("dim", [1, 4, 8, 12, 48, 64, 100, 256, 602, 1433])
+@pytest.mark.parametrize("dim", [1, 4, 8, 12, 48, 64, 100, 132, 172, 192, 256, 602, 1433])
 def test_sgc_propagate_widths(gp, dim):
     rng = np.random.default_rng(dim)
     rows = 700
