@@ -67,6 +67,7 @@ struct GemmArgs {
   uint32_t a_mn, b_mn;  // operand stored MN-major ([K rows][M or N cols] row-major)
   uint32_t bm;          // tile rows: BM x CTAs per tile
   uint32_t a_stream, b_stream;  // operand read once per GEMM (row-sized): L2 evict-first loads
+  uint32_t b_lo_tma;            // 3xTF32: B residual precomputed, TMA-loaded per stage
   GemmEpi epi;
 };
 
@@ -257,6 +258,13 @@ __device__ __forceinline__ float4 tf32_residual4(float4 v) {
   return make_float4(tf32_residual(v.x), tf32_residual(v.y), tf32_residual(v.z), tf32_residual(v.w));
 }
 
+// B residual for b_lo_tma: lo = x - tf32(x) over the whole operand buffer
+// (same rounding as the converters).
+__global__ void residual_kernel(const float* __restrict__ x, float* __restrict__ lo, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    lo[i] = tf32_residual(x[i]);
+}
+
 __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
   if (e.rowscale && col >= e.scale_col_begin) v *= __ldg(e.rowscale + row);
   if (e.bias) v += __ldg(e.bias + col);
@@ -327,7 +335,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 template <int NCTA, int EPIW>
 __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmArgs args) {
+                     const __grid_constant__ CUtensorMap tmBl, const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t BN = args.BN;
@@ -341,10 +349,15 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
   // converters of stage `it` write slot it % L once the MMAs of stage it - L
   // have drained it, so the TMA ring keeps S full stages in flight with only L
   // residual copies (the skinny GEMMs are bound by that TMA round trip)
+  // With b_lo_tma the B residual (a small weight operand, reused by every
+  // tile) is precomputed once per GEMM and TMA-loaded with each stage
+  // (sBt[s]); the converters then only split A.
   const uint32_t L = split3 ? args.lo_slots : 0;
-  uint8_t* sAl = sB + (size_t)S * B_STAGE;
+  const bool blt = split3 && args.b_lo_tma;
+  uint8_t* sBt = sB + (size_t)S * B_STAGE;
+  uint8_t* sAl = sBt + (blt ? (size_t)S * B_STAGE : 0);
   uint8_t* sBl = sAl + (size_t)L * A_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (size_t)L * B_STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (blt ? 0 : (size_t)L * B_STAGE));
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* conv = bars + 2 * S;
@@ -397,7 +410,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = A_STAGE + B_STAGE;
+      const uint32_t bytes = A_STAGE + B_STAGE * (blt ? 2 : 1);
       const uint64_t ef = policy_evict_first();
       const uint64_t pol_a = args.a_stream ? ef : 0, pol_b = args.b_stream ? ef : 0;
       uint32_t it = 0;
@@ -413,6 +426,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
           const int kx = (int)((kb0 + i) * BK);
           load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s), pol_a);
           load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), pol_b);
+          if (blt) load_operand(smem_u32(sBt + (size_t)s * B_STAGE), &tmBl, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), 0);
         }
       }
     }
@@ -435,7 +449,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
           const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
           const uint32_t lj = split3 ? it % L : 0;
           const uint32_t al = smem_u32(sAl + (size_t)lj * A_STAGE);
-          const uint32_t bl = smem_u32(sBl + (size_t)lj * B_STAGE);
+          const uint32_t bl = blt ? smem_u32(sBt + (size_t)s * B_STAGE) : smem_u32(sBl + (size_t)lj * B_STAGE);
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
             const uint32_t first = (i > 0 || ks > 0) ? 1u : 0u;
@@ -484,7 +498,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
             const uint32_t lj = it % L, lph = (it / L) & 1;
             mbar_wait(smem_u32(lo_empty + lj), lph ^ 1, 4);  // the MMAs of stage it - L are done with slot lj
             convert_tile(smem_u32(sA + (size_t)s * A_STAGE), smem_u32(sAl + (size_t)lj * A_STAGE), a4, tt);
-            convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)lj * B_STAGE), b4, tt);
+            if (!blt) convert_tile(smem_u32(sB + (size_t)s * B_STAGE), smem_u32(sBl + (size_t)lj * B_STAGE), b4, tt);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           }
           __syncwarp();
@@ -750,7 +764,16 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
   const uint32_t b_stage = BNh * BK * 4;
-  const size_t stage_bytes = (size_t)(A_STAGE + b_stage);
+  // 3xTF32 with a small, heavily reused B (the weights of a forward / input-
+  // gradient GEMM): its residual is computed once here and TMA-loaded with each
+  // stage, so the converters split only A (less shared-memory traffic and power)
+  static const int blo_env = [] {
+    const char* v = std::getenv("CATGNN_GEMM_B_LO");
+    return v ? std::atoi(v) : 0;  // A/B knob: measured no faster on reddit (off)
+  }();
+  const bool blt = split3 && blo_env && (uint64_t)N * K <= (4ull << 20) && M >= 4096 && splits == 1;
+  const size_t stage_bytes = (size_t)A_STAGE + (size_t)b_stage * (blt ? 2 : 1);
+  const size_t lo_bytes = (size_t)A_STAGE + (blt ? 0 : (size_t)b_stage);  // one residual slot
   static const int lo_env = [] {
     const char* v = std::getenv("CATGNN_GEMM_LO_SLOTS");
     return v ? std::atoi(v) : 2;
@@ -768,15 +791,15 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   uint32_t stages, lo_slots = 0;
   if (split3 && lo_env > 0) {
     lo_slots = (uint32_t)std::min<int>(lo_env, (int)kMaxLo);
-    stages = (uint32_t)std::min<size_t>(kMaxStages, (budget - lo_slots * stage_bytes) / stage_bytes);
+    stages = (uint32_t)std::min<size_t>(kMaxStages, (budget - lo_slots * lo_bytes) / stage_bytes);
   } else if (split3) {  // CATGNN_GEMM_LO_SLOTS=0: one residual copy per stage (previous layout)
-    stages = (uint32_t)std::min<size_t>(6, budget / (2 * stage_bytes));
+    stages = (uint32_t)std::min<size_t>(6, budget / (stage_bytes + lo_bytes));
     lo_slots = stages;
   } else {
     stages = (uint32_t)std::min<size_t>(kMaxStages, budget / stage_bytes);
   }
   if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
-  const size_t smem = 1024 + (size_t)(stages + lo_slots) * stage_bytes + kBarBytes(stages) + kEpiSmem;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (size_t)lo_slots * lo_bytes + kBarBytes(stages) + kEpiSmem;
 
   GemmArgs args{};
   args.M = M;
@@ -785,6 +808,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   args.BN = BN;
   args.stages = stages;
   args.lo_slots = lo_slots;
+  args.b_lo_tma = blt ? 1u : 0u;
   args.kb_per_split = kbps;
   args.tmem_cols = pow2_cols(2 * round_up(BN, 32));  // two accumulator buffers
   args.split3 = split3 ? 1u : 0u;
@@ -818,7 +842,19 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     args.epi.partial = nullptr;
   }
   CUtensorMap ta = a.mn_major ? make_map_mn(A, M, K, lda) : make_map(A, M, K, lda, BM);
+  const float* Blo = B;
+  if (blt) {  // the residual of B's whole extent ([N][ldb] K-major, [K][ldb] MN-major)
+    const uint64_t rows_b = b.mn_major ? K : N, cols_b = b.mn_major ? N : K;
+    const uint64_t count = (rows_b - 1) * ldb + cols_b;
+    float* lo = ctx->scratch_buf<float>("gemm_b_lo", count);
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, 148 * 8));
+    residual_kernel<<<g, 256, 0, ctx->stream>>>(B, lo, count);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+    Blo = lo;
+  }
   CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BNh);
+  CUtensorMap tbl = blt ? (b.mn_major ? make_map_mn(Blo, N, K, ldb) : make_map(Blo, N, K, ldb, BNh)) : tb;
   static bool attr_set[2][2] = {{false, false}, {false, false}};
   auto kern = pair ? (epiw == 8 ? gemm_tf32_kernel<2, 8> : gemm_tf32_kernel<2, 4>)
                    : (epiw == 8 ? gemm_tf32_kernel<1, 8> : gemm_tf32_kernel<1, 4>);
@@ -846,9 +882,9 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     cfg.stream = ctx->stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
+    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tbl, args));
   } else {
-    kern<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, args);
+    kern<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, tbl, args);
   }
   CG_CHECK_LAUNCH();
   ctx->launches++;
