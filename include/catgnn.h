@@ -148,6 +148,14 @@ int catgnn_features_upload(catgnn_features f, const float* host, uint64_t row_be
  * producers and consumers by stream order from then on (before capturing a
  * CUDA graph that uploads into and gathers from the store). */
 int catgnn_features_reset_deps(catgnn_features f);
+/* split_features (proj/include/gnnpart/store.hpp:63, store.cpp:97-116): writes
+ * <out_dir>/part-<s>/features.bin (FEA1) holding the rows of the global FEA1
+ * matrix `features` named by partition s's node table, in node-table order —
+ * byte-identical to the reference's files.  The matrix is read once and the
+ * rows are gathered on the device instead of one seek per node record.
+ * DataError (3) for a bad header or a node id past the matrix. */
+int catgnn_split_features(catgnn_ctx ctx, catgnn_artifact a, const char* features, const char* out_dir,
+                          uint32_t* files_written);
 int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f);
 /* Multi-GPU refresh of a feature store: rank r uploads rows [r*R, (r+1)*R)
  * (catgnn_features_upload with row_begin = r*R), then this in-place NCCL

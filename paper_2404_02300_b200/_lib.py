@@ -49,6 +49,7 @@ def _load():
         "catgnn_ctx_set_kernel_timing": (C.c_int, [vp, C.c_int]),
         "catgnn_ctx_wait": (C.c_int, [vp, vp]),
         "catgnn_features_reset_deps": (C.c_int, [vp]),
+        "catgnn_split_features": (C.c_int, [vp, vp, C.c_char_p, C.c_char_p, P(u32)]),
         "catgnn_model_last_loss_async": (C.c_int, [vp, P(f64), P(u64)]),
         "catgnn_ctx_set_sm_budget": (C.c_int, [vp, C.c_int, C.c_int]),
         "catgnn_ctx_kernel_time": (C.c_int, [vp, P(f64), P(u64), P(f64), P(u64)]),

@@ -9,8 +9,11 @@
 // the shard's padded layout x[r][0..ld) with ld = round_up(dim, 4); padding
 // columns stay zero.  HBM-bound: rows*dim*4 read + rows*ld*4 written.
 #include <algorithm>
+#include <cstdio>
+#include <filesystem>
 #include <map>
 
+#include "artifact.hpp"
 #include "comm.hpp"
 #include "shard.hpp"
 
@@ -211,5 +214,79 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
       if (!ev) CG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       CG_CUDA(cudaEventRecord(ev, st));
     }
+  });
+}
+
+// split_features (store.cpp:97-116): part-<s>/features.bin = the rows of the
+// global FEA1 matrix named by partition s's node table, in node-table order.
+// The reference seeks and reads one row per node record; here the matrix is
+// read once (bulk, pinned), uploaded, and every partition's rows are gathered
+// on the device and written back as FEA1 files.
+int catgnn_split_features(catgnn_ctx ctx, catgnn_artifact a, const char* features, const char* out_dir,
+                          uint32_t* files_written) {
+  return guarded([&] {
+    if (!ctx || !a || !features || !out_dir) throw ConfigError("null argument");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    namespace fs = std::filesystem;
+    const FeatureFile h = read_feature_header(features);
+    const size_t total = h.rows * (size_t)h.dim;
+    cudaStream_t st = ctx->stream;
+    float* pinned = nullptr;
+    CG_CUDA(cudaMallocHost(&pinned, std::max<size_t>(1, total) * 4));
+    struct Pinned {
+      float* p;
+      ~Pinned() { cudaFreeHost(p); }
+    } guard{pinned};
+    {
+      FILE* f = std::fopen(features, "rb");
+      if (!f) throw DataError(std::string("cannot open feature file: ") + features);
+      std::fseek(f, 20, SEEK_SET);
+      const size_t got = total ? std::fread(pinned, 4, total, f) : 0;
+      std::fclose(f);
+      if (got != total) throw DataError(std::string("short feature read: ") + features);
+    }
+    DevBuf<float> src;
+    src.alloc(std::max<size_t>(1, total));
+    if (total) CG_CUDA(cudaMemcpyAsync(src.p, pinned, total * 4, cudaMemcpyHostToDevice, st));
+    uint32_t written = 0;
+    for (uint32_t s = 0; s < a->num_partitions; ++s) {
+      const auto& ext = a->parts[s].ext;
+      for (uint64_t id : ext)  // FeatureFileReader::read_row (store.cpp:55-58)
+        if (id >= h.rows)
+          throw DataError("feature row " + std::to_string(id) + " out of range in " + std::string(features));
+      const uint64_t rows = ext.size();
+      DevBuf<uint64_t> ids;
+      DevBuf<float> dst;
+      ids.alloc(std::max<uint64_t>(1, rows));
+      dst.alloc(std::max<size_t>(1, rows * (size_t)h.dim));
+      if (rows) {
+        CG_CUDA(cudaMemcpyAsync(ids.p, ext.data(), rows * 8, cudaMemcpyHostToDevice, st));
+        const unsigned grid = (unsigned)std::min<uint64_t>((rows + 7) / 8, (uint64_t)ctx->num_sms * 8);
+        if (h.dim % 4 == 0)
+          gather_rows_kernel<4><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim);
+        else if (h.dim % 2 == 0)
+          gather_rows_kernel<2><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim);
+        else
+          gather_rows_kernel<1><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim);
+        CG_CHECK_LAUNCH();
+        ctx->launches++;
+        CG_CUDA(cudaMemcpyAsync(pinned, dst.p, rows * (size_t)h.dim * 4, cudaMemcpyDeviceToHost, st));
+      }
+      CG_CUDA(cudaStreamSynchronize(st));
+      const fs::path part_dir = fs::path(out_dir) / ("part-" + std::to_string(s));
+      fs::create_directories(part_dir);
+      const std::string out_path = (part_dir / "features.bin").string();
+      FILE* f = std::fopen(out_path.c_str(), "wb");
+      if (!f) throw DataError("cannot write feature file: " + out_path);
+      const uint32_t dtype = 1;
+      bool ok = std::fwrite("FEA1", 1, 4, f) == 4 && std::fwrite(&rows, 8, 1, f) == 1 &&
+                std::fwrite(&h.dim, 4, 1, f) == 1 && std::fwrite(&dtype, 4, 1, f) == 1;
+      const size_t n = rows * (size_t)h.dim;
+      if (ok && n) ok = std::fwrite(pinned, 4, n, f) == n;
+      ok = (std::fclose(f) == 0) && ok;
+      if (!ok) throw DataError("short write: " + out_path);
+      ++written;
+    }
+    if (files_written) *files_written = written;
   });
 }

@@ -551,6 +551,18 @@ class TrainingData:
     artifact: Optional[Artifact] = None
 
 
+def split_features(features: str, artifact_dir: str, out_dir: str, ctx: Optional[Context] = None) -> int:
+    """store.cpp:97-116: part-<s>/features.bin for every partition of the
+    artifact from the global FEA1 matrix (device row gather); returns the
+    number of files written."""
+    ctx = ctx or default_context()
+    art = Artifact(artifact_dir)
+    n = C.c_uint32()
+    check(lib.catgnn_split_features(ctx.handle, art.handle, str(features).encode(), str(out_dir).encode(),
+                                    C.byref(n)))
+    return int(n.value)
+
+
 def load_training_data(artifact_dir: str, input: str = "", features: str = "",
                        ctx: Optional[Context] = None, with_global: bool = True) -> TrainingData:
     """train.cpp:216-287: one device shard per partition plus the global shard."""

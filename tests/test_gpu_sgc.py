@@ -296,3 +296,27 @@ def test_feature_store_allgather_single_rank(gp, golden):
     with pytest.raises(gp.ConfigError):
         store.allgather(comm, n + 1)
     comm.close()
+
+
+def test_split_features_byte_identical_to_reference(gp, small_ds, small_artifact, tmp_path):
+    """split_features (store.cpp:97-116): the files the reference wrote into the
+    artifact are reproduced byte for byte by the device row gather."""
+    import os
+    n = gp.split_features(small_ds["feat_file"], small_artifact, str(tmp_path))
+    assert n == 2
+    for s in range(n):
+        mine = open(os.path.join(str(tmp_path), f"part-{s}", "features.bin"), "rb").read()
+        theirs = open(os.path.join(small_artifact, f"part-{s}", "features.bin"), "rb").read()
+        assert mine == theirs
+    # a node id past the matrix is a DataError, as in FeatureFileReader::read_row
+    short = str(tmp_path / "short.bin")
+    with open(small_ds["feat_file"], "rb") as f:
+        data = bytearray(f.read())
+    rows = int.from_bytes(data[4:12], "little")
+    dim = int.from_bytes(data[12:16], "little")
+    keep = rows // 2
+    data[4:12] = keep.to_bytes(8, "little")
+    with open(short, "wb") as f:
+        f.write(bytes(data[:20 + keep * dim * 4]))
+    with pytest.raises(gp.DataError):
+        gp.split_features(short, small_artifact, str(tmp_path / "x"))
