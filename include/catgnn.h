@@ -209,6 +209,14 @@ int catgnn_index_destroy(catgnn_index idx);
 int catgnn_complete_edges(catgnn_ctx ctx, const uint64_t* edges, uint64_t num_edges, const uint32_t* home,
                           const uint8_t* roles, uint64_t num_nodes, uint32_t p, uint32_t hops,
                           catgnn_completion* out);
+/* Same over an edge file (EDG1 `.bin` streamed in chunks through one pinned
+ * buffer — the stream never sits in host RAM; text files are read whole), with
+ * EdgeReader's add_reverse expansion (edge_stream.cpp:138-148) done on the
+ * device.  Identical results to reading the stream and calling
+ * catgnn_complete_edges. */
+int catgnn_complete_edges_file(catgnn_ctx ctx, const char* path, int add_reverse, const uint32_t* home,
+                               const uint8_t* roles, uint64_t num_nodes, uint32_t p, uint32_t hops,
+                               catgnn_completion* out);
 /* Same for arbitrary 64-bit external ids: endpoints are routed through the
  * device graph index (GraphIndex::dense); home[] and roles[] are indexed by
  * dense id as the reference's HomeMap (completion.hpp:55-59) is. */

@@ -72,6 +72,7 @@ def _load():
         "catgnn_features_allgather": (C.c_int, [vp, vp, u64]),
         "catgnn_complete_edges": (C.c_int, [vp, vp, u64, vp, vp, u64, u32, u32, P(vp)]),
         "catgnn_complete_edges_indexed": (C.c_int, [vp, vp, vp, u64, vp, vp, u32, u32, P(vp)]),
+        "catgnn_complete_edges_file": (C.c_int, [vp, C.c_char_p, C.c_int, vp, vp, u64, u32, u32, P(vp)]),
         "catgnn_index_build": (C.c_int, [vp, vp, u64, P(vp)]),
         "catgnn_index_info": (C.c_int, [vp, P(u64), P(u64), P(u64)]),
         "catgnn_index_export": (C.c_int, [vp, vp, vp]),

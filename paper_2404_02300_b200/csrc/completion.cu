@@ -21,8 +21,14 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <filesystem>
+#include <string>
 #include <vector>
 
+#include "artifact.hpp"
 #include "index.hpp"
 #include "shard.hpp"
 
@@ -149,6 +155,29 @@ T* dev(catgnn_ctx ctx, const char* name, size_t n) {
   return ctx->scratch_buf<T>(name, std::max<size_t>(n, 1));
 }
 
+// add_reverse expansion of one streamed chunk (EdgeReader::next,
+// edge_stream.cpp:138-148): record k -> (u, v) and, when u != v, (v, u), at
+// the output position given by the exclusive scan of the per-record counts.
+__global__ void expand_count_kernel(const uint64_t* __restrict__ rec, uint64_t n, uint32_t* cnt) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    cnt[k] = rec[2 * k] != rec[2 * k + 1] ? 2u : 1u;
+}
+__global__ void expand_scatter_kernel(const uint64_t* __restrict__ rec, uint64_t n, const uint64_t* __restrict__ off,
+                                      uint64_t* __restrict__ out) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = rec[2 * k], v = rec[2 * k + 1], o = off[k];
+    out[2 * o] = u;
+    out[2 * o + 1] = v;
+    if (u != v) {
+      out[2 * o + 2] = v;
+      out[2 * o + 3] = u;
+    }
+  }
+}
+struct Count32To64 {
+  __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+};
+
 // The per-partition work on node ids 0..n-1 (dense ids, or the ascending-ext
 // "runs" of a graph index): d_e routes and keys, d_ext is the original record
 // for the output, id_to_ext (ascending in id) maps node-table ids back.
@@ -253,40 +282,139 @@ void complete_core(catgnn_ctx ctx, const uint64_t* d_e, const uint64_t* d_ext, u
 
 using namespace catgnn;
 
+namespace {
+
+void check_completion_args(const uint32_t* home, uint64_t num_nodes, uint32_t p, uint32_t hops) {
+  if (hops < 1 || hops > 3) throw ConfigError("hop count must be in {1,2,3}");                 // :133
+  if (p == 0) throw DataError("home map does not cover the node set");                         // :65-66
+  if (p > 64) throw ConfigError("device completion supports at most 64 partitions");           // :147-148
+  if (num_nodes >= (1ull << 32)) throw ConfigError("node ids must fit 32 bits");
+  for (uint64_t v = 0; v < num_nodes; ++v)
+    if (home[v] >= p) throw DataError("home partition out of range");                         // :67-68
+}
+
+// d_e (m records, dense ids) is on the device: upload the home map and roles,
+// check the endpoints, run the per-partition completion, release the scratch.
+catgnn_completion_s* complete_dense(catgnn_ctx ctx, uint64_t* d_e, uint64_t m, const uint32_t* home,
+                                    const uint8_t* roles, uint64_t n, uint32_t p, uint32_t hops) {
+  cudaStream_t st = ctx->stream;
+  uint32_t* d_home = dev<uint32_t>(ctx, "cmp_home", n);
+  uint8_t* d_roles = roles ? dev<uint8_t>(ctx, "cmp_roles", n) : nullptr;
+  if (n) CG_CUDA(cudaMemcpyAsync(d_home, home, n * 4, cudaMemcpyHostToDevice, st));
+  if (roles && n) CG_CUDA(cudaMemcpyAsync(d_roles, roles, n, cudaMemcpyHostToDevice, st));
+  int* bad = dev<int>(ctx, "cmp_bad", 1);
+  CG_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  if (m) check_edges_kernel<<<grid_of(2 * m), 256, 0, st>>>(d_e, 2 * m, n, bad);
+  int h_bad = 0;
+  CG_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) throw DataError("edge endpoint outside the node set (external ids must be dense)");
+  auto res = std::make_unique<catgnn_completion_s>();
+  complete_core(ctx, d_e, d_e, m, d_home, d_roles, n, nullptr, p, hops, res.get());
+  // the completion scratch is sized by the stream: give it back
+  for (auto it = ctx->scratch.begin(); it != ctx->scratch.end();)
+    it = it->first.rfind("cmp_", 0) == 0 ? ctx->scratch.erase(it) : std::next(it);
+  return res.release();
+}
+
+}  // namespace
+
 int catgnn_complete_edges(catgnn_ctx ctx, const uint64_t* edges, uint64_t num_edges, const uint32_t* home,
                           const uint8_t* roles, uint64_t num_nodes, uint32_t p, uint32_t hops,
                           catgnn_completion* out) {
   return guarded([&] {
     if (!ctx || !out || (num_edges && !edges) || (num_nodes && !home)) throw ConfigError("null argument");
-    if (hops < 1 || hops > 3) throw ConfigError("hop count must be in {1,2,3}");                 // :133
-    if (p == 0) throw DataError("home map does not cover the node set");                         // :65-66
-    if (p > 64) throw ConfigError("device completion supports at most 64 partitions");           // :147-148
-    if (num_nodes >= (1ull << 32)) throw ConfigError("node ids must fit 32 bits");
-    for (uint64_t v = 0; v < num_nodes; ++v)
-      if (home[v] >= p) throw DataError("home partition out of range");                         // :67-68
+    check_completion_args(home, num_nodes, p, hops);
     CG_CUDA(cudaSetDevice(ctx->device));
-    cudaStream_t st = ctx->stream;
-    const uint64_t m = num_edges, n = num_nodes;
+    const uint64_t m = num_edges;
     uint64_t* d_e = dev<uint64_t>(ctx, "cmp_edges", 2 * m);
-    uint32_t* d_home = dev<uint32_t>(ctx, "cmp_home", n);
-    uint8_t* d_roles = roles ? dev<uint8_t>(ctx, "cmp_roles", n) : nullptr;
-    if (m) CG_CUDA(cudaMemcpyAsync(d_e, edges, 2 * m * 8, cudaMemcpyHostToDevice, st));
-    if (n) CG_CUDA(cudaMemcpyAsync(d_home, home, n * 4, cudaMemcpyHostToDevice, st));
-    if (roles && n) CG_CUDA(cudaMemcpyAsync(d_roles, roles, n, cudaMemcpyHostToDevice, st));
-    int* bad = dev<int>(ctx, "cmp_bad", 1);
-    CG_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-    if (m) check_edges_kernel<<<grid_of(2 * m), 256, 0, st>>>(d_e, 2 * m, n, bad);
-    int h_bad = 0;
-    CG_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
-    CG_CUDA(cudaStreamSynchronize(st));
-    if (h_bad) throw DataError("edge endpoint outside the node set (external ids must be dense)");
+    if (m) CG_CUDA(cudaMemcpyAsync(d_e, edges, 2 * m * 8, cudaMemcpyHostToDevice, ctx->stream));
+    *out = complete_dense(ctx, d_e, m, home, roles, num_nodes, p, hops);
+  });
+}
 
-    auto res = std::make_unique<catgnn_completion_s>();
-    complete_core(ctx, d_e, d_e, m, d_home, d_roles, n, nullptr, p, hops, res.get());
-    // the completion scratch is sized by the stream: give it back
-    for (auto it = ctx->scratch.begin(); it != ctx->scratch.end();)
-      it = it->first.rfind("cmp_", 0) == 0 ? ctx->scratch.erase(it) : std::next(it);
-    *out = res.release();
+// complete_edges over an EDG1 edge file streamed in chunks (SURVEY §8(f) row 1:
+// the papers100M-scale stream, 1.6 B records / 26 GB, never sits in host RAM —
+// only a pinned chunk does — and the reference's per-partition unordered_set is
+// replaced by the device sort).  add_reverse expands each record on the device.
+// Chunk size: CATGNN_STREAM_CHUNK records (default 4 M = 64 MB).
+int catgnn_complete_edges_file(catgnn_ctx ctx, const char* path, int add_reverse, const uint32_t* home,
+                               const uint8_t* roles, uint64_t num_nodes, uint32_t p, uint32_t hops,
+                               catgnn_completion* out) {
+  return guarded([&] {
+    if (!ctx || !out || !path || (num_nodes && !home)) throw ConfigError("null argument");
+    check_completion_args(home, num_nodes, p, hops);
+    CG_CUDA(cudaSetDevice(ctx->device));
+    namespace fs = std::filesystem;
+    if (fs::path(path).extension() != ".bin") {  // text streams: host read, then the same path
+      std::vector<uint64_t> e;
+      read_edge_stream(path, add_reverse != 0, e);
+      const uint64_t m = e.size() / 2;
+      uint64_t* d_e = dev<uint64_t>(ctx, "cmp_edges", 2 * m);
+      if (m) CG_CUDA(cudaMemcpyAsync(d_e, e.data(), 2 * m * 8, cudaMemcpyHostToDevice, ctx->stream));
+      *out = complete_dense(ctx, d_e, m, home, roles, num_nodes, p, hops);
+      return;
+    }
+    std::error_code ec;
+    if (!fs::is_regular_file(path, ec)) throw DataError(std::string("edge file not readable: ") + path);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw DataError(std::string("cannot open edge file: ") + path);
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    const uint64_t size = fs::file_size(path);
+    char magic[4] = {0, 0, 0, 0};
+    uint64_t off = 0;
+    if (size >= 4 && std::fread(magic, 1, 4, f) == 4 && std::memcmp(magic, "EDG1", 4) == 0) off = 4;
+    std::fseek(f, (long)off, SEEK_SET);
+    if ((size - off) % 16 != 0) throw DataError(std::string("binary edge file has truncated record: ") + path);
+    const uint64_t records = (size - off) / 16;
+    const uint64_t cap = add_reverse ? 2 * records : records;  // expanded records, upper bound
+    uint64_t* d_e = dev<uint64_t>(ctx, "cmp_edges", 2 * cap);
+    static const uint64_t chunk = [] {
+      const char* v = std::getenv("CATGNN_STREAM_CHUNK");
+      return (uint64_t)(v && *v ? std::max(1LL, std::atoll(v)) : (4LL << 20));
+    }();
+    cudaStream_t st = ctx->stream;
+    uint64_t* pinned = nullptr;
+    CG_CUDA(cudaMallocHost(&pinned, std::max<uint64_t>(1, std::min(chunk, records)) * 16));
+    struct Pinned {
+      uint64_t* p;
+      ~Pinned() { cudaFreeHost(p); }
+    } pin{pinned};
+    uint64_t* d_raw = add_reverse ? dev<uint64_t>(ctx, "cmp_raw", 2 * std::min(chunk, records)) : nullptr;
+    uint32_t* d_cnt = add_reverse ? dev<uint32_t>(ctx, "cmp_cnt", std::min(chunk, records)) : nullptr;
+    uint64_t* d_off = add_reverse ? dev<uint64_t>(ctx, "cmp_off", std::min(chunk, records) + 1) : nullptr;
+    Temp tmp{ctx};
+    uint64_t m = 0;  // expanded records so far
+    for (uint64_t done = 0; done < records;) {
+      const uint64_t n = std::min(chunk, records - done);
+      if (std::fread(pinned, 16, n, f) != n) throw DataError(std::string("short edge read: ") + path);
+      if (!add_reverse) {
+        CG_CUDA(cudaMemcpyAsync(d_e + 2 * m, pinned, n * 16, cudaMemcpyHostToDevice, st));
+        m += n;
+      } else {
+        CG_CUDA(cudaMemcpyAsync(d_raw, pinned, n * 16, cudaMemcpyHostToDevice, st));
+        expand_count_kernel<<<grid_of(n), 256, 0, st>>>(d_raw, n, d_cnt);
+        cub::TransformInputIterator<uint64_t, Count32To64, const uint32_t*> cnt64(d_cnt, Count32To64{});
+        size_t tb = 0;
+        CG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt64, d_off, n + 0, st));
+        CG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(tb), tb, cnt64, d_off, n, st));
+        expand_scatter_kernel<<<grid_of(n), 256, 0, st>>>(d_raw, n, d_off, d_e + 2 * m);
+        CG_CHECK_LAUNCH();
+        ctx->launches += 2;
+        uint64_t last_off = 0;
+        uint32_t last_cnt = 0;
+        CG_CUDA(cudaMemcpyAsync(&last_off, d_off + n - 1, 8, cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaMemcpyAsync(&last_cnt, d_cnt + n - 1, 4, cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaStreamSynchronize(st));
+        m += last_off + last_cnt;
+      }
+      CG_CUDA(cudaStreamSynchronize(st));  // the pinned chunk is refilled next
+      done += n;
+    }
+    *out = complete_dense(ctx, d_e, m, home, roles, num_nodes, p, hops);
   });
 }
 

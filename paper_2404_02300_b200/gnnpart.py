@@ -340,6 +340,36 @@ def compute_degrees(edges, ctx: Optional[Context] = None) -> GraphIndex:
     return GraphIndex(h, ctx)
 
 
+def complete_edges_file(path: str, home, roles=None, partitions: Optional[int] = None, hops: int = 1,
+                        add_reverse: bool = False, ctx: Optional[Context] = None) -> List[GraphPartition]:
+    """complete_edges over an edge file (EDG1 streamed in chunks; dense ids)."""
+    ctx = ctx or default_context()
+    h = np.ascontiguousarray(home, np.uint32)
+    r = None if roles is None else np.ascontiguousarray(roles, np.uint8)
+    p = int(partitions if partitions is not None else (int(h.max()) + 1 if h.size else 0))
+    c = C.c_void_p()
+    check(lib.catgnn_complete_edges_file(ctx.handle, str(path).encode(), int(add_reverse), _ptr(h), _ptr(r),
+                                         h.size, p, hops, C.byref(c)))
+    return _completion_parts(c, p)
+
+
+def _completion_parts(c, p) -> List[GraphPartition]:
+    try:
+        out = []
+        for s in range(p):
+            ne, nn = C.c_uint64(), C.c_uint64()
+            check(lib.catgnn_completion_part_counts(c, s, C.byref(ne), C.byref(nn), None))
+            pe = np.zeros((ne.value, 2), np.uint64)
+            ext = np.zeros(nn.value, np.uint64)
+            own = np.zeros(nn.value, np.uint8)
+            rl = np.zeros(nn.value, np.uint8)
+            check(lib.catgnn_completion_part(c, s, _ptr(pe), _ptr(ext), _ptr(own), _ptr(rl)))
+            out.append(GraphPartition(pe, ext, own, rl))
+        return out
+    finally:
+        lib.catgnn_completion_destroy(c)
+
+
 def complete_edges(edges, home, roles=None, partitions: Optional[int] = None, hops: int = 1,
                    ctx: Optional[Context] = None, index: Optional[GraphIndex] = None) -> List[GraphPartition]:
     """complete_edges (completion.cpp:130-171) on the device.  Without `index`

@@ -128,3 +128,32 @@ def test_indexed_completion_matches_reference(tmp_path, p, hops):
         assert np.array_equal(parts[s].ext, ext), s
         assert np.array_equal(parts[s].owner, own), s
         assert np.array_equal(parts[s].role, role), s
+
+
+@pytest.mark.parametrize("p,hops,add_reverse", [(4, 1, False), (3, 2, True), (2, 1, True)])
+def test_streamed_file_completion_matches_in_memory(tmp_path, p, hops, add_reverse):
+    """catgnn_complete_edges_file (EDG1 streamed through a pinned chunk, add_reverse
+    expanded on the device) equals the in-memory path on the reference reader's
+    stream (duplicates, reversed records, self-loops; 7-record chunks)."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    os.environ["CATGNN_STREAM_CHUNK"] = "7"
+    ds = dup_stream(tmp_path, 10, 3000, 11 + p)
+    e = ds["edges"].copy()
+    e[:40, 1] = e[:40, 0]  # self-loops (add_reverse keeps them single)
+    path = os.path.join(str(tmp_path), "loops.bin")
+    _write_edg1(path, e)
+    rng = np.random.default_rng(p)
+    home = rng.integers(0, p, ds["n"]).astype(np.uint32)
+    want_stream = e if not add_reverse else np.concatenate(
+        [np.stack([r, r[::-1]]) if r[0] != r[1] else r[None] for r in e]).reshape(-1, 2)
+    want = gp.complete_edges(want_stream, home, ds["roles"], p, hops)
+    got = gp.complete_edges_file(path, home, ds["roles"], p, hops, add_reverse=add_reverse)
+    for a, b in zip(want, got):
+        assert np.array_equal(a.edges, b.edges) and np.array_equal(a.ext, b.ext)
+        assert np.array_equal(a.owner, b.owner) and np.array_equal(a.role, b.role)
+
+
+def _write_edg1(path, e):
+    with open(path, "wb") as f:
+        f.write(b"EDG1")
+        f.write(np.ascontiguousarray(e, np.uint64).tobytes())
