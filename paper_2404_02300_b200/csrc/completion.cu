@@ -19,6 +19,8 @@
 // order.  Node presence is a byte map over the node ids.  All integer work:
 // HBM-bound sorts and compactions, no tensor cores.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -216,7 +218,7 @@ void complete_core(catgnn_ctx ctx, const uint64_t* d_e, const uint64_t* d_ext, u
     CG_CUDA(cudaStreamSynchronize(st));
     return c;
   };
-  cub::CountingInputIterator<uint64_t> pos(0);
+  thrust::counting_iterator<uint64_t> pos(0);
   const int key_bits = 64;
   for (uint32_t s = 0; s < p; ++s) {
     auto& P = res->parts[s];
@@ -397,7 +399,7 @@ int catgnn_complete_edges_file(catgnn_ctx ctx, const char* path, int add_reverse
       } else {
         CG_CUDA(cudaMemcpyAsync(d_raw, pinned, n * 16, cudaMemcpyHostToDevice, st));
         expand_count_kernel<<<grid_of(n), 256, 0, st>>>(d_raw, n, d_cnt);
-        cub::TransformInputIterator<uint64_t, Count32To64, const uint32_t*> cnt64(d_cnt, Count32To64{});
+        auto cnt64 = thrust::make_transform_iterator(d_cnt, Count32To64{});
         size_t tb = 0;
         CG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt64, d_off, n + 0, st));
         CG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(tb), tb, cnt64, d_off, n, st));

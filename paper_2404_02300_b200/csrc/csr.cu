@@ -11,6 +11,8 @@
 // offsets are a degree histogram + scan.  Everything is int32 column indices
 // and int64 offsets (train.hpp:19's u32 offsets overflow at papers scale).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -184,7 +186,7 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
   // offsets: row_ptr[0] = 0, row_ptr[1..] = inclusive scan of deg
   CG_CUDA(cudaMemsetAsync(s->row_ptr.p, 0, sizeof(int64_t), st));
   {
-    cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(deg, ToI64());
+    auto it = thrust::make_transform_iterator(deg, ToI64());
     size_t tmp_bytes = 0;
     CG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, it, s->row_ptr.p + 1, (int)rows, st));
     void* tmp = ctx->scratch_buf<unsigned char>("k1_cub", tmp_bytes);

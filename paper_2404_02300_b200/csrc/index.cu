@@ -12,6 +12,8 @@
 // table (binary search) that catgnn_complete_edges_indexed uses to route
 // arbitrary 64-bit ids.  Integer, HBM/sort-bound work.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <memory>
@@ -123,7 +125,7 @@ void build_index(catgnn_ctx ctx, const uint64_t* d_edges, uint64_t m, catgnn_ind
   CG_CUDA(cub::DeviceSelect::Flagged(buf("idx_cub", tb), tb, sv, flag, runs_first, count, n2, st));
   // degree = run length: positions of the run starts, differenced
   uint64_t* starts = reinterpret_cast<uint64_t*>(buf("idx_starts", (n2 + 1) * 8));
-  cub::CountingInputIterator<uint64_t> it(0);
+  thrust::counting_iterator<uint64_t> it(0);
   tb = 0;
   CG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, flag, starts, count, n2, st));
   CG_CUDA(cub::DeviceSelect::Flagged(buf("idx_cub", tb), tb, it, flag, starts, count, n2, st));
