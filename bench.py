@@ -144,7 +144,10 @@ def reference_jobs(prep, samples, budget_edges):
             local = np.searchsorted(ext, edges.ravel()).astype(np.uint32).reshape(-1, 2)
             csr[i] = (ext.size,) + tuple(ref.build_adjacency(ext.size, local))
         rows, off, nb = csr[i]
-        R0 = min(int(np.searchsorted(off, blk * budget_edges)), rows)
+        # block indices past a small partition's edges wrap around (every
+        # sample is a non-empty row range of the partition)
+        blk %= max(1, -(-int(off[rows]) // budget_edges))
+        R0 = min(int(np.searchsorted(off, blk * budget_edges)), max(rows - 1, 0))
         R1 = max(R0 + 1, min(int(np.searchsorted(off, (blk + 1) * budget_edges)), rows))
         off_s = np.clip(off, off[R0], off[R1]) - off[R0]
         jobs.append((rows, off_s, nb[off[R0]: off[R1]].copy(), int(off[R1] - off[R0])))
