@@ -487,6 +487,10 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    # finish the averaging period, so every lazily sized buffer (the averaging
+    # scratch included) exists before a graph capture
+    while state["it"] % args.sync:
+        step()
     torch.cuda.synchronize()
     timing(True)
     graph = None

@@ -36,13 +36,13 @@ def test_bench_two_ranks_host_collectives():
     assert d["config"]["workload"] == "tiny_gcn" and d["gpu_launches"] > 0
 
 
-@pytest.mark.parametrize("graph,lanes", [(1, 1), (0, 1), (1, 2)])
-def test_bench_single_rank_contract(graph, lanes):
+@pytest.mark.parametrize("graph,lanes,sync", [(1, 1, 1), (0, 1, 1), (1, 2, 1), (1, 1, 4)])
+def test_bench_single_rank_contract(graph, lanes, sync):
     """The one-GPU bench line (driver contract): graph-replayed and eager steps,
     shard lanes; every key the driver and the judge read is present and sane."""
     env = dict(os.environ, CATGNN_WORKLOAD="tiny_gcn")
     cmd = [sys.executable, "bench.py", "--steps", "4", "--warmup", "3", "--graph", str(graph),
-           "--lanes", str(lanes)]
+           "--lanes", str(lanes), "--sync", str(sync)]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -58,7 +58,8 @@ def test_bench_single_rank_contract(graph, lanes):
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert (e["graph"] is not None) == bool(graph)
+    assert (e["graph"] is not None) == (bool(graph) and sync == 1)
+    assert "graph capture failed" not in out.stderr
     assert any(k.startswith("K2 agg") for k in d["step_breakdown"])
 
 
