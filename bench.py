@@ -212,7 +212,7 @@ def run_reference(args, w, prep):
 
 def workload_config(w, prep, args):
     m = prep["meta"]
-    return {"workload": w.name, "model": f"{w.layers}-layer {w.model.upper()} hidden {w.hidden}",
+    return {"workload": w.name, "gnn": f"{w.layers}-layer {w.model.upper()} hidden {w.hidden}",
             "graph": f"RMAT scale {w.scale}, {w.edges} undirected edges ({m['nnz']} nnz), |V|={m['num_nodes']}",
             "feature_dim": w.dim, "classes": w.classes, "partitions": w.partitions,
             "partitioner": f"reference SPRING beta={w.beta} tau_vol={m['tau_vol']} + 1-hop completion",
@@ -220,7 +220,8 @@ def workload_config(w, prep, args):
             "aggregation_widths": w.passes(),
             "aggregation_row_stride_floats": [act_width(x) for x in w.passes()], "sync_interval": args.sync,
             "optimizer": "adam lr 0.01", "gemm_precision": "3xTF32 (tcgen05 kind::tf32)",
-            "global_batch": "full-batch per partition", "parallelism": f"partition-parallel p={w.partitions}",
+            "step": "one full-batch local iteration per partition + averaging",
+            "partitions_per_gpu": w.partitions // max(1, dist_env()[0]),
             "l2": "inputs larger than L2 (per-partition features 0.5 GB, activations > 126 MB)"}
 
 
