@@ -257,6 +257,9 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
     for (int i = 0; i < nr; ++i) {
       const int64_t r = rb + i;
       const int64_t e0 = __shfl_sync(0xffffffffu, rpa, i), e1 = __shfl_sync(0xffffffffu, rpb, i);
+#ifdef AGG_SKIP_SHORT  // diagnostics build: the cost of short rows (wrong results)
+      if (e1 - e0 < AGG_SKIP_SHORT) continue;
+#endif
       float4 selfv[VPL];
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
