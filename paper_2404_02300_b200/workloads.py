@@ -78,6 +78,10 @@ WORKLOADS = {
     # classes, papers' ~14.5 records per node and 1%/0.1%/0.2% roles), 2^24 ids, 220M records, p=8
     "papers_gin_s24": Workload("papers_gin_s24", "gin", 2, 256, 24, 220_000_000, 128, 172, 8,
                                (0.01, 0.001, 0.002), seed=4),
+    # configs[4]: the partition-count half of the k x s sweep on the reddit-shaped graph
+    # (k = 8 is reddit_gcn; s is bench.py --sync)
+    "reddit_gcn_p2": Workload("reddit_gcn_p2", "gcn", 2, 256, 18, 57_307_946, 602, 41, 2, (0.66, 0.10, 0.24)),
+    "reddit_gcn_p4": Workload("reddit_gcn_p4", "gcn", 2, 256, 18, 57_307_946, 602, 41, 4, (0.66, 0.10, 0.24)),
     # small smoke workload
     "tiny_gcn": Workload("tiny_gcn", "gcn", 2, 64, 12, 40_000, 32, 8, 4, (0.6, 0.2, 0.2), seed=3),
 }
