@@ -526,7 +526,11 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
   if (a.width % 4 || a.in_ld % 4 || a.out_ld % 4 || a.in_col % 4 || a.out_col % 4 ||
       (a.residual && (a.res_ld % 4 || a.res_col % 4)))
     throw ConfigError("aggregation widths/strides must be multiples of 4 floats");
-  if (a.in == a.out && a.in) throw ConfigError("aggregation cannot run in place");
+  // one buffer may be both input and output when the column ranges are disjoint
+  // (SAGE: mean(h) into the right half of [h | mean])
+  if (a.in == a.out && a.in && a.in_ld == a.out_ld && a.in_col < a.out_col + a.width && a.out_col < a.in_col + a.width)
+    throw ConfigError("aggregation cannot run in place");
+  if (a.in == a.out && a.in && a.in_ld != a.out_ld) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
   const uint32_t W4 = a.width / 4;
   for (uint32_t c4 = 0; c4 < W4; c4 += kMaxSlab4) {

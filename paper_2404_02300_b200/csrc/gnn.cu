@@ -49,6 +49,7 @@ struct Layer {
   uint32_t K_in = 0;    // round4(d_in): activation row stride of the input
   uint32_t D_out = 0;   // round4(d_out)
   uint32_t ld_act = 0;  // row stride of this layer's output activations (>= D_out)
+  bool out_in_next_mid = false;  // output written straight into the next (SAGE aggregate-first) layer's [h | mean]
   bool agg_first = false;
   // internal weight matrix (GEMM B operand): w_rows x w_cols
   uint32_t w_rows = 0, w_cols = 0;
@@ -324,6 +325,10 @@ const uint32_t kPadNarrow = [] {
   return v ? (uint32_t)std::atoi(v) : 16u;
 }();
 uint32_t act_width(uint32_t d) { return d < 128 ? round_up(d, kPadNarrow) : round_up(d, 4); }
+const bool kSageInPlace = [] {  // A/B knob (CATGNN_SAGE_INPLACE=0: copy h into [h | mean])
+  const char* v = std::getenv("CATGNN_SAGE_INPLACE");
+  return v ? v[0] != '0' : true;
+}();
 const bool kNarrowLd64 = [] {  // A/B knob; measured no faster on reddit (off)
   const char* v = std::getenv("CATGNN_NARROW_LD64");
   return v ? v[0] != '0' : false;
@@ -368,6 +373,13 @@ void plan_layers(catgnn_model_s* M) {
     M->layers.push_back(L);
   }
   M->n_params = off;
+  // A hidden layer followed by a SAGE aggregate-first layer writes its output
+  // straight into that layer's [h | mean] buffer (left half): no row copy.
+  for (size_t l = 0; l + 1 < M->layers.size(); ++l) {
+    const Layer& N = M->layers[l + 1];
+    M->layers[l].out_in_next_mid = c.kind == CATGNN_MODEL_SAGE && N.agg_first && N.K_in == M->layers[l].D_out &&
+                                   kSageInPlace;
+  }
 }
 
 // logical (row, col) of layer L -> internal index
@@ -455,8 +467,13 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
     Bufs& b = B[l];
     b.in = in;
     b.in_ld = in_ld;
-    b.out_ld = L.ld_act;
-    b.out = act(ctx, nm("H", l), rows, b.out_ld, fresh);
+    if (L.out_in_next_mid) {  // the next layer's [h | mean], left half
+      b.out_ld = 2 * M->layers[l + 1].K_in;
+      b.out = act(ctx, nm("mid", l + 1), rows, b.out_ld, fresh);
+    } else {
+      b.out_ld = L.ld_act;
+      b.out = act(ctx, nm("H", l), rows, b.out_ld, fresh);
+    }
     if (!last) {
       b.bits_words = (L.D_out + 31) / 32;
       b.bits = act_bits(ctx, nm("Hbits", l), rows, b.bits_words);
@@ -464,8 +481,9 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
     const float* bias = M->params.p + L.off_b;
     if (sage && L.agg_first) {
       b.mid_ld = 2 * L.K_in;
-      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
-      copy_rows(ctx, in, in_ld, b.mid, b.mid_ld, rows, L.K_in);
+      const bool inplace = l > 0 && M->layers[l - 1].out_in_next_mid;  // h already in the left half
+      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh && !inplace);
+      if (!inplace) copy_rows(ctx, in, in_ld, b.mid, b.mid_ld, rows, L.K_in);
       AggArgs a;
       a.in = in; a.in_ld = in_ld; a.out = b.mid; a.out_ld = b.mid_ld; a.out_col = L.K_in;
       a.width = L.K_in; a.norm = kNormMean;
@@ -878,7 +896,13 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
     const Layer& L = m->layers[layer];
     const float* src = nullptr;
     uint32_t ld = 0, w = L.d_out;
-    if (what == 0) { src = m->ctx->scratch_buf<float>(nm("H", layer), 1); ld = L.ld_act; }
+    if (what == 0 && L.out_in_next_mid) {
+      src = m->ctx->scratch_buf<float>(nm("mid", layer + 1), 1);
+      ld = 2 * m->layers[layer + 1].K_in;
+    } else if (what == 0) {
+      src = m->ctx->scratch_buf<float>(nm("H", layer), 1);
+      ld = L.ld_act;
+    }
     else if (what == 2) { src = m->ctx->scratch_buf<float>(nm("dZ", layer), 1); ld = L.ld_act; }
     else throw ConfigError("export: what must be 0 (H) or 2 (dZ)");
     if (width) *width = w;
