@@ -1,0 +1,45 @@
+"""Full-size parity for the bench workload (BASELINE configs[1], reddit-shaped GCN):
+one forward + backward of the 2-layer GCN on a whole SPRING partition (184 k rows,
+26 M nnz, 602-d) against the float64 oracle (oracle/gnn_oracle.py) — the north
+star's single-step tolerance (2e-3 relative, normwise) at the size bench.py times.
+The CSR the GPU builds is checked bit-exact against the reference's build_adjacency
+on the same partition first."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import gnn_oracle as go
+from oracle import ref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def test_reddit_partition_one_step_matches_oracle():
+    from paper_2404_02300_b200 import gnnpart as gp, workloads as W
+    from paper_2404_02300_b200.gnn import GNNModel
+    w = W.WORKLOADS["reddit_gcn"]
+    prep = W.prepare(w, lambda *a: None)
+    p = W.load_part(prep, 0)
+    ctx = gp.Context(0)
+    s = gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx)
+    rows = p["ext"].size
+    local = np.searchsorted(p["ext"], p["edges"].ravel()).astype(np.uint32).reshape(-1, 2)
+    off, nb = ref.build_adjacency(rows, local)
+    adj = s.adjacency()
+    assert np.array_equal(adj.offsets, off.astype(np.uint64)) and np.array_equal(adj.neighbors, nb)
+    train = np.nonzero((p["owner"] == 1) & (p["role"] == 1))[0].astype(np.int64)
+    m = GNNModel("gcn", 2, w.dim, w.hidden, w.classes, seed=5, ctx=ctx)
+    loss = m.forward_backward(s)
+    init = go.init_params(go.GCN, 2, w.dim, w.hidden, w.classes, seed=5)
+    o = go.OracleShard(go.Graph.from_csr(off, nb, rows), p["features"].astype(np.float64),
+                       p["labels"].astype(np.int64), train)
+    rep = go.Replica(go.GCN, go.unflatten(m.get_params().astype(np.float64), init))
+    loss_ref, H, _, grads = rep.forward_backward(o)
+    errs = {"loss": abs(loss - loss_ref) / abs(loss_ref)}
+    for l in range(2):
+        errs[f"H{l}"] = rel_err(m.export(l, 0, rows), H[l + 1])
+    for l, ((gW, gb), (rW, rb)) in enumerate(zip(m.unflatten(m.get_grads()), grads)):
+        errs[f"dW{l}"], errs[f"db{l}"] = rel_err(gW, rW), rel_err(gb, rb)
+    print("full-size relative errors:", {k: f"{v:.2e}" for k, v in errs.items()})
+    assert errs["loss"] <= 1e-3, errs
+    assert all(v < 2e-3 for k, v in errs.items() if k != "loss"), errs
