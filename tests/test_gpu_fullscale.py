@@ -1,6 +1,7 @@
-"""Full-size parity for the bench workload (BASELINE configs[1], reddit-shaped GCN):
-one forward + backward of the 2-layer GCN on a whole SPRING partition (184 k rows,
-26 M nnz, 602-d) against the float64 oracle (oracle/gnn_oracle.py) — the north
+"""Full-size parity for the bench workloads (BASELINE configs[1] reddit-shaped GCN,
+configs[2] products-shaped 3-layer SAGE): one forward + backward on a whole SPRING
+partition (reddit: 184 k rows, 26 M nnz, 602-d) against the float64 oracle
+(oracle/gnn_oracle.py) — the north
 star's single-step tolerance (2e-3 relative, normwise) at the size bench.py times.
 The CSR the GPU builds is checked bit-exact against the reference's build_adjacency
 on the same partition first."""
@@ -14,10 +15,12 @@ from oracle import ref
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def test_reddit_partition_one_step_matches_oracle():
+@pytest.mark.parametrize("workload", ["reddit_gcn", "products_sage"])
+def test_partition_one_step_matches_oracle(workload):
     from paper_2404_02300_b200 import gnnpart as gp, workloads as W
     from paper_2404_02300_b200.gnn import GNNModel
-    w = W.WORKLOADS["reddit_gcn"]
+    w = W.WORKLOADS[workload]
+    kind = {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[w.model]
     prep = W.prepare(w, lambda *a: None)
     p = W.load_part(prep, 0)
     ctx = gp.Context(0)
@@ -28,15 +31,15 @@ def test_reddit_partition_one_step_matches_oracle():
     adj = s.adjacency()
     assert np.array_equal(adj.offsets, off.astype(np.uint64)) and np.array_equal(adj.neighbors, nb)
     train = np.nonzero((p["owner"] == 1) & (p["role"] == 1))[0].astype(np.int64)
-    m = GNNModel("gcn", 2, w.dim, w.hidden, w.classes, seed=5, ctx=ctx)
+    m = GNNModel(w.model, w.layers, w.dim, w.hidden, w.classes, seed=5, ctx=ctx)
     loss = m.forward_backward(s)
-    init = go.init_params(go.GCN, 2, w.dim, w.hidden, w.classes, seed=5)
+    init = go.init_params(kind, w.layers, w.dim, w.hidden, w.classes, seed=5)
     o = go.OracleShard(go.Graph.from_csr(off, nb, rows), p["features"].astype(np.float64),
                        p["labels"].astype(np.int64), train)
-    rep = go.Replica(go.GCN, go.unflatten(m.get_params().astype(np.float64), init))
+    rep = go.Replica(kind, go.unflatten(m.get_params().astype(np.float64), init))
     loss_ref, H, _, grads = rep.forward_backward(o)
     errs = {"loss": abs(loss - loss_ref) / abs(loss_ref)}
-    for l in range(2):
+    for l in range(w.layers):
         errs[f"H{l}"] = rel_err(m.export(l, 0, rows), H[l + 1])
     for l, ((gW, gb), (rW, rb)) in enumerate(zip(m.unflatten(m.get_grads()), grads)):
         errs[f"dW{l}"], errs[f"db{l}"] = rel_err(gW, rW), rel_err(gb, rb)
