@@ -1,0 +1,140 @@
+"""North-star acceptance at the bench's full size (BASELINE configs[1]): 10 epochs of
+the 2-layer GCN over all 8 reddit-shaped SPRING partitions (s = 1, Adam 0.01) on the
+B200, against the float64 oracle (oracle/gnn_oracle.py) run on the host cores — the
+per-epoch loss within 1e-3 relative and the final test accuracy on the global graph
+within 0.5 pt.  The oracle's 8 replicas run in 8 worker processes (one partition
+each; the averaging is done in partition order in the parent, as the reference's
+model_average).  Output: one JSON line (gpurun_out/fullscale_ten_epochs.json).
+
+    python scripts/fullscale_ten_epochs.py [EPOCHS]
+"""
+import json
+import multiprocessing as mp
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+EPOCHS = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+SEED, HIDDEN, LR = 7, 256, 0.01
+
+
+def oracle_shard(prep, i):
+    from oracle import gnn_oracle as go, ref
+    from paper_2404_02300_b200 import workloads as W
+    p = W.load_part(prep, i)
+    rows = p["ext"].size
+    local = np.searchsorted(p["ext"], p["edges"].ravel()).astype(np.uint32).reshape(-1, 2)
+    off, nb = ref.build_adjacency(rows, local)
+    train = np.nonzero((p["owner"] == 1) & (p["role"] == 1))[0].astype(np.int64)
+    return go.OracleShard(go.Graph.from_csr(off, nb, rows), p["features"].astype(np.float64),
+                          p["labels"].astype(np.int64), train)
+
+
+def worker(prep, i, init_flat, conn):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(max(1, (os.cpu_count() or 8) // 8))
+    from oracle import gnn_oracle as go
+    sh = oracle_shard(prep, i)
+    w_classes = int(prep["meta"]["classes"]) if "classes" in prep["meta"] else None
+    like = go.init_params(go.GCN, 2, sh.X.shape[1], HIDDEN, w_classes, seed=SEED)
+    rep = go.Replica(go.GCN, go.unflatten(init_flat, like), lr=LR)
+    conn.send(len(sh.train_rows))
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
+        rep.params = go.unflatten(msg, like)
+        loss = rep.step(sh)
+        conn.send((loss, go.flatten(rep.params)))
+
+
+def main():
+    from paper_2404_02300_b200 import workloads as W
+    w = W.WORKLOADS["reddit_gcn"]
+    prep = W.prepare(w, lambda *a: None)
+    prep["meta"]["classes"] = w.classes
+    t0 = time.time()
+    # ---- B200 -------------------------------------------------------------
+    from paper_2404_02300_b200 import gnn, gnnpart as gp
+    ctx = gp.Context(0)
+    X = np.load(os.path.join(prep["dir"], "features.npy"), mmap_mode="r")
+    labels = np.load(os.path.join(prep["dir"], "labels.npy"))
+    roles = np.load(os.path.join(prep["dir"], "roles.npy"))
+    shards, counts = [], []
+    for i in range(w.partitions):
+        p = W.load_part(prep, i, X, labels)
+        shards.append(gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx))
+        counts.append(int(np.sum((p["owner"] == 1) & (p["role"] == 1))))
+    res = gnn.distributed_train("gcn", shards, counts, 1, EPOCHS, 2, HIDDEN, w.classes, seed=SEED, lr=LR, ctx=ctx)
+    t_gpu = time.time() - t0
+    # global graph (the full stream, train.cpp:229-238) for the test accuracy
+    raw = np.fromfile(os.path.join(prep["dir"], "edges.bin"), dtype=np.uint8)
+    edges = raw[4:].view(np.uint64).reshape(-1, 2)
+    V = labels.size
+    test = np.nonzero(roles == 3)[0]
+    gsh = gp.Shard.from_edges(V, edges.astype(np.uint32), np.ascontiguousarray(X, np.float32), ctx)
+    m = gnn.GNNModel("gcn", 2, w.dim, HIDDEN, w.classes, seed=SEED, ctx=ctx)
+    m.set_params(res.params)
+    logits, _ = m.forward(gsh, logits=True)
+    acc_gpu = float(np.mean(np.argmax(logits[test], axis=1) == labels[test]))
+    del shards, gsh
+    # ---- float64 oracle, 8 worker processes --------------------------------
+    from oracle import gnn_oracle as go
+    like = go.init_params(go.GCN, 2, w.dim, HIDDEN, w.classes, seed=SEED)
+    init_flat = go.flatten(like)
+    t1 = time.time()
+    ctxm = mp.get_context("fork")
+    pipes, procs = [], []
+    for i in range(w.partitions):
+        a, b = ctxm.Pipe()
+        pr = ctxm.Process(target=worker, args=(prep, i, init_flat, b))
+        pr.start()
+        pipes.append(a)
+        procs.append(pr)
+    ocounts = [c.recv() for c in pipes]
+    assert ocounts == counts, (ocounts, counts)
+    alpha = go.sync_weights(ocounts)
+    shared = init_flat
+    losses = []
+    for _ in range(EPOCHS):
+        for c in pipes:
+            c.send(shared)
+        out = [c.recv() for c in pipes]
+        losses.append(sum(a * o[0] for a, o in zip(alpha, out)))
+        flat = np.zeros_like(shared)
+        for a, o in zip(alpha, out):
+            flat = flat + a * o[1]
+        shared = flat
+    for c in pipes:
+        c.send(None)
+    for pr in procs:
+        pr.join()
+    t_oracle = time.time() - t1
+    G = go.Graph.from_csr(*oracle_global_csr(edges, V), V)
+    H, Zs, _ = go.forward(go.GCN, go.unflatten(shared, like), G, np.asarray(X, np.float64), [False, False])
+    acc_oracle = float(np.mean(np.argmax(Zs[-1][test], axis=1) == labels[test]))
+    rel = [abs(a - b) / abs(b) for a, b in zip(res.losses, losses)]
+    line = {"check": "reddit_gcn 10-epoch loss and final test accuracy, B200 vs float64 oracle",
+            "epochs": EPOCHS, "partitions": w.partitions, "sync_interval": 1, "seed": SEED,
+            "loss_gpu": res.losses, "loss_oracle": losses, "max_rel_loss_err": max(rel),
+            "test_acc_gpu": acc_gpu, "test_acc_oracle": acc_oracle,
+            "acc_diff_pt": 100 * abs(acc_gpu - acc_oracle), "test_rows": int(test.size),
+            "pass": bool(max(rel) <= 1e-3 and 100 * abs(acc_gpu - acc_oracle) <= 0.5),
+            "seconds": {"gpu_incl_load": round(t_gpu, 1), "oracle_8_procs": round(t_oracle, 1)}}
+    print(json.dumps(line), flush=True)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "fullscale_ten_epochs.json"), "w") as f:
+        f.write(json.dumps(line) + "\n")
+
+
+def oracle_global_csr(edges, V):
+    from oracle import ref
+    return ref.build_adjacency(V, edges.astype(np.uint32))
+
+
+if __name__ == "__main__":
+    main()
