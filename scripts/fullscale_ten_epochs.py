@@ -6,7 +6,11 @@ within 0.5 pt.  The oracle's 8 replicas run in 8 worker processes (one partition
 each; the averaging is done in partition order in the parent, as the reference's
 model_average).  Output: one JSON line (gpurun_out/fullscale_ten_epochs.json).
 
-    python scripts/fullscale_ten_epochs.py [EPOCHS]
+    python scripts/fullscale_ten_epochs.py [EPOCHS] [WORKLOAD]   (reddit_gcn | products_sage)
+
+products_sage: eight float64 oracle workers over the 1.3 M-row partitions exceed the
+196 GB of host RAM on this pool's boxes (a worker died after 47 min); only reddit_gcn
+has been run to completion.
 """
 import json
 import multiprocessing as mp
@@ -19,6 +23,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 EPOCHS = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+WORKLOAD = sys.argv[2] if len(sys.argv) > 2 else "reddit_gcn"
 SEED, HIDDEN, LR = 7, 256, 0.01
 
 
@@ -39,9 +44,10 @@ def worker(prep, i, init_flat, conn):
     threadpool_limits(max(1, (os.cpu_count() or 8) // 8))
     from oracle import gnn_oracle as go
     sh = oracle_shard(prep, i)
-    w_classes = int(prep["meta"]["classes"]) if "classes" in prep["meta"] else None
-    like = go.init_params(go.GCN, 2, sh.X.shape[1], HIDDEN, w_classes, seed=SEED)
-    rep = go.Replica(go.GCN, go.unflatten(init_flat, like), lr=LR)
+    w = _workload()
+    kind = _kind(w)
+    like = go.init_params(kind, w.layers, sh.X.shape[1], HIDDEN, w.classes, seed=SEED)
+    rep = go.Replica(kind, go.unflatten(init_flat, like), lr=LR)
     conn.send(len(sh.train_rows))
     while True:
         msg = conn.recv()
@@ -52,11 +58,20 @@ def worker(prep, i, init_flat, conn):
         conn.send((loss, go.flatten(rep.params)))
 
 
+def _workload():
+    from paper_2404_02300_b200 import workloads as W
+    return W.WORKLOADS[WORKLOAD]
+
+
+def _kind(w):
+    from oracle import gnn_oracle as go
+    return {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[w.model]
+
+
 def main():
     from paper_2404_02300_b200 import workloads as W
-    w = W.WORKLOADS["reddit_gcn"]
+    w = _workload()
     prep = W.prepare(w, lambda *a: None)
-    prep["meta"]["classes"] = w.classes
     t0 = time.time()
     # ---- B200 -------------------------------------------------------------
     from paper_2404_02300_b200 import gnn, gnnpart as gp
@@ -69,7 +84,8 @@ def main():
         p = W.load_part(prep, i, X, labels)
         shards.append(gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx))
         counts.append(int(np.sum((p["owner"] == 1) & (p["role"] == 1))))
-    res = gnn.distributed_train("gcn", shards, counts, 1, EPOCHS, 2, HIDDEN, w.classes, seed=SEED, lr=LR, ctx=ctx)
+    res = gnn.distributed_train(w.model, shards, counts, 1, EPOCHS, w.layers, HIDDEN, w.classes, seed=SEED, lr=LR,
+                                ctx=ctx)
     t_gpu = time.time() - t0
     # global graph (the full stream, train.cpp:229-238) for the test accuracy
     raw = np.fromfile(os.path.join(prep["dir"], "edges.bin"), dtype=np.uint8)
@@ -77,14 +93,15 @@ def main():
     V = labels.size
     test = np.nonzero(roles == 3)[0]
     gsh = gp.Shard.from_edges(V, edges.astype(np.uint32), np.ascontiguousarray(X, np.float32), ctx)
-    m = gnn.GNNModel("gcn", 2, w.dim, HIDDEN, w.classes, seed=SEED, ctx=ctx)
+    m = gnn.GNNModel(w.model, w.layers, w.dim, HIDDEN, w.classes, seed=SEED, ctx=ctx)
     m.set_params(res.params)
     logits, _ = m.forward(gsh, logits=True)
     acc_gpu = float(np.mean(np.argmax(logits[test], axis=1) == labels[test]))
     del shards, gsh
     # ---- float64 oracle, 8 worker processes --------------------------------
     from oracle import gnn_oracle as go
-    like = go.init_params(go.GCN, 2, w.dim, HIDDEN, w.classes, seed=SEED)
+    kind = _kind(w)
+    like = go.init_params(kind, w.layers, w.dim, HIDDEN, w.classes, seed=SEED)
     init_flat = go.flatten(like)
     t1 = time.time()
     ctxm = mp.get_context("fork")
@@ -115,10 +132,12 @@ def main():
         pr.join()
     t_oracle = time.time() - t1
     G = go.Graph.from_csr(*oracle_global_csr(edges, V), V)
-    H, Zs, _ = go.forward(go.GCN, go.unflatten(shared, like), G, np.asarray(X, np.float64), [False, False])
+    params = go.unflatten(shared, like)
+    fl = go.Replica(kind, params).flags(w.dim)
+    H, Zs, _ = go.forward(kind, params, G, np.asarray(X, np.float64), fl)
     acc_oracle = float(np.mean(np.argmax(Zs[-1][test], axis=1) == labels[test]))
     rel = [abs(a - b) / abs(b) for a, b in zip(res.losses, losses)]
-    line = {"check": "reddit_gcn 10-epoch loss and final test accuracy, B200 vs float64 oracle",
+    line = {"check": f"{w.name} {EPOCHS}-epoch loss and final test accuracy, B200 vs float64 oracle",
             "epochs": EPOCHS, "partitions": w.partitions, "sync_interval": 1, "seed": SEED,
             "loss_gpu": res.losses, "loss_oracle": losses, "max_rel_loss_err": max(rel),
             "test_acc_gpu": acc_gpu, "test_acc_oracle": acc_oracle,
