@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <string>
 
 #include "shard.hpp"
@@ -508,14 +509,18 @@ AggFn pick_fixup(uint32_t w4) {
   }
 }
 
-int blocks_per_sm(AggFn fn) {
-  static std::map<AggFn, int> cache;
-  auto it = cache.find(fn);
+int blocks_per_sm(int device, AggFn fn) {
+  // keyed by device ordinal (the occupancy query is per device); callers on
+  // several host threads share the cache
+  static std::mutex mu;
+  static std::map<std::pair<int, AggFn>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({device, fn});
   if (it != cache.end()) return it->second;
   int b = 0;
   CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 256, 0));
   b = std::max(1, b);
-  cache[fn] = b;
+  cache[{device, fn}] = b;
   return b;
 }
 
@@ -577,7 +582,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
                                                    (a.mask_bits || a.bits_out ? " bits" : "") +
                                                    (detail ? " rows=" + std::to_string(s->rows) : std::string())
                                              : std::string());
-    const int bps = blocks_per_sm(fn);
+    const int bps = blocks_per_sm(ctx->device, fn);
     static const int sms_env = env_int("CATGNN_AGG_SMS", 0);  // A/B knob: SMs the persistent grid covers
     const uint64_t warps_needed = std::max<uint64_t>(1, s->n_units);
     const unsigned grid = (unsigned)std::max<uint64_t>(

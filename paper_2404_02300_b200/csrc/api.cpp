@@ -145,6 +145,13 @@ void set_labels(catgnn_shard_s* s, const int32_t* labels, const uint32_t* tr, ui
       if (r >= s->rows) throw DataError("role row outside the shard");
   int32_t mx = 0;
   for (int32_t l : s->h_labels) mx = std::max(mx, l);
+  s->train_label_min = 0;
+  s->train_label_max = -1;
+  for (size_t i = 0; i < s->h_train.size(); ++i) {
+    const int32_t l = s->h_labels[s->h_train[i]];
+    s->train_label_min = i ? std::min(s->train_label_min, l) : l;
+    s->train_label_max = i ? std::max(s->train_label_max, l) : l;
+  }
   s->classes = (uint32_t)std::max(1, mx + 1);
   s->labels.alloc(std::max<uint64_t>(1, s->rows));
   s->d_train.alloc(std::max<uint64_t>(1, ntr));

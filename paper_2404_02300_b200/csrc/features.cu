@@ -231,8 +231,13 @@ int catgnn_split_features(catgnn_ctx ctx, catgnn_artifact a, const char* feature
     const FeatureFile h = read_feature_header(features);
     const size_t total = h.rows * (size_t)h.dim;
     cudaStream_t st = ctx->stream;
+    // the pinned buffer is also the D2H target of every partition's rows: size
+    // it for the largest node table too (a table may repeat ids; the reference
+    // writes one row per record, store.cpp:104-112)
+    size_t max_part = 0;
+    for (const auto& t : a->parts) max_part = std::max(max_part, t.ext.size() * (size_t)h.dim);
     float* pinned = nullptr;
-    CG_CUDA(cudaMallocHost(&pinned, std::max<size_t>(1, total) * 4));
+    CG_CUDA(cudaMallocHost(&pinned, std::max<size_t>({1, total, max_part}) * 4));
     struct Pinned {
       float* p;
       ~Pinned() { cudaFreeHost(p); }

@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <array>
+#include <map>
 #include <mutex>
 
 #include "gemm.hpp"
@@ -855,13 +857,19 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   }
   CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BNh);
   CUtensorMap tbl = blt ? (b.mn_major ? make_map_mn(Blo, N, K, ldb) : make_map(Blo, N, K, ldb, BNh)) : tb;
-  static bool attr_set[2][2] = {{false, false}, {false, false}};
+  // cudaFuncSetAttribute is per device: one flag set per device ordinal
+  static std::mutex attr_mu;
+  static std::map<int, std::array<bool, 4>> attr_set;
   auto kern = pair ? (epiw == 8 ? gemm_tf32_kernel<2, 8> : gemm_tf32_kernel<2, 4>)
                    : (epiw == 8 ? gemm_tf32_kernel<1, 8> : gemm_tf32_kernel<1, 4>);
   const int kThreads = epiw == 8 ? threads_for<8>() : threads_for<4>();
-  if (!attr_set[ncta - 1][epiw == 8]) {
-    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set[ncta - 1][epiw == 8] = true;
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    bool& done = attr_set[ctx->device][(ncta - 1) * 2 + (epiw == 8)];
+    if (!done) {
+      CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      done = true;
+    }
   }
   // timing label: the GEMM's shape class (row-sized extents as "rows")
   auto dim = [](uint32_t x) { return x > 4096 ? std::string("rows") : std::to_string(x); };

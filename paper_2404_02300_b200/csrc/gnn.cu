@@ -675,6 +675,9 @@ void check_pair(catgnn_model m, catgnn_shard s) {
   if (!s) throw ConfigError("null shard");
   if (s->ctx != m->ctx) throw ConfigError("model and shard must share one context");
   if (s->dim != m->cfg.in_dim) throw DataError("shard feature width differs from the model input width");
+  // a train label outside [0, classes) would silently drop its one-hot term in K4
+  if (!s->h_train.empty() && (s->train_label_min < 0 || (uint32_t)s->train_label_max >= m->cfg.classes))
+    throw DataError("train-row label outside [0, classes) of the model");
 }
 
 }  // namespace

@@ -175,6 +175,142 @@ __global__ void __launch_bounds__(kSgcThreads) sgc_train_kernel(const Replica* _
   }
 }
 
+// Shapes that do not fit one CTA's shared memory (dim*C + batch*C floats over
+// 227 KB, e.g. the reference's default batch 512 with 128-d features and 172
+// classes, or softmax_gradient over a whole train set) or with more than 256
+// classes: the same algorithm and update order as sgc_train_kernel, with W/b
+// updated in place in global memory and the batch's P and row ids in a
+// per-replica global scratch slab.  __syncthreads orders the block's global
+// writes exactly as it orders the shared-memory ones above.
+__global__ void __launch_bounds__(kSgcThreads) sgc_train_global_kernel(const Replica* __restrict__ reps,
+                                                                       float* scratch, size_t slab,
+                                                                       uint32_t dim, uint32_t C, float lr,
+                                                                       uint32_t batch, uint32_t n_epochs,
+                                                                       int grad_only) {
+  const Replica rep = reps[blockIdx.x];
+  float* P = scratch + (size_t)blockIdx.x * slab;                      // batch*C
+  uint32_t* rows = reinterpret_cast<uint32_t*>(P + (size_t)batch * C);  // batch
+  float* W = rep.W;
+  float* bv = rep.b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  if (rep.n_train == 0) return;
+  for (uint32_t ep = 0; ep < n_epochs; ++ep) {
+    const uint32_t* ord = rep.order + (size_t)ep * rep.n_train;
+    for (uint64_t start = 0; start < rep.n_train; start += batch) {
+      const uint32_t cnt = (uint32_t)(batch < rep.n_train - start ? (uint64_t)batch : rep.n_train - start);
+      for (uint32_t i = tid; i < cnt; i += blockDim.x) rows[i] = ord[start + i];
+      __syncthreads();
+      const float inv_cnt = 1.0f / (float)cnt;
+      for (uint32_t bi = warp; bi < cnt; bi += nwarps) {
+        const uint32_t row = rows[bi];
+        const float* x = rep.x + (size_t)row * rep.ld;
+        float* pr = P + (size_t)bi * C;
+        float m = -INFINITY;
+        for (uint32_t c0 = 0; c0 < C; c0 += 32) {  // logits, chunk by chunk
+          const float v = row_logit_chunk(x, dim, W, C, c0, lane);
+          if (c0 + lane < C) {
+            pr[c0 + lane] = v + bv[c0 + lane];
+            m = fmaxf(m, pr[c0 + lane]);
+          }
+        }
+        m = warp_max(m);
+        float s = 0.f;
+        for (uint32_t c = lane; c < C; c += 32) {
+          const float e = expf(pr[c] - m);
+          pr[c] = e;
+          s += e;
+        }
+        s = warp_sum(s);
+        const int y = rep.labels[row];
+        for (uint32_t c = lane; c < C; c += 32) {
+          float p = pr[c] / s;
+          if ((int)c == y) p -= 1.0f;
+          pr[c] = p * inv_cnt;
+        }
+      }
+      __syncthreads();
+      for (uint32_t k = tid; k < dim; k += blockDim.x) {
+        for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+          const uint32_t cn = min(32u, C - c0);
+          float g[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) g[i] = 0.f;
+          for (uint32_t bi = 0; bi < cnt; ++bi) {
+            const float xv = rep.x[(size_t)rows[bi] * rep.ld + k];
+            const float* pr = P + (size_t)bi * C + c0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < (int)cn) g[i] = fmaf(xv, pr[i], g[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < (int)cn) {
+              if (grad_only) rep.gW[(size_t)k * C + c0 + i] = g[i];
+              else W[(size_t)k * C + c0 + i] -= lr * g[i];
+            }
+        }
+      }
+      for (uint32_t c = tid; c < C; c += blockDim.x) {
+        float gbv = 0.f;
+        for (uint32_t bi = 0; bi < cnt; ++bi) gbv += P[(size_t)bi * C + c];
+        if (grad_only) rep.gb[c] = gbv;
+        else bv[c] -= lr * gbv;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Any class count (> 256): logits chunk by chunk with an online max / sum of
+// exponentials, so nothing per row is stored; first-maximum argmax because the
+// chunks are visited in increasing class order and only a strictly larger
+// logit replaces the best.
+__global__ void sgc_eval_any_kernel(const float* __restrict__ x, uint32_t ld, uint32_t dim,
+                                    const float* __restrict__ W, const float* __restrict__ b, uint32_t C,
+                                    const int32_t* __restrict__ labels, const uint32_t* __restrict__ mask,
+                                    uint64_t n_mask, unsigned long long* correct, double* row_loss) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = wid; i < n_mask; i += nw) {
+    const uint32_t row = mask[i];
+    const float* xr = x + (size_t)row * ld;
+    const int y = labels[row];
+    float best = -INFINITY, s = 0.f, zy = 0.f;
+    int bidx = 0x7fffffff;
+    for (uint32_t c0 = 0; c0 < C; c0 += 32) {
+      const float v = row_logit_chunk(xr, dim, W, C, c0, lane);
+      if (c0 + lane < C) {
+        const float z = v + b[c0 + lane];
+        if (z > best) {
+          s = s * expf(best - z) + 1.0f;  // rescale the running sum to the new maximum
+          best = z;
+          bidx = (int)(c0 + lane);
+        } else {
+          s += expf(z - best);
+        }
+        if ((int)(c0 + lane) == y) zy = z;
+      }
+    }
+    float gbest = best;
+    int gidx = bidx;
+#pragma unroll
+    for (int m = 16; m; m >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, gbest, m);
+      int oi = __shfl_xor_sync(0xffffffffu, gidx, m);
+      if (ob > gbest || (ob == gbest && oi < gidx)) { gbest = ob; gidx = oi; }
+    }
+    if (row_loss) {
+      const float ls = best == -INFINITY ? 0.f : s * expf(best - gbest);
+      const float tot = warp_sum(ls);
+      zy = warp_sum(zy);
+      if (lane == 0) row_loss[i] = (double)gbest + log((double)tot) - (double)zy;
+    }
+    if (lane == 0 && correct && gidx == y) atomicAdd(correct, 1ull);
+  }
+}
+
 // Per mask row: argmax (first maximum, like Eigen's maxCoeff) vs label, plus
 // the row's cross-entropy for the loss hook.
 template <int CT>
@@ -283,10 +419,8 @@ void launch_eval(const float* x, uint32_t ld, uint32_t dim, const float* W, cons
 
 void sgc_train(catgnn_ctx ctx, const std::vector<SgcReplicaHost>& reps, uint32_t dim, uint32_t C,
                float lr, uint32_t batch, uint32_t n_epochs, bool grad_only) {
-  if (C == 0 || C > 256) throw ConfigError("class count must be in [1, 256] for the SGC kernel");
-  size_t smem = sgc_smem_bytes(dim, C, batch);
-  if (smem > 227 * 1024)
-    throw ConfigError("SGC parameters + batch do not fit in shared memory (dim*C + batch*C too large)");
+  if (C == 0) throw ConfigError("class count must be >= 1");
+  if (batch == 0) throw ConfigError("batch size must be >= 1");
   std::vector<Replica> h(reps.size());
   for (size_t i = 0; i < reps.size(); ++i)
     h[i] = Replica{reps[i].x, reps[i].ld, reps[i].labels, reps[i].order, reps[i].n_train,
@@ -294,12 +428,26 @@ void sgc_train(catgnn_ctx ctx, const std::vector<SgcReplicaHost>& reps, uint32_t
   Replica* d = ctx->scratch_buf<Replica>("sgc_reps", h.size());
   CG_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(Replica), cudaMemcpyHostToDevice, ctx->stream));
   const uint32_t n = (uint32_t)h.size();
-  const int ct = (int)((C + 31) / 32);
-  switch (ct) {
-    case 1: launch_train<1>(d, n, dim, C, lr, batch, n_epochs, grad_only, smem, ctx->stream); break;
-    case 2: launch_train<2>(d, n, dim, C, lr, batch, n_epochs, grad_only, smem, ctx->stream); break;
-    case 3: case 4: launch_train<4>(d, n, dim, C, lr, batch, n_epochs, grad_only, smem, ctx->stream); break;
-    default: launch_train<8>(d, n, dim, C, lr, batch, n_epochs, grad_only, smem, ctx->stream); break;
+  // a batch never holds more rows than the largest train set
+  uint64_t max_rows = 1;
+  for (const auto& r : reps) max_rows = std::max<uint64_t>(max_rows, r.n_train);
+  const uint32_t eff_batch = (uint32_t)std::min<uint64_t>(batch, max_rows);
+  const size_t smem = sgc_smem_bytes(dim, C, eff_batch);
+  if (C <= 256 && smem <= 227 * 1024) {
+    const int ct = (int)((C + 31) / 32);
+    switch (ct) {
+      case 1: launch_train<1>(d, n, dim, C, lr, eff_batch, n_epochs, grad_only, smem, ctx->stream); break;
+      case 2: launch_train<2>(d, n, dim, C, lr, eff_batch, n_epochs, grad_only, smem, ctx->stream); break;
+      case 3: case 4: launch_train<4>(d, n, dim, C, lr, eff_batch, n_epochs, grad_only, smem, ctx->stream); break;
+      default: launch_train<8>(d, n, dim, C, lr, eff_batch, n_epochs, grad_only, smem, ctx->stream); break;
+    }
+  } else {
+    // W/b stay where the caller put them (global); P + rows per replica in scratch
+    const size_t slab = round_up64((uint64_t)eff_batch * C + eff_batch, 4);
+    float* scratch = ctx->scratch_buf<float>("sgc_global_slab", slab * n);
+    sgc_train_global_kernel<<<n, kSgcThreads, 0, ctx->stream>>>(d, scratch, slab, dim, C, lr, eff_batch,
+                                                                 n_epochs, grad_only);
+    CG_CHECK_LAUNCH();
   }
   ctx->launches++;
   CG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -308,13 +456,20 @@ void sgc_train(catgnn_ctx ctx, const std::vector<SgcReplicaHost>& reps, uint32_t
 void sgc_eval(catgnn_ctx ctx, const float* x, uint32_t ld, uint32_t dim, const float* W,
               const float* b, uint32_t C, const int32_t* labels, const uint32_t* mask,
               uint64_t n_mask, unsigned long long* correct, double* row_loss) {
-  if (C == 0 || C > 256) throw ConfigError("class count must be in [1, 256]");
+  if (C == 0) throw ConfigError("class count must be >= 1");
   const int ct = (int)((C + 31) / 32);
   switch (ct) {
     case 1: launch_eval<1>(x, ld, dim, W, b, C, labels, mask, n_mask, correct, row_loss, ctx->stream); break;
     case 2: launch_eval<2>(x, ld, dim, W, b, C, labels, mask, n_mask, correct, row_loss, ctx->stream); break;
     case 3: case 4: launch_eval<4>(x, ld, dim, W, b, C, labels, mask, n_mask, correct, row_loss, ctx->stream); break;
-    default: launch_eval<8>(x, ld, dim, W, b, C, labels, mask, n_mask, correct, row_loss, ctx->stream); break;
+    case 5: case 6: case 7: case 8:
+      launch_eval<8>(x, ld, dim, W, b, C, labels, mask, n_mask, correct, row_loss, ctx->stream); break;
+    default: {
+      unsigned grid = (unsigned)std::min<uint64_t>((n_mask + 7) / 8, 148 * 16);
+      sgc_eval_any_kernel<<<std::max(1u, grid), 256, 0, ctx->stream>>>(x, ld, dim, W, b, C, labels, mask,
+                                                                       n_mask, correct, row_loss);
+      CG_CHECK_LAUNCH();
+    }
   }
   ctx->launches++;
 }

@@ -42,6 +42,7 @@ struct catgnn_shard_s {
   catgnn::DevBuf<int32_t> labels;
   catgnn::DevBuf<uint32_t> d_train, d_val, d_test;
   uint32_t classes = 1;
+  int32_t train_label_min = 0, train_label_max = -1;  // over the train rows (model class-range check)
   // replica map (only for shards created from a partition)
   std::vector<uint64_t> ext_ids;
   std::vector<uint8_t> owner, role;
