@@ -2,7 +2,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload reddit_gcn] [--sync S]
-    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+    (N > 1: launched under `python -m torch.distributed.run --nproc-per-node N ...
+     bench.py --gpus N`, or started plainly with --gpus N, in which case bench.py
+     re-executes itself under torch.distributed.run with N ranks; the world size
+     must equal --gpus)
 
 Workload (default, BASELINE.json configs[1]): 2-layer GCN (hidden 256) on the
 reddit-shaped synthetic RMAT graph (scale 18, 57,307,946 undirected edges =
@@ -107,6 +110,30 @@ def dist_env():
     return world, rank, local
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(gpus):
+    """`python bench.py --gpus N` without a launcher: re-execute this command as N
+    ranks under torch.distributed.run (one process per GPU, 127.0.0.1
+    rendezvous) and return its exit code.  NCCL_DEBUG=INFO (INIT subsystem) so
+    the communicator's rank count is visible in the log."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    log(f"[bench] --gpus {gpus} without a launcher: {' '.join(cmd)}")
+    return subprocess.call(cmd, env=env)
+
+
 def act_width(d):
     """Row stride of a device activation (gnn.cu act_width): 16-float multiples below 128."""
     return (d + 15) // 16 * 16 if d < 128 else (d + 3) // 4 * 4
@@ -117,16 +144,72 @@ def agg_bytes(nnz, rows, width, self_term):
     return nnz * (4 + 4 * width) + rows * (4 * width * (1 + self_term) + 8)
 
 
-def load_ncu_traffic(workload):
-    """ncu DRAM bytes per K2 launch for this workload (profiles/r01_k2_traffic.json,
-    written from the `ncu --set full` capture of the same bench command)."""
-    p = os.path.join(ROOT, "profiles", "r01_k2_traffic.json")
+def load_ncu_traffic(w):
+    """ncu DRAM / L2 bytes of every K2 launch of one step of this workload
+    (profiles/r02_k2_traffic_<workload>.json, scripts/k2_traffic.py: an ncu
+    metric pass over the same bench command), or None."""
+    p = os.path.join(ROOT, "profiles", f"r02_k2_traffic_{w.name}.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        if d.get("workload", "reddit_gcn") == workload:
+        if d.get("workload_key") == w.key():
             return d
     return None
+
+
+def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step, hbm, hbm_src, l2_gbs, hbm_rd):
+    """Roofline of K2 whose every number is a fraction of the peak it is divided by:
+    * effective_gbs: SURVEY §8(d) algorithmic bytes (nnz*(4+4d) + N*(4d(1+self)+8)
+      per pass) / in-step K2 time.  Each gathered row counts once per edge, so on
+      RMAT hubs this exceeds what DRAM moves: it is what the SMs pull through L2.
+    * dram_gbs: ncu DRAM bytes of the same launches / the same in-step time.
+    * bound "hbm" when the DRAM rate is near the HBM peak (dram_frac >= 0.75),
+      else "l2" when the effective rate exceeds the HBM peak (the gathers are
+      served from L2: the ceiling is the measured L2 read rate), else "hbm"."""
+    self_term = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
+    widths = w.passes()
+    algo = sum(agg_bytes(nz, rw, wd, self_term) for nz, rw in zip(part_nnz, part_rows) for wd in widths)
+    comp = sum(2 * 4 * wd * rw + 4 * nz + 8 * (rw + 1) for nz, rw in zip(part_nnz, part_rows) for wd in widths)
+    t = agg_ms_step / 1e3
+    eff = algo / t / 1e9 if t > 0 else None
+    ncu = load_ncu_traffic(w)
+    dram = l2b = None
+    if ncu:
+        mine_set = set(mine)
+        recs = [r for r in ncu["launches"] if r["partition"] in mine_set]
+        dram = sum(r["dram_bytes"] for r in recs)
+        l2b = sum(r["l2_bytes"] for r in recs)
+    dram_gbs = dram / t / 1e9 if (dram and t > 0) else None
+    dram_frac = dram_gbs / hbm if dram_gbs else None
+    if dram_frac is not None and dram_frac >= 0.75:
+        bound = "hbm"
+    elif eff and eff > hbm and l2_gbs:
+        bound = "l2"
+    else:
+        bound = "hbm"
+    if bound == "l2":
+        achieved, peak, src = eff, l2_gbs, ("catgnn_probe_read_bandwidth: 64 MB buffer, 128-bit ld.global.cg, "
+                                            "50 passes, best of 3 (measured L2 read rate, same device)")
+    else:
+        achieved, peak, src = (dram_gbs if dram_gbs else eff), hbm, f"MEASURED_PEAKS.json hbm_gbs ({hbm_src})"
+    per_launch = max(agg_launches, 1)
+    return {"bound": bound, "kernel": "catgnn::agg_kernel (K2 neighbourhood aggregation)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
+            "traffic": dram / per_launch if dram else None, "peak_source": src,
+            "effective_gbs": eff, "algorithmic_bytes_per_step": algo,
+            "algorithmic_bytes_per_launch": algo / per_launch,
+            "dram_bytes_per_step": dram, "dram_gbs": dram_gbs, "dram_frac": dram_frac,
+            "hbm_peak_gbs": hbm, "hbm_read_probe_gbs": hbm_rd,
+            "l2_read_peak_gbs": l2_gbs, "l2_frac": eff / l2_gbs if (eff and l2_gbs) else None,
+            "l2_bytes_per_step_ncu": l2b,
+            "compulsory_bytes_per_step": comp, "dram_over_compulsory": dram / comp if dram else None,
+            "launches_per_step": agg_launches, "agg_ms_per_step": agg_ms_step,
+            "agg_share_of_step": agg_ms_step / ms_step,
+            "traffic_source": (ncu["source"] if ncu else "no ncu capture for this workload "
+                               "(profiles/r02_k2_traffic_<workload>.json)"),
+            "note": "frac = achieved / peak of the bound that applies; effective_gbs counts every gathered "
+                    "row per edge (SURVEY §8(d) bytes) and exceeds the DRAM peak when rows are re-served "
+                    "from L2; dram_* are ncu DRAM bytes over the in-step K2 time"}
 
 
 def reference_jobs(prep, samples, budget_edges):
@@ -246,9 +329,13 @@ def main():
                     help="replay the device-resident step as one CUDA graph (1) or enqueue it eagerly (0)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args.gpus))
     from paper_2404_02300_b200 import workloads as W
     w = W.WORKLOADS[args.workload]
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"world size {world} (WORLD_SIZE) != --gpus {args.gpus}: launch one rank per GPU")
     if args.impl == "reference":
         if rank == 0:
             prep = W.prepare(w, log)
@@ -260,8 +347,15 @@ def main():
     # CATGNN_BENCH_HOST_COLLECTIVES=1: validation mode for the multi-rank flow on a
     # single-GPU box (ranks share the device, gloo on the host replaces NCCL)
     host_coll = os.environ.get("CATGNN_BENCH_HOST_COLLECTIVES") == "1"
+    ndev = torch.cuda.device_count()
+    if world > ndev and not host_coll:
+        # more ranks than GPUs (e.g. --gpus 2 on a one-GPU box): NCCL refuses two
+        # ranks on one device, so the ranks share the GPUs and collectives go through
+        # gloo on the host; the line says so (config.shared_devices)
+        log(f"[bench] {world} ranks on {ndev} GPU(s): ranks share devices, host (gloo) collectives")
+        host_coll = True
     if host_coll:
-        local = local % max(1, torch.cuda.device_count())
+        local = local % max(1, ndev)
     torch.cuda.set_device(local)
     if world > 1:
         if host_coll:
@@ -280,7 +374,7 @@ def main():
     meta = prep["meta"]
 
     from paper_2404_02300_b200 import gnnpart as gp
-    from paper_2404_02300_b200.gnn import ADAM, Comm, GNNModel, model_average, sync_weights
+    from paper_2404_02300_b200.gnn import ADAM, Comm, GNNModel, model_average, sync_weights, weighted_sum
     stream = torch.cuda.Stream()
     ctx = gp.Context(local, stream.cuda_stream)
     # shard lanes: partition k of this rank trains on lane k % L (own stream and
@@ -319,6 +413,7 @@ def main():
     alpha_all = sync_weights(counts_all)
     my_alpha = [alpha_all[i] for i in mine]
     my_counts = [counts_all[i] for i in mine]
+    shared_devices = world > ndev
     comm = None
     feat_comm = None
     if world > 1 and not host_coll:
@@ -349,11 +444,9 @@ def main():
         if world == 1:
             model_average(reps, my_counts, shared)
         else:
-            if len(reps) == 1:
-                shared.copy_params_from(reps[0])
-            else:
-                model_average(reps, my_counts, shared)
-            shared.scale(sum(my_alpha))
+            # this rank's share sum_i alpha_i theta_i with the GLOBAL alphas (a
+            # rank without train rows contributes zeros), then the all-reduce
+            weighted_sum(reps, my_alpha, shared)
             if comm is not None:
                 shared.allreduce(comm)  # C1: NCCL all-reduce on the library stream
             else:  # host-collective validation mode
@@ -537,33 +630,18 @@ def main():
     value = edges_per_step * args.steps / (total_ms / 1e3)
 
     # roofline of the dominant kernel (K2) from per-launch CUDA events
-    self_terms = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
-    algo_bytes = sum(agg_bytes(nz, rw, wd, self_terms) for nz, rw in zip(part_nnz, part_rows) for wd in widths)
     agg_ms_step = kt["agg_ms"] / timed_steps
     hbm, bf16, src = peaks()
-    achieved_gbs = algo_bytes / (agg_ms_step / 1e3) / 1e9 if agg_ms_step > 0 else None
     per_launch = kt["agg_launches"] / timed_steps
-    ncu = load_ncu_traffic(w.name)
-    roofline = {"bound": "hbm", "kernel": "catgnn::agg_kernel (K2 neighbourhood aggregation)",
-                "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved_gbs / hbm) if achieved_gbs else None,
-                "traffic": ncu.get("dram_bytes_per_launch") if ncu else None,
-                "algorithmic_bytes_per_launch": algo_bytes / max(per_launch, 1),
-                "launches_per_step": per_launch, "agg_ms_per_step": agg_ms_step,
-                "agg_share_of_step": agg_ms_step / ms_step,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                "note": "algorithmic bytes per SURVEY §8(d); RMAT hub rows are re-served from L2, so "
-                        "algorithmic GB/s can exceed the DRAM peak — traffic is ncu dram bytes"}
-    # L2 / HBM read-rate probes (same device, after the timed region): the 256-wide
-    # gathers hit L2 69% of the time, so the L2 read rate is their practical ceiling
+    # L2 / HBM read-rate probes (same device, after the timed region)
+    l2_gbs = hbm_rd_gbs = None
     try:
         l2_gbs = max(gp.probe_read_bandwidth(64 << 20, 50, ctx) for _ in range(3))
         hbm_rd_gbs = max(gp.probe_read_bandwidth(4 << 30, 3, ctx) for _ in range(2))
-        roofline.update({"l2_read_peak_gbs": l2_gbs, "hbm_read_probe_gbs": hbm_rd_gbs,
-                         "l2_frac": (achieved_gbs / l2_gbs) if achieved_gbs else None,
-                         "l2_peak_source": "catgnn_probe_read_bandwidth: 64 MB buffer, 128-bit ld.global.cg, 50 passes, best of 3"})
     except Exception as ex:  # pragma: no cover
         log("[probe] failed:", ex)
+    roofline = k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, per_launch, ms_step, hbm, src, l2_gbs,
+                           hbm_rd_gbs)
     # useful GEMM flops per step: forward + weight gradient (+ input gradient past layer 0)
     gemm_flops = 0
     for rows_i in part_rows:
@@ -621,11 +699,15 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
 
     if rank == 0:
+        cfg = workload_config(w, prep, args)
+        if host_coll:
+            cfg["collectives"] = "host (gloo): validation mode, not an NVLink measurement"
+            cfg["shared_devices"] = bool(shared_devices)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 aggregation)",
                 "data": "synthetic (RMAT + reference SPRING partitions, random-init weights)",
-                "config": workload_config(w, prep, args), "roofline": roofline, "gemm": gemm,
+                "config": cfg, "roofline": roofline, "gemm": gemm,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "step_breakdown": breakdown,
                 "global_nnz_edges_per_s": meta["nnz"] * len(widths) * args.steps / (total_ms / 1e3),
                 "clocks": clk.summary()}

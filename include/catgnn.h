@@ -280,6 +280,12 @@ int catgnn_distributed_train(uint32_t p, const catgnn_shard* shards, catgnn_shar
 #define CATGNN_MODEL_GCN 1  /* h' = D^-1/2 (A+I) D^-1/2 h W^T + b           */
 #define CATGNN_MODEL_SAGE 2 /* h' = h W_s^T + mean_N(h) W_n^T + b          */
 #define CATGNN_MODEL_GIN 3  /* h' = ((1+eps) h + sum_N h) W^T + b, eps = 0 */
+/* h' = D~^-1 (A+I) h W^T + b, zero-initialised: with one layer this is the
+ * reference's own model (sgc_propagate with prop_hops = 1, then softmax
+ * regression, train.cpp:49-94, zero_params :67-72), here trained full-batch
+ * through the GNN kernels (K2 + K3 + K4 + K5) so that machinery can be checked
+ * against the compiled reference's distributed_train. */
+#define CATGNN_MODEL_SGC 4
 #define CATGNN_OPT_SGD 0
 #define CATGNN_OPT_ADAM 1
 typedef struct {
@@ -328,6 +334,57 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
  * alpha from sync_weights(train_counts); dst may alias one of src. */
 int catgnn_model_average(uint32_t n, const catgnn_model* src, const uint64_t* train_counts,
                          catgnn_model dst);
+/* Weighted sum with caller-supplied weights (model_average's loop,
+ * train.cpp:164-169, with alpha from the GLOBAL sync_weights): a rank's share
+ * of the cross-rank average before catgnn_model_allreduce.  Zero weights are
+ * fine (a rank whose partitions hold no train rows contributes zeros). */
+int catgnn_model_weighted_sum(uint32_t n, const catgnn_model* src, const double* alpha, catgnn_model dst);
+
+/* ------------------------------------ GNN distributed training (north star) */
+/* distributed_train (train.cpp:289-340, train.hpp:118-124) for the GNN models:
+ * the artifact's partitions are loaded (load_training_data, train.cpp:216-287),
+ * each trained full-batch (one local iteration = forward + backward + one
+ * optimizer step), and every sync_interval iterations
+ * (chunks of min(s, remaining), :315-316) the replicas restart from the
+ * alpha-weighted average of all partitions (sync_weights over the partitions'
+ * owner && train counts, :139-172).  After each average the val / test
+ * micro-F1 of the averaged model on the global graph is recorded (:324-335)
+ * when eval_global is set.
+ * comm == NULL: this process trains every partition.  Otherwise rank r of the
+ * communicator trains partitions r, r + nranks, ... and the
+ * average is the alpha-prescaled weighted sum + ncclAllReduce over NVLink.
+ * Errors as the reference: workers == 0 or p % workers != 0 or
+ * sync_interval == 0 -> ConfigError (2); p % nranks != 0 -> ConfigError. */
+typedef struct {
+  catgnn_model_config model; /* in_dim 0 = the artifact's feature width; classes 0 = max label + 1 */
+  uint32_t epochs;           /* local iterations */
+  uint32_t sync_interval;
+  uint32_t workers;          /* logical workers q (the reference's p % q check) */
+  int eval_global;           /* record val/test micro-F1 on the global graph per sync */
+} catgnn_gnn_train_config;
+typedef struct {
+  float* params;             /* out: logical flat parameters (catgnn_model_get_params layout) or NULL */
+  uint64_t params_capacity;  /* floats available at params */
+  uint64_t num_params;       /* out */
+  double* losses;            /* out: per local iteration sum_i alpha_i mean-CE_i over ALL partitions */
+  uint64_t loss_capacity;
+  uint64_t n_losses;         /* out */
+  uint64_t* hist_epoch; uint64_t* hist_syncs; double* hist_val; double* hist_test;
+  uint64_t hist_capacity;
+  uint64_t n_hist;           /* out */
+  uint64_t averaging_ops;    /* out */
+  uint32_t in_dim, classes;  /* out: resolved model widths */
+  catgnn_model* model_out;   /* if non-NULL, receives the averaged model (destroy with catgnn_model_destroy) */
+} catgnn_gnn_result;
+int catgnn_gnn_distributed_train(catgnn_ctx ctx, const char* artifact_dir, const char* input,
+                                 const char* features, const catgnn_gnn_train_config* cfg,
+                                 catgnn_comm comm, catgnn_gnn_result* result);
+/* train_local (train.cpp:130-137) on the device: zero_params + train_epochs
+ * over the shard's train rows with cfg->seed, on the shard's features
+ * propagated prop_hops times (the --compare-centralized path of train-sim,
+ * gnnpart.cpp:330-339, calls it on the global shard).  W (dim x classes) and b
+ * (classes) are outputs; classes = max label + 1 over the shard. */
+int catgnn_train_local(catgnn_shard s, const catgnn_train_config* cfg, float* W, float* b, uint32_t* classes);
 
 /* ---------------------------------------------------------- multi-GPU (C1) */
 int catgnn_comm_unique_id(char id[128]);

@@ -13,9 +13,12 @@ layers under the reference's conventions:
     tensor (train.cpp:139-172), chunks of min(s, remaining) local iterations
     (train.cpp:315-323); optimizer state is per replica and not averaged;
   * micro-F1 = pooled TP/(TP+miss) with first-index argmax (train.cpp:174-198).
-Its only pinned piece is the aggregation primitive: with mean-with-self
-normalisation `aggregate` IS sgc_propagate, checked against the reference in
-tests/test_gnn_oracle.py.
+Pinned to the compiled reference (tests/test_gnn_oracle.py): with
+mean-with-self normalisation `aggregate` IS sgc_propagate; the SGC kind (one
+layer, D~^-1 (A+I) h W^T + b, zero init, SGD, full batch) reproduces the
+reference's own distributed_train (prop_hops = 1, batch >= every train set);
+loss / dlogits / dW against softmax_loss / softmax_gradient, `model_average`
+against model_average and `micro_f1` against evaluate_micro_f1.
 
 Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this.
 """
@@ -29,7 +32,7 @@ import scipy.sparse as sp
 
 from paper_2404_02300_b200.synth import mix64, seed_for  # common.hpp:27-39 restated
 
-GCN, SAGE, GIN = 1, 2, 3
+GCN, SAGE, GIN, SGC = 1, 2, 3, 4
 SGD, ADAM = 0, 1
 
 
@@ -86,9 +89,14 @@ def layer_dims(kind, layers, in_dim, hidden, classes):
 
 
 def init_params(kind, layers, in_dim, hidden, classes, seed):
-    """Glorot-uniform from splitmix64(seed_for(seed, layer) + i), biases zero."""
+    """Glorot-uniform from splitmix64(seed_for(seed, layer) + i), biases zero;
+    the SGC kind is zero-initialised like the reference (zero_params,
+    train.cpp:67-72)."""
     params = []
     for l, (d_in, d_out, _, shape) in enumerate(layer_dims(kind, layers, in_dim, hidden, classes)):
+        if kind == SGC:
+            params.append([np.zeros(shape), np.zeros(d_out)])
+            continue
         a = np.sqrt(6.0 / (d_in + d_out))
         base = seed_for(seed, l)
         n = shape[0] * shape[1]
@@ -124,6 +132,10 @@ def forward(kind, params, G: Graph, X, agg_first_flags):
             aux.append(A_h)
         elif kind == GIN:
             A_h = G.aggregate(h, "none", True)
+            Z = A_h @ W.T + b
+            aux.append(A_h)
+        elif kind == SGC:
+            A_h = G.aggregate(h, "sgc", True)  # sgc_propagate, one hop (train.cpp:49-65)
             Z = A_h @ W.T + b
             aux.append(A_h)
         else:
@@ -165,12 +177,14 @@ def backward(kind, params, G: Graph, H, Zs, aux, dZ_last, agg_first_flags):
         W, b = params[l]
         h = H[l]
         db = dZ.sum(axis=0)
-        if kind in (GCN, GIN):
+        if kind in (GCN, GIN, SGC):
             dW = dZ.T @ aux[l]
             dA = dZ @ W
             if kind == GCN:
                 dinv = 1.0 / np.sqrt(1.0 + G.deg)
                 dh = G.aggregate(dA, "gcn", True, pre=dinv)
+            elif kind == SGC:  # transpose of D~^-1 (A+I): (A+I) D~^-1
+                dh = G.aggregate(dA, "none", True, pre=1.0 / (1.0 + G.deg))
             else:
                 dh = G.aggregate(dA, "none", True)
         else:
@@ -256,6 +270,15 @@ def sync_weights(counts):
     return alpha
 
 
+def model_average(params_list, counts):
+    """train.cpp:154-172: sum_i alpha_i theta_i from zero, in partition order."""
+    alpha = sync_weights(counts)
+    flat = np.zeros_like(flatten(params_list[0]))
+    for a, p in zip(alpha, params_list):
+        flat = flat + a * flatten(p)
+    return unflatten(flat, params_list[0])
+
+
 def micro_f1(Z, labels, rows):
     rows = np.asarray(rows, np.int64)
     pred = np.argmax(Z[rows], axis=1)  # first maximum, like Eigen maxCoeff
@@ -285,10 +308,7 @@ def distributed_train(kind, shards: List[OracleShard], sync_interval, epochs, la
             for a, r, s in zip(alpha, reps, shards):
                 ep_loss += a * r.step(s)
             losses.append(ep_loss)
-        flat = np.zeros_like(flatten(shared))
-        for a, r in zip(alpha, reps):
-            flat = flat + a * flatten(r.params)
-        shared = unflatten(flat, shared)
+        shared = model_average([r.params for r in reps], counts)
         done += chunk
         ops += 1
         if global_shard is not None:
@@ -298,3 +318,12 @@ def distributed_train(kind, shards: List[OracleShard], sync_interval, epochs, la
             tf = micro_f1(Zs[-1], global_shard.labels, global_shard.test_rows) if len(global_shard.test_rows) else 0.0
             hist.append((done, ops, vf, tf))
     return dict(params=shared, losses=losses, history=hist, averaging_ops=ops)
+
+
+def shard_from_ref(rs) -> OracleShard:
+    """OracleShard from oracle.ref.TrainingData.shard() (load_training_data,
+    train.cpp:216-287, as the compiled reference built it)."""
+    rows = rs.labels.size
+    return OracleShard(Graph.from_csr(rs.offsets, rs.neighbors, rows), np.asarray(rs.features, np.float64),
+                       rs.labels.astype(np.int64), rs.train_rows.astype(np.int64),
+                       rs.val_rows.astype(np.int64), rs.test_rows.astype(np.int64))

@@ -108,6 +108,9 @@ def _load():
         "catgnn_model_forward": (C.c_int, [vp, vp, vp, C.c_int, P(f64)]),
         "catgnn_model_export": (C.c_int, [vp, u32, C.c_int, vp, P(u32)]),
         "catgnn_model_average": (C.c_int, [u32, vp, vp, vp]),
+        "catgnn_model_weighted_sum": (C.c_int, [u32, vp, vp, vp]),
+        "catgnn_gnn_distributed_train": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p, vp, vp, vp]),
+        "catgnn_train_local": (C.c_int, [vp, vp, vp, vp, P(u32)]),
         "catgnn_comm_unique_id": (C.c_int, [vp]),
         "catgnn_comm_create": (C.c_int, [vp, C.c_int, C.c_int, vp, P(vp)]),
         "catgnn_comm_destroy": (C.c_int, [vp]),
@@ -172,3 +175,17 @@ class ModelConfig(C.Structure):
     _fields_ = [("kind", C.c_int), ("layers", C.c_uint32), ("in_dim", C.c_uint32), ("hidden", C.c_uint32),
                 ("classes", C.c_uint32), ("optimizer", C.c_int), ("lr", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("seed", C.c_uint64)]
+
+
+class GnnTrainConfig(C.Structure):
+    _fields_ = [("model", ModelConfig), ("epochs", C.c_uint32), ("sync_interval", C.c_uint32),
+                ("workers", C.c_uint32), ("eval_global", C.c_int)]
+
+
+class GnnResult(C.Structure):
+    _fields_ = [("params", C.c_void_p), ("params_capacity", C.c_uint64), ("num_params", C.c_uint64),
+                ("losses", C.c_void_p), ("loss_capacity", C.c_uint64), ("n_losses", C.c_uint64),
+                ("hist_epoch", C.c_void_p), ("hist_syncs", C.c_void_p), ("hist_val", C.c_void_p),
+                ("hist_test", C.c_void_p), ("hist_capacity", C.c_uint64), ("n_hist", C.c_uint64),
+                ("averaging_ops", C.c_uint64), ("in_dim", C.c_uint32), ("classes", C.c_uint32),
+                ("model_out", C.c_void_p)]

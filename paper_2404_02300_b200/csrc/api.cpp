@@ -222,6 +222,13 @@ std::vector<uint32_t> epoch_orders(const std::vector<uint32_t>& train_rows, uint
   return all;
 }
 
+// Re-raise the error a nested ABI call recorded, with its category.
+[[noreturn]] void throw_last_error_code(int rc) {
+  if (rc == CATGNN_ECONFIG) throw ConfigError(g_last_error);
+  if (rc == CATGNN_EDATA) throw DataError(g_last_error);
+  throw InternalError(g_last_error);
+}
+
 void ensure_prop(catgnn_shard_s* s) {
   if (!s->xprop.p) throw ConfigError("features not propagated: call catgnn_sgc_propagate first");
 }
@@ -771,6 +778,28 @@ int catgnn_train_epochs(uint32_t n, const catgnn_shard* shards, float* const* W,
       CG_CUDA(cudaMemcpyAsync(b[i], pw + wn, classes * 4, cudaMemcpyDeviceToHost, st));
     }
     CG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// train_local (train.cpp:130-137): zero_params(dim, max label + 1) then
+// train_epochs over [0, epochs) with cfg->seed, on the shard's features
+// propagated prop_hops times (the caller, train-sim --compare-centralized,
+// gnnpart.cpp:330-335, propagates the global shard first).  W == NULL queries
+// the class count only.
+int catgnn_train_local(catgnn_shard s, const catgnn_train_config* cfg, float* W, float* b, uint32_t* classes) {
+  return guarded([&] {
+    check_shard(s);
+    if (!cfg) throw ConfigError("null argument");
+    if (classes) *classes = s->classes;
+    if (!W) return;
+    if (!b) throw ConfigError("null argument");
+    if (catgnn_sgc_propagate(s, cfg->prop_hops)) throw InternalError(g_last_error);
+    std::fill(W, W + (size_t)s->dim * s->classes, 0.f);  // zero_params (train.cpp:67-72)
+    std::fill(b, b + s->classes, 0.f);
+    const uint64_t seed = cfg->seed;
+    catgnn_shard_s* const sh = s;
+    if (int rc = catgnn_train_epochs(1, &sh, &W, &b, s->classes, cfg->lr, cfg->batch, 0, cfg->epochs, &seed))
+      throw_last_error_code(rc);
   });
 }
 

@@ -56,12 +56,14 @@ struct ToI64 {
 };
 
 __global__ void degree_scales_kernel(const int64_t* __restrict__ row_ptr, uint64_t rows,
-                                     float* __restrict__ dinv, float* __restrict__ inv_deg) {
+                                     float* __restrict__ dinv, float* __restrict__ inv_deg,
+                                     float* __restrict__ inv_deg1) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
        r += (uint64_t)gridDim.x * blockDim.x) {
     float d = (float)(row_ptr[r + 1] - row_ptr[r]);
     dinv[r] = 1.0f / sqrtf(1.0f + d);
     inv_deg[r] = d > 0.f ? 1.0f / d : 0.0f;
+    inv_deg1[r] = 1.0f / (1.0f + d);  // sgc_propagate's scale (train.cpp:60), as K2's kNormSgc
   }
 }
 
@@ -224,8 +226,10 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
   }
   s->dinv.alloc(std::max<uint32_t>(1, rows));
   s->inv_deg.alloc(std::max<uint32_t>(1, rows));
+  s->inv_deg1.alloc(std::max<uint32_t>(1, rows));
   if (rows) {
-    degree_scales_kernel<<<grid_for(rows), 256, 0, st>>>(s->row_ptr.p, rows, s->dinv.p, s->inv_deg.p);
+    degree_scales_kernel<<<grid_for(rows), 256, 0, st>>>(s->row_ptr.p, rows, s->dinv.p, s->inv_deg.p,
+                                                         s->inv_deg1.p);
     CG_CHECK_LAUNCH();
     ctx->launches++;
   }

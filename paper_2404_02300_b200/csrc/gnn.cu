@@ -35,6 +35,7 @@
 #include "artifact.hpp"
 #include "comm.hpp"
 #include "gemm.hpp"
+#include "model.hpp"
 #include "sgc.hpp"
 #include "shard.hpp"
 
@@ -44,20 +45,7 @@ namespace catgnn {
 
 namespace {
 
-struct Layer {
-  uint32_t d_in = 0, d_out = 0;
-  uint32_t K_in = 0;    // round4(d_in): activation row stride of the input
-  uint32_t D_out = 0;   // round4(d_out)
-  uint32_t ld_act = 0;  // row stride of this layer's output activations (>= D_out)
-  bool out_in_next_mid = false;  // output written straight into the next (SAGE aggregate-first) layer's [h | mean]
-  bool agg_first = false;
-  // internal weight matrix (GEMM B operand): w_rows x w_cols
-  uint32_t w_rows = 0, w_cols = 0;
-  uint64_t off_w = 0, off_b = 0;
-  // logical (exported) weight shape
-  uint32_t lw_rows = 0, lw_cols = 0;
-  uint32_t gemm_n = 0;   // forward GEMM N (transform-first SAGE: D_out + d_out)
-};
+
 
 __device__ __forceinline__ float wsum(float v) {
 #pragma unroll
@@ -279,20 +267,7 @@ double unit_uniform(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
 }  // namespace
 }  // namespace catgnn
 
-struct catgnn_model_s {
-  catgnn_ctx ctx = nullptr;
-  catgnn_model_config cfg{};
-  std::vector<Layer> layers;
-  uint64_t n_params = 0;
-  DevBuf<float> params, grads, m, v;
-  uint64_t step = 0;                       // updates issued (host count)
-  DevBuf<unsigned long long> step_dev;     // [completed updates, block ticket] (Adam bias correction)
-  uint64_t last_rows = 0;
-  catgnn_shard last_shard = nullptr;
-  double last_loss = 0.0;
-  DevBuf<double> loss_dev;  // sum of the last step's per-row losses (read lazily)
-  uint64_t loss_rows = 0;   // train rows of that step
-};
+
 
 namespace catgnn {
 namespace {
@@ -430,9 +405,17 @@ void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t
   ctx->launches += 2;
 }
 
+// Forward aggregation of a layer: post ⊙ (A + I)(pre ⊙ h) with
+//   GCN  pre = post = (1+deg)^-1/2,  SGC  pre = 1, post = 1/(1+deg)  (train.cpp:60),
+//   GIN  pre = post = 1.
+// A is symmetric, so the backward is pre ⊙ (A + I)(post ⊙ g): bwd_pre / bwd_norm.
 int agg_norm(const catgnn_model_s* M) {
-  return M->cfg.kind == CATGNN_MODEL_GCN ? kNormGcn : kNormNone;
+  return M->cfg.kind == CATGNN_MODEL_GCN ? kNormGcn : M->cfg.kind == CATGNN_MODEL_SGC ? kNormSgc : kNormNone;
 }
+const float* bwd_pre(const catgnn_model_s* M, const catgnn_shard_s* S) {
+  return M->cfg.kind == CATGNN_MODEL_GCN ? S->dinv.p : M->cfg.kind == CATGNN_MODEL_SGC ? S->inv_deg1.p : nullptr;
+}
+int bwd_norm(const catgnn_model_s* M) { return M->cfg.kind == CATGNN_MODEL_GCN ? kNormGcn : kNormNone; }
 
 struct Bufs {
   const float* in;  // H_{l-1}
@@ -537,7 +520,6 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   cudaStream_t st = ctx->stream;
   const uint64_t rows = S->rows;
   const uint32_t R4 = round_up((uint32_t)std::max<uint64_t>(rows, 1), 4);
-  const bool gcn = M->cfg.kind == CATGNN_MODEL_GCN;
   const bool sage = M->cfg.kind == CATGNN_MODEL_SAGE;
   const size_t nl = M->layers.size();
   // K4: dZ of the last layer
@@ -551,17 +533,17 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   double* loss_dev = M->loss_dev.p;
   CG_CUDA(cudaMemsetAsync(loss_dev, 0, 8, st));
   M->loss_rows = ntr;
-  // GCN transform-first: the last layer's backward aggregation gathers
-  // dinv * dZ, produced here by K4 instead of per edge in K2
+  // GCN / SGC transform-first: the last layer's backward aggregation gathers
+  // bwd_pre * dZ, produced here by K4 instead of per edge in K2
   float* dZs = nullptr;
-  if (gcn && !LL.agg_first) {
+  if (bwd_pre(M, S) && !LL.agg_first) {
     dZs = act(ctx, "dZs", rows, LL.ld_act, false);
     CG_CUDA(cudaMemsetAsync(dZs, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   }
   if (ntr) {
     softmax_ce_kernel<<<grid1d(ntr * 32), 256, 0, st>>>(B[nl - 1].out, B[nl - 1].out_ld, LL.d_out,
                                                       S->labels.p, S->d_train.p, ntr, dZ, LL.ld_act, row_loss,
-                                                      dZs ? S->dinv.p : nullptr, dZs);
+                                                      dZs ? bwd_pre(M, S) : nullptr, dZs);
     CG_CHECK_LAUNCH();
     sum_doubles_kernel<<<1, 1024, 0, st>>>(row_loss, ntr, loss_dev);
     CG_CHECK_LAUNCH();
@@ -622,7 +604,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         gemm(ctx, GemmOperand{dZ, dZ_ld, false}, GemmOperand{M->params.p + L.off_w, L.w_cols, true}, (uint32_t)rows,
              L.w_cols, L.d_out, e2, 1, kBwdPrecision);
         AggArgs a;
-        a.in = dA; a.in_ld = L.K_in; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
+        a.in = dA; a.in_ld = L.K_in; a.pre = bwd_pre(M, S); a.self = 1; a.norm = bwd_norm(M);
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in;
         a.mask_bits = hbits; a.mask_words = hwords;
         aggregate(S, a);
@@ -630,7 +612,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
     } else {  // GCN / GIN transform-first
       float* dT = act(ctx, "dmid", rows, L.ld_act, false);
       AggArgs a;
-      a.in = dZ; a.in_ld = dZ_ld; a.pre = gcn ? S->dinv.p : nullptr; a.self = 1; a.norm = agg_norm(M);
+      a.in = dZ; a.in_ld = dZ_ld; a.pre = bwd_pre(M, S); a.self = 1; a.norm = bwd_norm(M);
       if (li == nl - 1 && dZs) { a.in = dZs; a.pre = nullptr; }  // pre-scaled by K4
       a.out = dT; a.out_ld = L.ld_act; a.width = L.D_out;
       aggregate(S, a);
@@ -680,7 +662,45 @@ void check_pair(catgnn_model m, catgnn_shard s) {
     throw DataError("train-row label outside [0, classes) of the model");
 }
 
+__global__ void loss_accum_kernel(const double* __restrict__ loss_sum, double weight, double* acc) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *acc += weight * *loss_sum;
+}
+
 }  // namespace
+
+void model_train_step(catgnn_model m, catgnn_shard s) {
+  check_pair(m, s);
+  auto B = forward(m, s);
+  backward(m, s, B, false);
+  optimizer_step(m);
+  m->last_shard = s;
+}
+
+void model_weighted_sum(const std::vector<catgnn_model>& src, const std::vector<double>& alpha,
+                        catgnn_model dst) {
+  check_model(dst);
+  if (src.empty() || src.size() != alpha.size()) throw DataError("model averaging needs one weight per replica");
+  std::vector<const float*> ptrs(src.size());
+  for (size_t i = 0; i < src.size(); ++i) {
+    check_model(src[i]);
+    if (src[i]->n_params != dst->n_params) throw DataError("model shapes differ across replicas");
+    if (src[i]->ctx->device != dst->ctx->device) throw ConfigError("models are on different devices");
+    dst->ctx->wait_for(src[i]->ctx);  // replicas trained on other contexts' streams finish first
+    ptrs[i] = src[i]->params.p;
+  }
+  float* tmp = dst->ctx->scratch_buf<float>("avg_tmp", dst->n_params);
+  average_params(dst->ctx, ptrs, alpha, dst->n_params, tmp);
+  CG_CUDA(cudaMemcpyAsync(dst->params.p, tmp, dst->n_params * 4, cudaMemcpyDeviceToDevice, dst->ctx->stream));
+}
+
+void model_accumulate_loss(catgnn_model m, double weight, double* acc) {
+  check_model(m);
+  if (!m->loss_dev.p || m->loss_rows == 0) return;
+  loss_accum_kernel<<<1, 32, 0, m->ctx->stream>>>(m->loss_dev.p, weight / (double)m->loss_rows, acc);
+  CG_CHECK_LAUNCH();
+  m->ctx->launches++;
+}
+
 }  // namespace catgnn
 
 
@@ -690,7 +710,8 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
   return guarded([&] {
     if (!ctx || !cfg || !out) throw ConfigError("null argument");
     CG_CUDA(cudaSetDevice(ctx->device));
-    if (cfg->kind != CATGNN_MODEL_GCN && cfg->kind != CATGNN_MODEL_SAGE && cfg->kind != CATGNN_MODEL_GIN)
+    if (cfg->kind != CATGNN_MODEL_GCN && cfg->kind != CATGNN_MODEL_SAGE && cfg->kind != CATGNN_MODEL_GIN &&
+        cfg->kind != CATGNN_MODEL_SGC)
       throw ConfigError("unknown model kind");
     if (cfg->layers < 1 || cfg->in_dim < 1 || cfg->classes < 1 || (cfg->layers > 1 && cfg->hidden < 1))
       throw ConfigError("model needs >= 1 layer and positive widths");
@@ -712,11 +733,11 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
     CG_CUDA(cudaMemsetAsync(M->step_dev.p, 0, 2 * sizeof(unsigned long long), ctx->stream));
     // Glorot-uniform init: W[i] = (2u-1)*sqrt(6/(d_in+d_out)), u from
     // splitmix64(seed_for(seed, layer) + i) over the logical row-major index;
-    // biases zero.  (The reference's SGC model is zero-initialised,
-    // train.cpp:67-72; multi-layer nets need a seeded init shared with the oracle.)
+    // biases zero.  The SGC kind is the reference's model and is
+    // zero-initialised like it (zero_params, train.cpp:67-72).
     std::vector<float> logical(logical_count(M.get()), 0.f);
     uint64_t k = 0;
-    for (size_t l = 0; l < M->layers.size(); ++l) {
+    for (size_t l = 0; l < M->layers.size() && cfg->kind != CATGNN_MODEL_SGC; ++l) {
       const Layer& L = M->layers[l];
       const double a = std::sqrt(6.0 / (double)(L.d_in + L.d_out));
       const uint64_t base = seed_for(cfg->seed, l);
@@ -931,17 +952,17 @@ int catgnn_model_average(uint32_t n, const catgnn_model* src, const uint64_t* tr
       }
       alpha[n - 1] = 1.0 - partial;
     }
-    std::vector<const float*> ptrs(n);
-    for (uint32_t i = 0; i < n; ++i) {
-      check_model(src[i]);
-      if (src[i]->n_params != dst->n_params) throw DataError("model shapes differ across replicas");
-      if (src[i]->ctx->device != dst->ctx->device) throw ConfigError("models are on different devices");
-      dst->ctx->wait_for(src[i]->ctx);  // replicas trained on other contexts' streams finish first
-      ptrs[i] = src[i]->params.p;
-    }
-    float* tmp = dst->ctx->scratch_buf<float>("avg_tmp", dst->n_params);
-    average_params(dst->ctx, ptrs, alpha, dst->n_params, tmp);
-    CG_CUDA(cudaMemcpyAsync(dst->params.p, tmp, dst->n_params * 4, cudaMemcpyDeviceToDevice, dst->ctx->stream));
+    model_weighted_sum(std::vector<catgnn_model>(src, src + n), alpha, dst);
+  });
+}
+
+// A rank's share of the model average across ranks: dst = sum_i alpha_i src_i
+// with the GLOBAL sync_weights of its partitions (a rank whose partitions hold
+// no train rows contributes zeros, as the reference weights them by 0).
+int catgnn_model_weighted_sum(uint32_t n, const catgnn_model* src, const double* alpha, catgnn_model dst) {
+  return guarded([&] {
+    if (n == 0 || !src || !alpha) throw DataError("model averaging needs one weight per replica");
+    model_weighted_sum(std::vector<catgnn_model>(src, src + n), std::vector<double>(alpha, alpha + n), dst);
   });
 }
 

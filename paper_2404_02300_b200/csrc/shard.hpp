@@ -11,6 +11,7 @@
 //   xprop    f32[rows][ld]      SGC-propagated features (sgc_propagate output)
 //   dinv     f32[rows]          (1+deg)^-1/2  (GCN normalisation)
 //   inv_deg  f32[rows]          1/deg, 0 for deg 0 (SAGE mean)
+//   inv_deg1 f32[rows]          1/(1+deg)     (SGC normalisation, train.cpp:60)
 //   units    int4[n_units]      aggregation work units (see aggregate.cu)
 //   heavy    int4[n_heavy]      split rows: {row, first partial slot, chunks, 0}
 #pragma once
@@ -27,7 +28,7 @@ struct catgnn_shard_s {
   uint64_t num_edges = 0;
   catgnn::DevBuf<int64_t> row_ptr;
   catgnn::DevBuf<int32_t> col;
-  catgnn::DevBuf<float> dinv, inv_deg;
+  catgnn::DevBuf<float> dinv, inv_deg, inv_deg1;
   // aggregation plan (built once per shard, reused by every pass)
   catgnn::DevBuf<int4> units;
   catgnn::DevBuf<int4> heavy;

@@ -18,11 +18,11 @@ from typing import List, Optional
 
 import numpy as np
 
-from ._lib import ModelConfig, check, lib
+from ._lib import GnnResult, GnnTrainConfig, ModelConfig, check, lib
 from .gnnpart import Context, Shard, default_context
 
-GCN, SAGE, GIN = 1, 2, 3
-KINDS = {"gcn": GCN, "sage": SAGE, "gin": GIN}
+GCN, SAGE, GIN, SGC = 1, 2, 3, 4
+KINDS = {"gcn": GCN, "sage": SAGE, "gin": GIN, "sgc": SGC}
 SGD, ADAM = 0, 1
 
 
@@ -40,6 +40,16 @@ class GNNModel:
         check(lib.catgnn_model_create(self.ctx.handle, C.byref(self.cfg), C.byref(h)))
         self.handle = h
         self.num_params = int(lib.catgnn_model_num_params(h))
+
+    @classmethod
+    def adopt(cls, handle: C.c_void_p, ctx: Context, cfg: ModelConfig) -> "GNNModel":
+        """Wrap a model the library created (e.g. catgnn_gnn_distributed_train's result)."""
+        m = cls.__new__(cls)
+        m.ctx = ctx
+        m.handle = handle
+        m.num_params = int(lib.catgnn_model_num_params(handle))
+        m.cfg = cfg
+        return m
 
     def layer_shapes(self):
         out = []
@@ -140,6 +150,15 @@ def model_average(models: List[GNNModel], counts, dst: GNNModel):
     check(lib.catgnn_model_average(n, arr, _ptr(c), dst.handle))
 
 
+def weighted_sum(models: List[GNNModel], alpha, dst: GNNModel):
+    """dst = sum_i alpha_i models_i (model_average's loop with given weights):
+    a rank's share of the cross-rank average, alpha from the global sync_weights."""
+    n = len(models)
+    arr = (C.c_void_p * n)(*[m.handle.value for m in models])
+    a = np.ascontiguousarray(alpha, np.float64)
+    check(lib.catgnn_model_weighted_sum(n, arr, _ptr(a), dst.handle))
+
+
 class Comm:
     """NCCL communicator, one rank per GPU (C1)."""
 
@@ -226,16 +245,9 @@ def distributed_train(kind, shards: List[Shard], counts, sync_interval: int, epo
         if comm is None:
             model_average(reps, counts, shared)
         else:
-            # C1: sum_i alpha_i theta_i over this rank's replicas, then all-reduce
-            loc = np.ascontiguousarray(counts, np.uint64)
-            if len(reps) == 1:
-                shared.copy_params_from(reps[0])
-                shared.scale(alpha[0])
-            else:
-                # in-process weighted sum with the rank-local alphas
-                tot = sum(alpha)
-                model_average(reps, loc, shared)
-                shared.scale(tot)
+            # C1: sum_i alpha_i theta_i over this rank's replicas with the global
+            # alphas (a rank without train rows contributes zeros), then all-reduce
+            weighted_sum(reps, alpha, shared)
             shared.allreduce(comm)
         done += chunk
         res.averaging_ops += 1
@@ -245,3 +257,37 @@ def distributed_train(kind, shards: List[Shard], counts, sync_interval: int, epo
             res.history.append((done, res.averaging_ops, vf, tf))
     res.params = shared.get_params()
     return res
+
+
+def distributed_train_artifact(artifact_dir: str, kind, epochs: int, sync_interval: int, layers: int = 2,
+                               hidden: int = 256, classes: int = 0, workers: int = 1, seed: int = 0,
+                               optimizer=ADAM, lr: float = 0.01, beta1=0.9, beta2=0.999, eps=1e-8,
+                               eval_global: bool = True, input: str = "", features: str = "",
+                               comm: Optional[Comm] = None, ctx: Optional[Context] = None) -> GNNTrainResult:
+    """catgnn_gnn_distributed_train: the whole loop in the library (C++ host
+    side of the drop-in) on an artifact directory, like train-sim
+    (proj/tools/gnnpart.cpp:310-321 -> distributed_train, train.cpp:289-340)."""
+    ctx = ctx or default_context()
+    k = KINDS[kind] if isinstance(kind, str) else kind
+    cfg = GnnTrainConfig(ModelConfig(k, layers, 0, hidden, classes, optimizer, lr, beta1, beta2, eps, seed),
+                         epochs, sync_interval, workers, int(eval_global))
+    cap_h = epochs // max(sync_interval, 1) + 2
+    he = np.zeros(cap_h, np.uint64); hs = np.zeros(cap_h, np.uint64)
+    hv = np.zeros(cap_h); ht = np.zeros(cap_h)
+    losses = np.zeros(max(epochs, 1))
+    model = C.c_void_p()
+    res = GnnResult(None, 0, 0, losses.ctypes.data, losses.size, 0, he.ctypes.data, hs.ctypes.data,
+                    hv.ctypes.data, ht.ctypes.data, cap_h, 0, 0, 0, 0, C.cast(C.pointer(model), C.c_void_p))
+    check(lib.catgnn_gnn_distributed_train(ctx.handle, str(artifact_dir).encode(), str(input).encode(),
+                                           str(features).encode(), C.byref(cfg),
+                                           comm.handle if comm else None, C.byref(res)))
+    mc = ModelConfig(k, layers, res.in_dim, hidden, res.classes, optimizer, lr, beta1, beta2, eps, seed)
+    m = GNNModel.adopt(model, ctx, mc)
+    params = m.get_params()
+    n = min(res.n_hist, cap_h)
+    hist = [(int(he[i]), int(hs[i]), float(hv[i]), float(ht[i])) for i in range(n)]
+    out = GNNTrainResult(params=params, losses=losses[:res.n_losses].tolist(), history=hist,
+                         averaging_ops=int(res.averaging_ops))
+    out.in_dim, out.classes = int(res.in_dim), int(res.classes)
+    out.model = m
+    return out

@@ -530,10 +530,15 @@ def train_epochs(params, shards, cfg: TrainConfig, epoch_begin: int, epoch_end: 
 
 
 def train_local(shard: Shard, cfg: TrainConfig) -> ModelParams:
-    """train.cpp:130-137 (expects propagated features)."""
-    classes = max(int(shard.labels.max(initial=0)) + 1, 1)
-    p = zero_params(shard.dim, classes)
-    train_epochs(p, shard, cfg, 0, cfg.epochs, cfg.seed)
+    """train.cpp:130-137 via catgnn_train_local: zero_params(dim, max label + 1),
+    then train_epochs over the shard's train rows with cfg.seed, on its
+    features propagated cfg.prop_hops times (train-sim --compare-centralized,
+    gnnpart.cpp:330-335, on the global shard)."""
+    classes = C.c_uint32()
+    check(lib.catgnn_train_local(shard.handle, C.byref(cfg), None, None, C.byref(classes)))
+    p = zero_params(shard.dim, classes.value)
+    check(lib.catgnn_train_local(shard.handle, C.byref(cfg), _ptr(p.weight), _ptr(p.bias), C.byref(classes)))
+    p.epochs_trained = cfg.epochs
     return p
 
 

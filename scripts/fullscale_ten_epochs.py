@@ -8,6 +8,10 @@ model_average).  Output: one JSON line (gpurun_out/fullscale_ten_epochs.json).
 
     python scripts/fullscale_ten_epochs.py [EPOCHS] [WORKLOAD]   (reddit_gcn | products_sage)
 
+The oracle half alone is frozen into tests/golden/fullscale_<workload>.json by
+tests/golden/make_fullscale_fixture.py; tests/test_gpu_fullscale.py runs the B200
+half against that fixture on every GPU test run.
+
 products_sage: eight float64 oracle workers over the 1.3 M-row partitions exceed the
 196 GB of host RAM on this pool's boxes (a worker died after 47 min); only reddit_gcn
 has been run to completion.
@@ -22,8 +26,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-EPOCHS = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-WORKLOAD = sys.argv[2] if len(sys.argv) > 2 else "reddit_gcn"
+EPOCHS = 10
+WORKLOAD = "reddit_gcn"
 SEED, HIDDEN, LR = 7, 256, 0.01
 
 
@@ -39,12 +43,12 @@ def oracle_shard(prep, i):
                           p["labels"].astype(np.int64), train)
 
 
-def worker(prep, i, init_flat, conn):
+def worker(prep, i, init_flat, conn, name):
     from threadpoolctl import threadpool_limits
     threadpool_limits(max(1, (os.cpu_count() or 8) // 8))
     from oracle import gnn_oracle as go
     sh = oracle_shard(prep, i)
-    w = _workload()
+    w = _workload(name)
     kind = _kind(w)
     like = go.init_params(kind, w.layers, sh.X.shape[1], HIDDEN, w.classes, seed=SEED)
     rep = go.Replica(kind, go.unflatten(init_flat, like), lr=LR)
@@ -58,9 +62,9 @@ def worker(prep, i, init_flat, conn):
         conn.send((loss, go.flatten(rep.params)))
 
 
-def _workload():
+def _workload(name=None):
     from paper_2404_02300_b200 import workloads as W
-    return W.WORKLOADS[WORKLOAD]
+    return W.WORKLOADS[name or WORKLOAD]
 
 
 def _kind(w):
@@ -68,56 +72,72 @@ def _kind(w):
     return {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[w.model]
 
 
-def main():
-    from paper_2404_02300_b200 import workloads as W
-    w = _workload()
-    prep = W.prepare(w, lambda *a: None)
-    t0 = time.time()
-    # ---- B200 -------------------------------------------------------------
-    from paper_2404_02300_b200 import gnn, gnnpart as gp
-    ctx = gp.Context(0)
+def load_global(prep):
+    from paper_2404_02300_b200 import workloads as W  # noqa: F401
     X = np.load(os.path.join(prep["dir"], "features.npy"), mmap_mode="r")
     labels = np.load(os.path.join(prep["dir"], "labels.npy"))
     roles = np.load(os.path.join(prep["dir"], "roles.npy"))
+    raw = np.fromfile(os.path.join(prep["dir"], "edges.bin"), dtype=np.uint8)
+    edges = raw[4:].view(np.uint64).reshape(-1, 2)
+    return X, labels, roles, edges
+
+
+def run_gpu(epochs=EPOCHS, name=None):
+    """The B200 half: all partitions through the library (s = 1), then the
+    averaged model's test accuracy on the global graph.  Returns a dict."""
+    from paper_2404_02300_b200 import workloads as W
+    from paper_2404_02300_b200 import gnn, gnnpart as gp
+    w = _workload(name)
+    prep = W.prepare(w, lambda *a: None)
+    t0 = time.time()
+    ctx = gp.Context(0)
+    X, labels, roles, edges = load_global(prep)
     shards, counts = [], []
     for i in range(w.partitions):
         p = W.load_part(prep, i, X, labels)
         shards.append(gp.Shard.from_part(p["ext"], p["owner"], p["role"], p["labels"], p["edges"], p["features"], ctx))
         counts.append(int(np.sum((p["owner"] == 1) & (p["role"] == 1))))
-    res = gnn.distributed_train(w.model, shards, counts, 1, EPOCHS, w.layers, HIDDEN, w.classes, seed=SEED, lr=LR,
+    res = gnn.distributed_train(w.model, shards, counts, 1, epochs, w.layers, HIDDEN, w.classes, seed=SEED, lr=LR,
                                 ctx=ctx)
-    t_gpu = time.time() - t0
+    del shards
     # global graph (the full stream, train.cpp:229-238) for the test accuracy
-    raw = np.fromfile(os.path.join(prep["dir"], "edges.bin"), dtype=np.uint8)
-    edges = raw[4:].view(np.uint64).reshape(-1, 2)
     V = labels.size
     test = np.nonzero(roles == 3)[0]
     gsh = gp.Shard.from_edges(V, edges.astype(np.uint32), np.ascontiguousarray(X, np.float32), ctx)
     m = gnn.GNNModel(w.model, w.layers, w.dim, HIDDEN, w.classes, seed=SEED, ctx=ctx)
     m.set_params(res.params)
     logits, _ = m.forward(gsh, logits=True)
-    acc_gpu = float(np.mean(np.argmax(logits[test], axis=1) == labels[test]))
-    del shards, gsh
-    # ---- float64 oracle, 8 worker processes --------------------------------
+    acc = float(np.mean(np.argmax(logits[test], axis=1) == labels[test]))
+    return dict(losses=list(res.losses), test_acc=acc, test_rows=int(test.size), counts=counts,
+                seconds=round(time.time() - t0, 1), key=w.key(), meta=prep["meta"])
+
+
+def run_oracle(epochs=EPOCHS, name=None):
+    """The float64 oracle half: one worker process per partition (averaging in
+    partition order in the parent, as model_average), then the test accuracy of
+    the averaged model on the global graph."""
     from oracle import gnn_oracle as go
+    from paper_2404_02300_b200 import workloads as W
+    w = _workload(name)
+    prep = W.prepare(w, lambda *a: None)
+    X, labels, roles, edges = load_global(prep)
     kind = _kind(w)
     like = go.init_params(kind, w.layers, w.dim, HIDDEN, w.classes, seed=SEED)
     init_flat = go.flatten(like)
     t1 = time.time()
     ctxm = mp.get_context("fork")
-    pipes, procs = [], []
+    pipes, workers = [], []
     for i in range(w.partitions):
         a, b = ctxm.Pipe()
-        pr = ctxm.Process(target=worker, args=(prep, i, init_flat, b))
+        pr = ctxm.Process(target=worker, args=(prep, i, init_flat, b, w.name))
         pr.start()
         pipes.append(a)
-        procs.append(pr)
-    ocounts = [c.recv() for c in pipes]
-    assert ocounts == counts, (ocounts, counts)
-    alpha = go.sync_weights(ocounts)
+        workers.append(pr)
+    counts = [c.recv() for c in pipes]
+    alpha = go.sync_weights(counts)
     shared = init_flat
     losses = []
-    for _ in range(EPOCHS):
+    for _ in range(epochs):
         for c in pipes:
             c.send(shared)
         out = [c.recv() for c in pipes]
@@ -128,22 +148,35 @@ def main():
         shared = flat
     for c in pipes:
         c.send(None)
-    for pr in procs:
+    for pr in workers:
         pr.join()
-    t_oracle = time.time() - t1
+    V = labels.size
+    test = np.nonzero(roles == 3)[0]
     G = go.Graph.from_csr(*oracle_global_csr(edges, V), V)
     params = go.unflatten(shared, like)
     fl = go.Replica(kind, params).flags(w.dim)
     H, Zs, _ = go.forward(kind, params, G, np.asarray(X, np.float64), fl)
-    acc_oracle = float(np.mean(np.argmax(Zs[-1][test], axis=1) == labels[test]))
-    rel = [abs(a - b) / abs(b) for a, b in zip(res.losses, losses)]
+    acc = float(np.mean(np.argmax(Zs[-1][test], axis=1) == labels[test]))
+    return dict(losses=losses, test_acc=acc, test_rows=int(test.size), counts=counts,
+                seconds=round(time.time() - t1, 1), key=w.key(), meta=prep["meta"])
+
+
+def main():
+    global EPOCHS, WORKLOAD
+    EPOCHS = int(sys.argv[1]) if len(sys.argv) > 1 else EPOCHS
+    WORKLOAD = sys.argv[2] if len(sys.argv) > 2 else WORKLOAD
+    w = _workload()
+    g = run_gpu(EPOCHS)
+    o = run_oracle(EPOCHS)
+    assert o["counts"] == g["counts"], (o["counts"], g["counts"])
+    rel = [abs(a - b) / abs(b) for a, b in zip(g["losses"], o["losses"])]
     line = {"check": f"{w.name} {EPOCHS}-epoch loss and final test accuracy, B200 vs float64 oracle",
             "epochs": EPOCHS, "partitions": w.partitions, "sync_interval": 1, "seed": SEED,
-            "loss_gpu": res.losses, "loss_oracle": losses, "max_rel_loss_err": max(rel),
-            "test_acc_gpu": acc_gpu, "test_acc_oracle": acc_oracle,
-            "acc_diff_pt": 100 * abs(acc_gpu - acc_oracle), "test_rows": int(test.size),
-            "pass": bool(max(rel) <= 1e-3 and 100 * abs(acc_gpu - acc_oracle) <= 0.5),
-            "seconds": {"gpu_incl_load": round(t_gpu, 1), "oracle_8_procs": round(t_oracle, 1)}}
+            "loss_gpu": g["losses"], "loss_oracle": o["losses"], "max_rel_loss_err": max(rel),
+            "test_acc_gpu": g["test_acc"], "test_acc_oracle": o["test_acc"],
+            "acc_diff_pt": 100 * abs(g["test_acc"] - o["test_acc"]), "test_rows": g["test_rows"],
+            "pass": bool(max(rel) <= 1e-3 and 100 * abs(g["test_acc"] - o["test_acc"]) <= 0.5),
+            "seconds": {"gpu_incl_load": g["seconds"], "oracle_procs": o["seconds"]}}
     print(json.dumps(line), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "fullscale_ten_epochs.json"), "w") as f:

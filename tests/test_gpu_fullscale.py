@@ -1,10 +1,19 @@
 """Full-size parity for the bench workloads (BASELINE configs[1] reddit-shaped GCN,
-configs[2] products-shaped 3-layer SAGE): one forward + backward on a whole SPRING
-partition (reddit: 184 k rows, 26 M nnz, 602-d) against the float64 oracle
-(oracle/gnn_oracle.py) — the north
-star's single-step tolerance (2e-3 relative, normwise) at the size bench.py times.
-The CSR the GPU builds is checked bit-exact against the reference's build_adjacency
-on the same partition first."""
+configs[2] products-shaped 3-layer SAGE, configs[3] papers-shaped GIN at 2^24 ids):
+one forward + backward on a whole SPRING partition (reddit: 184 k rows, 26 M nnz,
+602-d; papers_gin_s24: 112 M nnz) against the float64 oracle (oracle/gnn_oracle.py)
+— the north star's single-step tolerance (2e-3 relative, normwise) at the size
+bench.py times.  The CSR the GPU builds is checked bit-exact against the
+reference's build_adjacency on the same partition first.
+
+The north-star acceptance proper — loss within 1e-3 relative over the first 10
+epochs and final test accuracy within 0.5 pt — runs the bench's whole reddit
+workload (8 partitions, s = 1, Adam) on the B200 against the oracle's run frozen in
+tests/golden/fullscale_reddit_gcn.json (tests/golden/make_fullscale_fixture.py)."""
+import json
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -15,7 +24,7 @@ from oracle import ref
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-@pytest.mark.parametrize("workload", ["reddit_gcn", "products_sage"])
+@pytest.mark.parametrize("workload", ["reddit_gcn", "products_sage", "papers_gin_s24"])
 def test_partition_one_step_matches_oracle(workload):
     from paper_2404_02300_b200 import gnnpart as gp, workloads as W
     from paper_2404_02300_b200.gnn import GNNModel
@@ -46,3 +55,20 @@ def test_partition_one_step_matches_oracle(workload):
     print("full-size relative errors:", {k: f"{v:.2e}" for k, v in errs.items()})
     assert errs["loss"] <= 1e-3, errs
     assert all(v < 2e-3 for k, v in errs.items() if k != "loss"), errs
+
+
+def test_ten_epochs_match_frozen_oracle():
+    here = os.path.dirname(os.path.abspath(__file__))
+    fx = json.load(open(os.path.join(here, "golden", "fullscale_reddit_gcn.json")))
+    sys.path.insert(0, os.path.join(os.path.dirname(here), "scripts"))
+    import fullscale_ten_epochs as F
+    from paper_2404_02300_b200 import workloads as W
+    assert W.WORKLOADS["reddit_gcn"].key() == fx["workload_key"]
+    assert (F.SEED, F.HIDDEN, F.LR) == (fx["seed"], fx["hidden"], fx["lr"])
+    g = F.run_gpu(fx["epochs"], "reddit_gcn")
+    # same synthetic graph and partitions as the oracle saw
+    assert g["meta"]["part_rows"] == fx["part_rows"] and g["counts"] == fx["train_counts"]
+    rel = np.abs(np.array(g["losses"]) - np.array(fx["losses"])) / np.abs(np.array(fx["losses"]))
+    print("10-epoch loss rel err", rel.max(), "acc", g["test_acc"], "oracle", fx["test_acc"])
+    assert rel.max() <= 1e-3
+    assert 100 * abs(g["test_acc"] - fx["test_acc"]) <= 0.5
