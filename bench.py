@@ -214,9 +214,13 @@ def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step
 
 def reference_jobs(prep, samples, budget_edges):
     """Bounded samples for the reference CPU path: samples = [(partition,
-    block)]; the partition CSR comes from the reference's own build_adjacency
-    and rows [R0, R1) holding the block-th ~budget_edges local edges keep their
-    neighbour lists (other rows have none, as gather sources only)."""
+    block)].  Each sample is a SELF-CONTAINED row-block subgraph: the rows
+    [R0, R1) holding the block-th ~budget_edges local edges of the partition
+    CSR (the reference's own build_adjacency) keep their neighbour lists, and
+    the rows they gather from are renumbered after them with empty lists — so
+    the reference's per-row loop runs over the sample's rows plus its gather
+    sources only, not over the whole partition (whose other rows' edges the
+    sample does not count)."""
     from oracle import ref
     jobs, csr = [], {}
     for i, blk in samples:
@@ -232,8 +236,16 @@ def reference_jobs(prep, samples, budget_edges):
         blk %= max(1, -(-int(off[rows]) // budget_edges))
         R0 = min(int(np.searchsorted(off, blk * budget_edges)), max(rows - 1, 0))
         R1 = max(R0 + 1, min(int(np.searchsorted(off, (blk + 1) * budget_edges)), rows))
-        off_s = np.clip(off, off[R0], off[R1]) - off[R0]
-        jobs.append((rows, off_s, nb[off[R0]: off[R1]].copy(), int(off[R1] - off[R0])))
+        nbs = nb[off[R0]: off[R1]].astype(np.int64)
+        ns = R1 - R0
+        # compact ids: sampled rows 0..ns-1, then the other gather sources
+        others = np.setdiff1d(np.unique(nbs), np.arange(R0, R1))
+        remap = np.where((nbs >= R0) & (nbs < R1), nbs - R0, ns + np.searchsorted(others, nbs))
+        rows_c = ns + others.size
+        off_c = np.empty(rows_c + 1, np.uint32)
+        off_c[:ns + 1] = (off[R0:R1 + 1] - off[R0]).astype(np.uint32)
+        off_c[ns + 1:] = off_c[ns]
+        jobs.append((rows_c, off_c, remap.astype(np.uint32), int(off[R1] - off[R0]), ns))
     return jobs
 
 
@@ -247,7 +259,7 @@ def cpu_reference_rate(w, jobs, seed=0):
     results = [None] * len(jobs)
 
     def run(j):
-        rows, off_s, nb_s, edges_s = jobs[j]
+        rows, off_s, nb_s, edges_s, _ = jobs[j]
         rng = np.random.default_rng(seed + j)
         t = 0.0
         for wd in widths:
@@ -264,9 +276,10 @@ def cpu_reference_rate(w, jobs, seed=0):
         th.join()
     edges = sum(r[0] for r in results)
     wall = max(r[1] for r in results)
-    sample = (f"reference sgc_propagate (1 hop) over {len(jobs)} row blocks of ~{jobs[0][3]} local edges "
-              f"(distinct rows of the partitions, round-robin), one pass per epoch width {widths}, f64 "
-              f"column-major (Eigen MatrixXd), {len(jobs)} host thread(s), one block each")
+    sample = (f"reference sgc_propagate (1 hop) over {len(jobs)} self-contained row-block subgraph(s) of "
+              f"~{jobs[0][3]} local edges ({jobs[0][4]} rows + {jobs[0][0] - jobs[0][4]} gather-source rows "
+              f"in the first), distinct row blocks of the partitions round-robin, one pass per epoch width "
+              f"{widths}, f64 column-major (Eigen MatrixXd), {len(jobs)} host thread(s), one block each")
     return edges / wall, len(jobs), sample
 
 
@@ -338,7 +351,8 @@ def main():
         raise SystemExit(f"world size {world} (WORLD_SIZE) != --gpus {args.gpus}: launch one rank per GPU")
     if args.impl == "reference":
         if rank == 0:
-            prep = W.prepare(w, log)
+            # NumPy RMAT: the reference arm's process never loads libcatgnn.so
+            prep = W.prepare(w, log, native=False)
             run_reference(args, w, prep)
         return
 

@@ -478,6 +478,11 @@ AggFn pick_kernel(uint32_t w4, bool pre, bool bits, int* lpn_out) {
   // use 8 lanes x 2 float4 (4 neighbours per load instruction)
   if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre, bits); }
   if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre, bits); }
+  // 41-48 floats (the class rows): 4 lanes x 3 float4, 8 neighbours per load
+  // instruction and no idle lanes (8 lanes x 2 float4 leave 4 of 16 slots
+  // empty); bit-mask passes keep 8 lanes (bit words assembled per 8 columns)
+  static const int narrow43 = env_int("CATGNN_AGG_NARROW43", 1);
+  if (narrow43 && w4 > 8 && w4 <= 12 && !bits) { *lpn_out = 4; return pick_pre<3, 4>(pre, bits); }
   if (w4 <= 16) { *lpn_out = 8; return pick_pre<2, 8>(pre, bits); }
   // 129-192 floats (e.g. 172 classes): 16 lanes x 3 float4, two neighbours per
   // load instruction (48 float4 slots instead of 64)

@@ -554,7 +554,12 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
         // 128-byte lines (its lanes own 32 different rows); the ReLU-backward
         // mask is one 32-bit word per row and chunk, and ReLU layers emit the
         // same word for their own backward (bits_out).
-        if (col0 + 32 <= args.N && !e.partial) {
+        // columns this chunk stores through the staging tile: a whole chunk, or
+        // the ragged tail when the caller lets the padding up to store_cols be
+        // written (a multiple of 4 columns)
+        const uint32_t ns = max(args.N, e.store_cols);
+        const uint32_t nc = min(32u, ns - col0);
+        if (!e.partial && (nc == 32 || (e.store_cols && nc % 4 == 0))) {
           const uint32_t mw = mrow ? mw_cur : 0xffffffffu;
           uint32_t bw = 0;
 #pragma unroll
@@ -576,13 +581,23 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
             bw |= ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3)) << (4 * i);
             T[lane * kTileLd4 + i] = o;
           }
+          if (nc < 32) bw &= (1u << nc) - 1u;  // staged columns past the stored ones are not results
           if (e.bits_out && row_ok) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
           __syncwarp();
+          if (nc == 32) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t rr = 4 * i + r8, grow = rbase + rr;
-            if (grow < args.M)
-              reinterpret_cast<float4*>(e.out + (size_t)grow * e.ld_out + e.out_col + col0)[c4] = T[rr * kTileLd4 + c4];
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t rr = 4 * i + r8, grow = rbase + rr;
+              if (grow < args.M)
+                reinterpret_cast<float4*>(e.out + (size_t)grow * e.ld_out + e.out_col + col0)[c4] = T[rr * kTileLd4 + c4];
+            }
+          } else {  // ragged tail: nc/4 float4 per row, consecutive lanes along the row
+            const uint32_t n4 = nc / 4;
+            for (uint32_t f = lane; f < 32 * n4; f += 32) {
+              const uint32_t rr = f / n4, cc = f % n4, grow = rbase + rr;
+              if (grow < args.M)
+                reinterpret_cast<float4*>(e.out + (size_t)grow * e.ld_out + e.out_col + col0)[cc] = T[rr * kTileLd4 + cc];
+            }
           }
           __syncwarp();
           continue;
@@ -720,6 +735,8 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   GemmEpi epi = epi_in;
   if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
   if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  if (epi.store_cols && (epi.store_cols % 4 || epi.store_cols < N || epi.out_col + epi.store_cols > epi.ld_out))
+    throw ConfigError("GEMM store_cols must be a multiple of 4 in [N, ld_out - out_col]");
   if (K == 0) {  // empty contraction: the epilogue of a zero accumulator
     const uint64_t total = (uint64_t)M * N;
     unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
@@ -982,5 +999,32 @@ extern "C" int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K
     gemm_tn(ctx, dA, lda, dB, lda, M, N, K, e, split_k, precision);
     CG_CUDA(cudaMemcpy2DAsync(Cout, N * 4, dC, ldc * 4, N * 4, M, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// Diagnostics hook (scripts/gemm_micro.py): one K3 GEMM on caller-owned DEVICE
+// buffers, enqueued on ctx's stream without a host sync (timed by the caller
+// with events on that stream).  Not part of the drop-in boundary.
+extern "C" int catgnn_debug_gemm_dev(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
+                                     uint32_t lda, int a_mn, const float* B, uint32_t ldb, int b_mn, float* C,
+                                     uint32_t ldc, uint32_t split_k, int precision, const float* rowscale,
+                                     const float* bias, int relu, const uint32_t* mask_bits, uint32_t mask_words,
+                                     uint32_t* bits_out, uint32_t bits_words, uint32_t store_cols) {
+  using namespace catgnn;
+  return guarded([&] {
+    if (!ctx) throw ConfigError("null context");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    GemmEpi e{};
+    e.store_cols = store_cols;
+    e.out = C;
+    e.ld_out = ldc;
+    e.rowscale = rowscale;
+    e.bias = bias;
+    e.relu = relu;
+    e.mask_bits = mask_bits;
+    e.mask_words = mask_words;
+    e.bits_out = bits_out;
+    e.bits_words = bits_words;
+    gemm(ctx, GemmOperand{A, lda, a_mn != 0}, GemmOperand{B, ldb, b_mn != 0}, M, N, K, e, split_k, precision);
   });
 }

@@ -19,6 +19,11 @@ struct GemmEpi {
   uint32_t mask_words = 0;
   uint32_t* bits_out = nullptr;
   uint32_t bits_words = 0;
+  // columns [N, store_cols) of the output rows are padding the caller wants
+  // written with the epilogue of a zero accumulator (zero when bias is
+  // zero-padded): lets a ragged last 32-column chunk (N = 41 classes) use the
+  // staged, line-coalesced stores; 0 = write only [0, N)
+  uint32_t store_cols = 0;
   float* partial = nullptr;  // internal (split-K workspace)
 };
 

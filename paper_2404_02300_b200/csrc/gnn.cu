@@ -495,11 +495,13 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       aggregate(S, a);
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
       e.bits_out = b.bits; e.bits_words = b.bits_words;
+      if (!L.out_in_next_mid) e.store_cols = b.out_ld;  // zero padding (bias is zero-padded)
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN transform-first
       b.mid_ld = L.ld_act;
       b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
       GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld; e.rowscale = gcn ? S->dinv.p : nullptr;
+      e.store_cols = b.mid_ld;  // the padding of T is zero either way: staged stores for the ragged tail
       gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;

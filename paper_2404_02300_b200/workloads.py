@@ -94,8 +94,12 @@ def cache_dir(w: Workload) -> str:
     return d
 
 
-def prepare(w: Workload, log=print) -> dict:
-    """Builds (or loads) the partitioned dataset; returns a dict of arrays/metadata."""
+def prepare(w: Workload, log=print, native: bool = True) -> dict:
+    """Builds (or loads) the partitioned dataset; returns a dict of arrays/metadata.
+    native=False generates the RMAT stream with the NumPy statement
+    (synth.rmat_edges_numpy, bit-identical to the C++ generator) so a process
+    that must not load libcatgnn.so (bench.py --impl reference) can build the
+    cache."""
     d = cache_dir(w)
     meta_path = os.path.join(d, "meta.json")
     if os.path.exists(meta_path):
@@ -104,7 +108,10 @@ def prepare(w: Workload, log=print) -> dict:
         log(f"[prep] cached {d}")
         return dict(meta=meta, dir=d)
     t0 = time.time()
-    e, n, _ = synth.rmat_edges(w.scale, w.edges, seed=w.seed)
+    if native:
+        e, n, _ = synth.rmat_edges(w.scale, w.edges, seed=w.seed)
+    else:
+        e, n, _ = synth.rmat_edges_numpy(w.scale, w.edges, seed=w.seed)
     t1 = time.time()
     edge_file = os.path.join(d, "edges.bin")
     with open(edge_file, "wb") as f:
@@ -115,7 +122,7 @@ def prepare(w: Workload, log=print) -> dict:
     t2 = time.time()
     labels, roles = synth.node_meta(n, w.classes, *w.fracs, seed=w.seed)
     parts = None
-    if w.edges >= 100_000_000:
+    if w.edges >= 100_000_000 and native:
         # device completion (csrc/completion.cu, bit-exact with the reference) when a GPU is here
         try:
             import torch
