@@ -255,7 +255,7 @@ class TrainingData:
                                            C.byref(a), C.byref(b_), C.byref(c_)))
             dim = dd.value
         W = np.zeros((dim, classes)); b = np.zeros(classes)
-        cap = (epochs + sync_interval - 1) // sync_interval + 1
+        cap = (epochs + max(sync_interval, 1) - 1) // max(sync_interval, 1) + 1
         he = np.zeros(cap, np.uint64); hs = np.zeros(cap, np.uint64)
         hv = np.zeros(cap); ht = np.zeros(cap)
         dim_o = C.c_uint32(); cls_o = C.c_uint32(); nh = C.c_uint64(); ops = C.c_uint64()

@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
            "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-3, "usecond": 1,
-         "msecond": 1e3, "second": 1e6, "%": 1, "": 1}
+         "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6, "%": 1, "": 1}
 
 
 def compulsory_bytes(nnz, rows, width, self_term):
@@ -42,13 +42,14 @@ def main():
     w = W.WORKLOADS[workload]
     prep = W.prepare(w, lambda *a: None)
     meta = prep["meta"]
-    log = os.path.join(ROOT, "gpurun_out", f"k2_traffic_{workload}.csv")
-    os.makedirs(os.path.dirname(log), exist_ok=True)
-    env = dict(os.environ, CATGNN_WORKLOAD=workload)
-    cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:agg_", "--csv",
-           "--log-file", log, sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1",
-           "--graph", "0", "--no-e2e", "--no-cpu-baseline"]
-    subprocess.run(cmd, env=env, check=True, stdout=subprocess.DEVNULL)
+    log = os.environ.get("K2_TRAFFIC_CSV") or os.path.join(ROOT, "gpurun_out", f"k2_traffic_{workload}.csv")
+    if not os.environ.get("K2_TRAFFIC_CSV"):  # else: re-summarise an existing capture
+        os.makedirs(os.path.dirname(log), exist_ok=True)
+        env = dict(os.environ, CATGNN_WORKLOAD=workload)
+        cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:agg_", "--csv",
+               "--log-file", log, sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1",
+               "--graph", "0", "--no-e2e", "--no-cpu-baseline"]
+        subprocess.run(cmd, env=env, check=True, stdout=subprocess.DEVNULL)
     launches = {}
     with open(log) as f:
         text = f.read()
