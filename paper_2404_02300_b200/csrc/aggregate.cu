@@ -478,17 +478,9 @@ AggFn pick_kernel(uint32_t w4, bool pre, bool bits, int* lpn_out) {
   // use 8 lanes x 2 float4 (4 neighbours per load instruction)
   if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre, bits); }
   if (w4 <= 8) { *lpn_out = 8; return pick_pre<1, 8>(pre, bits); }
-  // 41-48 floats (the class rows): 4 lanes x 3 float4, 8 neighbours per load
-  // instruction and no idle lanes (8 lanes x 2 float4 leave 4 of 16 slots
-  // empty); bit-mask passes keep 8 lanes (bit words assembled per 8 columns)
-  static const int narrow43 = env_int("CATGNN_AGG_NARROW43", 1);
-  if (narrow43 && w4 > 8 && w4 <= 12 && !bits) { *lpn_out = 4; return pick_pre<3, 4>(pre, bits); }
   if (w4 <= 16) { *lpn_out = 8; return pick_pre<2, 8>(pre, bits); }
   // 129-192 floats (e.g. 172 classes): 16 lanes x 3 float4, two neighbours per
   // load instruction (48 float4 slots instead of 64)
-  // 128-float slabs: 16 lanes x 2 float4, two neighbours per load instruction
-  static const int w128_16 = env_int("CATGNN_AGG_W128_16", 0);
-  if (w128_16 && w4 == 32 && !bits) { *lpn_out = 16; return pick_pre<2, 16>(pre, bits); }
   static const int mid16 = env_int("CATGNN_AGG_MID16", 1);
   if (mid16 && w4 > 32 && w4 <= 48) { *lpn_out = 16; return pick_pre<3, 16>(pre, bits); }
   *lpn_out = 32;
@@ -546,13 +538,8 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
   if (a.in == a.out && a.in && a.in_ld != a.out_ld) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
   const uint32_t W4 = a.width / 4;
-  // CATGNN_AGG_SLAB (float4 units, multiple of 8): column slabs per launch — A/B
-  // knob for gathered operands larger than L2 (e.g. 32 = two 128-float halves
-  // of a 256-wide pass, each half's 94 MB of rows L2-resident)
-  static const uint32_t slab_env = (uint32_t)std::max(0, env_int("CATGNN_AGG_SLAB", 0));
-  const uint32_t slab4 = (slab_env >= 8 && slab_env % 8 == 0) ? std::min(slab_env, kMaxSlab4) : kMaxSlab4;
-  for (uint32_t c4 = 0; c4 < W4; c4 += slab4) {
-    const uint32_t w4 = std::min(slab4, W4 - c4);
+  for (uint32_t c4 = 0; c4 < W4; c4 += kMaxSlab4) {
+    const uint32_t w4 = std::min(kMaxSlab4, W4 - c4);
     AggKernelArgs p{};
     p.row_ptr = s->row_ptr.p;
     p.col = s->col.p;

@@ -40,22 +40,35 @@ def main():
         t0 = time.perf_counter()
         ref.sgc_propagate_colmajor(off, nb, x, rows, wd, 1)
         full[wd] = nnz / (time.perf_counter() - t0)
-    # bench.py's estimate: self-contained samples of ~300k edges, one at a time on one core
+    # bench.py's estimate: self-contained samples of ~300k edges on one core
+    # (cpu_reference_rate with one job at a time: raw and gather-source-corrected)
     nblk = 4
     jobs = bench.reference_jobs(prep, [(part, b * 17) for b in range(nblk)], 300_000)
-    est = {}
+
+    class One:  # this partition's schedule restricted to one width
+        def __init__(self, wd):
+            self.wd = wd
+
+        def passes(self):
+            return [self.wd]
+    est, raw = {}, {}
     for wd in widths:
-        es, ts = 0, 0.0
-        for rows_c, off_c, nb_c, e_s, _ in jobs:
-            x = np.random.default_rng(wd + 1).standard_normal(rows_c * wd)
-            t0 = time.perf_counter()
-            ref.sgc_propagate_colmajor(off_c, nb_c, x, rows_c, wd, 1)
-            ts += time.perf_counter() - t0
-            es += e_s
-        est[wd] = es / ts
+        es = tc = tr = 0.0
+        for jb in jobs:
+            rate, _, sample = bench.cpu_reference_rate(One(wd), [jb])
+            e = jb[3]
+            es += e
+            tc += e / rate
+            tr += e / float(sample.rsplit("uncorrected ", 1)[1].split()[0])
+        est[wd] = es / tc
+        raw[wd] = es / tr
     line = {"workload": workload, "partition": part, "rows": rows, "nnz": nnz,
-            "full_pass_edges_per_s": full, "sampled_edges_per_s": est,
+            "full_pass_edges_per_s": full, "sampled_edges_per_s": est, "sampled_uncorrected_edges_per_s": raw,
             "sample_over_full": {wd: est[wd] / full[wd] for wd in widths},
+            "uncorrected_over_full": {wd: raw[wd] / full[wd] for wd in widths},
+            # one epoch's passes of the workload (edges x passes / summed time), as bench.py reports
+            "epoch_sample_over_full": (sum(1 / full[wd] for wd in W.WORKLOADS[workload].passes() if wd in full) /
+                                       sum(1 / est[wd] for wd in W.WORKLOADS[workload].passes() if wd in est)),
             "note": "1 core each; reference sgc_propagate (f64 column-major Eigen via oracle/_ref); the sampled "
                     "rate is what bench.py's cpu_baseline / --impl reference extrapolate from"}
     print(json.dumps(line), flush=True)
