@@ -403,7 +403,9 @@ int catgnn_model_allreduce(catgnn_model m, catgnn_comm c);
 int catgnn_gemm_tn(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A,
                    const float* B, float* C, uint32_t split_k, int precision);
 /* General form: A given as M x K (a_mn = 0) or K x M (a_mn = 1, read MN-major
- * by the tensor core), B as N x K or K x N; C[M x N] = A . B^T. */
+ * by the tensor core), B as N x K or K x N; C[M x N] = A . B^T.  precision 4 =
+ * bf16x3: both operands split on the device into bf16 (hi, lo) pairs and
+ * multiplied as lo*hi + hi*lo + hi*hi with kind::f16 MMAs (~2^-16 relative). */
 int catgnn_gemm(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const float* A, int a_mn,
                 const float* B, int b_mn, float* C, uint32_t split_k, int precision);
 /* Synthetic RMAT(a,b,c,1-a-b-c) stream of num_edges unique undirected pairs, no

@@ -24,6 +24,8 @@
 #include <mutex>
 #include <string>
 
+#include <cuda_bf16.h>
+
 #include "shard.hpp"
 
 namespace catgnn {
@@ -57,6 +59,9 @@ struct AggKernelArgs {
   uint32_t mask_words;                     // 32-bit words per row
   uint32_t* __restrict__ bits_out;         // output > 0 bits (forward ReLU layers)
   uint32_t bits_words;
+  uint2* __restrict__ out_hi;  // bf16x3 output pair (4 bf16 per float4 column group)
+  uint2* __restrict__ out_lo;
+  uint32_t out_s_ld;           // in bf16 elements
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -134,9 +139,19 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
       a.z = (m & 4u) ? a.z : 0.f; a.w = (m & 8u) ? a.w : 0.f;
     }
     if (BITS) nib[q] = (a.x > 0.f) | ((a.y > 0.f) << 1) | ((a.z > 0.f) << 2) | ((a.w > 0.f) << 3);
-    float4* dst = reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4);
-    if (p.stream_hint) __stcs(dst, a);  // evict-first: keep L2 for the gathered rows
-    else *dst = a;
+    if (p.out) {
+      float4* dst = reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4);
+      if (p.stream_hint) __stcs(dst, a);  // evict-first: keep L2 for the gathered rows
+      else *dst = a;
+    }
+    if (p.out_hi) {  // hi = bf16(v), lo = bf16(v - hi): the next GEMM's pre-split operand
+      const __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+      const __nv_bfloat162 l0 = __floats2bfloat162_rn(a.x - __low2float(h0), a.y - __high2float(h0));
+      const __nv_bfloat162 l1 = __floats2bfloat162_rn(a.z - __low2float(h1), a.w - __high2float(h1));
+      const size_t o = ((size_t)r * p.out_s_ld + c4 * 4) / 4;
+      p.out_hi[o] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+      p.out_lo[o] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+    }
   }
   if (BITS && p.bits_out) {  // 1 bit per output element (> 0): the next backward's ReLU mask
 #pragma unroll
@@ -537,6 +552,9 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     throw ConfigError("aggregation cannot run in place");
   if (a.in == a.out && a.in && a.in_ld != a.out_ld) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
+  if (!a.out && !a.out_hi) throw ConfigError("aggregation needs an output");
+  if (a.out_hi && (!a.out_lo || a.out_s_ld % 8 || a.out_s_ld < a.width))
+    throw ConfigError("bf16 aggregation output needs hi and lo rows of >= width elements, a multiple of 8");
   const uint32_t W4 = a.width / 4;
   for (uint32_t c4 = 0; c4 < W4; c4 += kMaxSlab4) {
     const uint32_t w4 = std::min(kMaxSlab4, W4 - c4);
@@ -572,6 +590,9 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.mask_words = a.mask_words;
     p.bits_out = a.bits_out ? a.bits_out + c4 / 8 : nullptr;
     p.bits_words = a.bits_words;
+    p.out_hi = a.out_hi ? reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.out_hi) + c4 * 4) : nullptr;
+    p.out_lo = a.out_lo ? reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.out_lo) + c4 * 4) : nullptr;
+    p.out_s_ld = a.out_s_ld;
     static const int hint = env_int("CATGNN_AGG_HINT", 1);
     p.stream_hint = hint;
     int lpn = 32;

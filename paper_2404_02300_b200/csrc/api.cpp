@@ -111,6 +111,7 @@ void h2d(T* dst, const T* src, size_t n, cudaStream_t st) {
 // runs at a fraction of it), then an on-device re-pitch when dim % 4 != 0.
 void copy_features_in(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   cudaStream_t st = s->ctx->stream;
+  s->x_version++;  // the bf16x3 copy (gnn.cu) is re-split on next use
   const size_t bytes = s->rows * (size_t)dim * sizeof(float);
   if (s->ld == dim) {
     CG_CUDA(cudaMemcpyAsync(s->x.p, feats, bytes, cudaMemcpyHostToDevice, st));
@@ -126,6 +127,7 @@ void upload_features(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   s->dim = dim;
   s->ld = round_up(std::max<uint32_t>(dim, 1), 4);
   s->x.alloc(std::max<uint64_t>(1, s->rows) * s->ld);
+  s->x_version++;
   s->xprop.release();
   if (s->rows == 0 || dim == 0) return;
   if (s->ld != dim) CG_CUDA(cudaMemsetAsync(s->x.p, 0, s->x.bytes(), s->ctx->stream));

@@ -189,6 +189,7 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
     if (s->rows && s->ext_max >= f->rows)  // train.cpp:279-281
       throw DataError("feature row " + std::to_string(s->ext_max) + " out of range of the feature store");
     const uint32_t ld = round_up(f->dim, 4);
+    s->x_version++;  // the bf16x3 copy (gnn.cu) is re-split on next use
     if (s->dim != f->dim || !s->x.p) {
       s->dim = f->dim;
       s->ld = ld;

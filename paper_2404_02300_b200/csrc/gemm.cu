@@ -59,6 +59,7 @@ constexpr size_t epi_smem(int epiw) { return (size_t)epiw * 32 * kTileLd4 * 16; 
 struct GemmArgs {
   uint32_t M, N, K;
   uint32_t BN;
+  uint32_t bk;        // K elements per k-block (stage): 32 fp32 / 64 bf16 = 128-byte rows
   uint32_t stages;
   uint32_t lo_slots;  // 3xTF32: ring of lo (residual) tile slots, decoupled from the TMA stages
   uint32_t kb_per_split;
@@ -163,6 +164,19 @@ __device__ __forceinline__ uint64_t umma_desc_mn(uint32_t addr) {
          (1ull << 61);
 }
 
+// MN-major 16-bit operands (bf16x3 path): canonical SWIZZLE_128B layout —
+// 64-element (128 B) atoms along M/N, one {64 x 64} TMA box each, LBO = 8 KB
+// between M/N atoms, SBO = 1 KB between 8-row K groups; one MMA (K = 16) spans
+// two K groups, so k-steps advance 2 KB.
+__device__ __forceinline__ uint64_t umma_desc_mn16(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | (512ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// descriptor of k-step ks (K = 16 bf16) of a bf16 stage tile (K-major rows of
+// 64 elements = 128 B, SWIZZLE_128B: +32 B per k-step as for tf32)
+__device__ __forceinline__ uint64_t op_desc16(uint32_t base, int ks, bool mn) {
+  return mn ? umma_desc_mn16(base + ks * 2048) : umma_desc(base + ks * 32);
+}
+
 // descriptor of k-step ks (K = 8 elements) of a stage tile in either layout
 __device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks, bool mn) {
   return mn ? umma_desc_mn(base + ks * 1024) : umma_desc(base + ks * 32);
@@ -181,6 +195,34 @@ __device__ __forceinline__ void load_operand(uint32_t dst, const CUtensorMap* ma
       if (policy) tma_load_2d_hint(dst + a * 4096, map, r0 + (int)(32 * a), k0, bar, policy);
       else tma_load_2d(dst + a * 4096, map, r0 + (int)(32 * a), k0, bar);
     }
+  }
+}
+
+// bf16 x bf16 -> f32 (kind::f16, K = 16 per instruction)
+template <int NCTA>
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  if (NCTA == 2)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// TMA fill of one bf16 operand half (hi or lo) of a stage: K-major = one
+// {64 x rows} box; MN-major = rows/64 boxes of {64 (M/N) x 64 (K)} 8 KB apart.
+__device__ __forceinline__ void load_operand16(uint32_t dst, const CUtensorMap* map, bool mn, int k0, int r0,
+                                               uint32_t rows, uint32_t bar) {
+  if (!mn) {
+    tma_load_2d(dst, map, k0, r0, bar);
+  } else {
+    for (uint32_t a = 0; a < rows / 64; ++a) tma_load_2d(dst + a * 8192, map, r0 + (int)(64 * a), k0, bar);
   }
 }
 
@@ -281,7 +323,7 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, uint32_t t, uint3
   const uint32_t n = t % a.nt, m = (t / a.nt) % a.mt, z = t / (a.nt * a.mt);
   m0 = m * a.bm;
   n0 = n * a.BN;
-  const uint32_t nkb_total = (a.K + BK - 1) / BK;
+  const uint32_t nkb_total = (a.K + a.bk - 1) / a.bk;
   kb0 = z * a.kb_per_split;
   const uint32_t kb1 = min(nkb_total, kb0 + a.kb_per_split);
   nkb = kb1 > kb0 ? kb1 - kb0 : 0;
@@ -334,19 +376,27 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // Pair protocol: full[s] / empty[s] are per CTA (local TMA, multicast MMA
 // commit); conv[s] and tempty[b] live in the rank-0 CTA and count the arrivals
 // of both CTAs' converter / epilogue warps; tfull[b] is multicast.
-template <int NCTA, int EPIW>
+// BF = true: the bf16x3 path — operands arrive pre-split as bf16 (hi, lo)
+// pairs (tmA / tmAl, tmB / tmBl), each stage holds the hi and lo halves of A
+// and B (64 K-elements = 128-byte rows), the MMA warp issues lo*hi + hi*lo +
+// hi*hi with kind::f16 (K = 16) and no converter pass exists (the converter
+// warps only relay "stage ready" in a CTA pair).
+template <int NCTA, int EPIW, bool BF>
 __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmBl, const GemmArgs args) {
+                     const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmAl,
+                     const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t BN = args.BN;
   const uint32_t BNh = BN / NCTA;  // B rows (N) held by this CTA
-  const uint32_t B_STAGE = BNh * BK * 4;
+  const uint32_t B_STAGE = BNh * BK * 4;  // BNh rows of 128 B (bf16: one of the two halves)
+  const uint32_t A_STG = BF ? 2 * A_STAGE : A_STAGE;  // stage strides: bf16 stages hold hi and lo
+  const uint32_t B_STG = BF ? 2 * B_STAGE : B_STAGE;
   const uint32_t S = args.stages;
   const bool split3 = args.split3 != 0;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)S * A_STAGE;
+  uint8_t* sB = smem + (size_t)S * A_STG;
   // 3xTF32 residual tiles (same swizzled layout) in a ring of L slots: the
   // converters of stage `it` write slot it % L once the MMAs of stage it - L
   // have drained it, so the TMA ring keeps S full stages in flight with only L
@@ -356,7 +406,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
   // (sBt[s]); the converters then only split A.
   const uint32_t L = split3 ? args.lo_slots : 0;
   const bool blt = split3 && args.b_lo_tma;
-  uint8_t* sBt = sB + (size_t)S * B_STAGE;
+  uint8_t* sBt = sB + (size_t)S * B_STG;
   uint8_t* sAl = sBt + (blt ? (size_t)S * B_STAGE : 0);
   uint8_t* sBl = sAl + (size_t)L * A_STAGE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sBl + (blt ? 0 : (size_t)L * B_STAGE));
@@ -412,7 +462,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = A_STAGE + B_STAGE * (blt ? 2 : 1);
+      const uint32_t bytes = BF ? A_STG + B_STG : A_STAGE + B_STAGE * (blt ? 2 : 1);
       const uint64_t ef = policy_evict_first();
       const uint64_t pol_a = args.a_stream ? ef : 0, pol_b = args.b_stream ? ef : 0;
       uint32_t it = 0;
@@ -425,10 +475,19 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(smem_u32(empty + s), ph ^ 1, 0);
           mbar_expect_tx(smem_u32(full + s), bytes);
-          const int kx = (int)((kb0 + i) * BK);
-          load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s), pol_a);
-          load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), pol_b);
-          if (blt) load_operand(smem_u32(sBt + (size_t)s * B_STAGE), &tmBl, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), 0);
+          const int kx = (int)((kb0 + i) * args.bk);
+          if constexpr (BF) {
+            const uint32_t fb = smem_u32(full + s);
+            const uint32_t a0 = smem_u32(sA + (size_t)s * A_STG), b0 = smem_u32(sB + (size_t)s * B_STG);
+            load_operand16(a0, &tmA, args.a_mn, kx, (int)m0, BM, fb);
+            load_operand16(a0 + A_STAGE, &tmAl, args.a_mn, kx, (int)m0, BM, fb);
+            load_operand16(b0, &tmB, args.b_mn, kx, (int)n0, BNh, fb);
+            load_operand16(b0 + B_STAGE, &tmBl, args.b_mn, kx, (int)n0, BNh, fb);
+          } else {
+            load_operand(smem_u32(sA + (size_t)s * A_STAGE), &tmA, args.a_mn, kx, (int)m0, BM, smem_u32(full + s), pol_a);
+            load_operand(smem_u32(sB + (size_t)s * B_STAGE), &tmB, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), pol_b);
+            if (blt) load_operand(smem_u32(sBt + (size_t)s * B_STAGE), &tmBl, args.b_mn, kx, (int)n0, BNh, smem_u32(full + s), 0);
+          }
         }
       }
     }
@@ -447,8 +506,19 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
           const uint32_t s = it % S, ph = (it / S) & 1;
           mbar_wait(smem_u32(via_conv ? conv + s : full + s), ph, 2);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = smem_u32(sA + (size_t)s * A_STAGE);
-          const uint32_t b0 = smem_u32(sB + (size_t)s * B_STAGE);
+          const uint32_t a0 = smem_u32(sA + (size_t)s * A_STG);
+          const uint32_t b0 = smem_u32(sB + (size_t)s * B_STG);
+          if constexpr (BF) {  // small terms first: lo*hi, hi*lo, then hi*hi
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {  // K = 16 bf16 (32 bytes) per instruction
+              const uint32_t first = (i > 0 || ks > 0) ? 1u : 0u;
+              mma_bf16<NCTA>(acc, op_desc16(a0 + A_STAGE, ks, amn), op_desc16(b0, ks, bmn), args.idesc, first);
+              mma_bf16<NCTA>(acc, op_desc16(a0, ks, amn), op_desc16(b0 + B_STAGE, ks, bmn), args.idesc, 1u);
+              mma_bf16<NCTA>(acc, op_desc16(a0, ks, amn), op_desc16(b0, ks, bmn), args.idesc, 1u);
+            }
+            commit_to<NCTA>(smem_u32(empty + s));
+            continue;
+          }
           const uint32_t lj = split3 ? it % L : 0;
           const uint32_t al = smem_u32(sAl + (size_t)lj * A_STAGE);
           const uint32_t bl = blt ? smem_u32(sBt + (size_t)s * B_STAGE) : smem_u32(sBl + (size_t)lj * B_STAGE);
@@ -831,6 +901,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   args.kb_per_split = kbps;
   args.tmem_cols = pow2_cols(2 * round_up(BN, 32));  // two accumulator buffers
   args.split3 = split3 ? 1u : 0u;
+  args.bk = BK;
   args.mt = mt;
   args.nt = nt;
   args.splits = splits;
@@ -877,8 +948,8 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   // cudaFuncSetAttribute is per device: one flag set per device ordinal
   static std::mutex attr_mu;
   static std::map<int, std::array<bool, 4>> attr_set;
-  auto kern = pair ? (epiw == 8 ? gemm_tf32_kernel<2, 8> : gemm_tf32_kernel<2, 4>)
-                   : (epiw == 8 ? gemm_tf32_kernel<1, 8> : gemm_tf32_kernel<1, 4>);
+  auto kern = pair ? (epiw == 8 ? gemm_tf32_kernel<2, 8, false> : gemm_tf32_kernel<2, 4, false>)
+                   : (epiw == 8 ? gemm_tf32_kernel<1, 8, false> : gemm_tf32_kernel<1, 4, false>);
   const int kThreads = epiw == 8 ? threads_for<8>() : threads_for<4>();
   {
     std::lock_guard<std::mutex> lk(attr_mu);
@@ -907,9 +978,208 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     cfg.stream = ctx->stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tbl, args));
+    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tbl, ta, args));
   } else {
-    kern<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, tbl, args);
+    kern<<<grid, kThreads, smem, ctx->stream>>>(ta, tb, tbl, ta, args);
+  }
+  CG_CHECK_LAUNCH();
+  ctx->launches++;
+  if (splits > 1) {
+    const uint64_t total = (uint64_t)M * N;
+    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
+    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(partial, splits, M, N, epi);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  ctx->end_timed(t);
+}
+
+namespace {
+
+CUtensorMap make_map16(const __nv_bfloat16* ptr, uint64_t rows, uint64_t K, uint32_t ld, uint32_t box_rows) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16)
+    throw ConfigError("bf16 GEMM operand must be 16-byte aligned with a row stride multiple of 8 elements");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(ptr), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw InternalError("cuTensorMapEncodeTiled (bf16) failed: " + std::to_string((int)r));
+  return m;
+}
+
+// MN-major bf16 operand stored [K rows][MN cols]: {64 (MN) x 64 (K)} boxes, 128-byte
+// inner rows, SWIZZLE_128B; OOB zero-filled.
+CUtensorMap make_map16_mn(const __nv_bfloat16* ptr, uint64_t mn, uint64_t K, uint32_t ld) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16)
+    throw ConfigError("bf16 GEMM operand must be 16-byte aligned with a row stride multiple of 8 elements");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {mn, K};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(ptr), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw InternalError("cuTensorMapEncodeTiled (bf16, MN-major) failed: " + std::to_string((int)r));
+  return m;
+}
+
+// hi = bf16(x) (round to nearest), lo = bf16(x - hi): x = hi + lo to ~2^-17
+__global__ void split_bf16_kernel(const float* __restrict__ in, uint32_t ld_in, uint64_t rows, uint32_t cols,
+                                  __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo, uint32_t ld_out) {
+  const uint32_t q = ld_out / 2;  // bf16 pairs per output row
+  const uint64_t total = rows * q;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / q;
+    const uint32_t c = (uint32_t)(i % q) * 2;
+    const float x0 = c < cols ? in[r * ld_in + c] : 0.f;
+    const float x1 = c + 1 < cols ? in[r * ld_in + c + 1] : 0.f;
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - __low2float(h), x1 - __high2float(h));
+    reinterpret_cast<__nv_bfloat162*>(hi + r * ld_out)[c / 2] = h;
+    reinterpret_cast<__nv_bfloat162*>(lo + r * ld_out)[c / 2] = l;
+  }
+}
+
+}  // namespace
+
+void split_bf16(catgnn_ctx ctx, const float* in, uint32_t ld_in, uint64_t rows, uint32_t cols, __nv_bfloat16* hi,
+                __nv_bfloat16* lo, uint32_t ld_out) {
+  if (ld_out % 2 || cols > ld_out) throw ConfigError("split_bf16: output stride must be even and >= cols");
+  const uint64_t total = rows * (ld_out / 2);
+  if (!total) return;
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)ctx->num_sms * 16));
+  split_bf16_kernel<<<g, 256, 0, ctx->stream>>>(in, ld_in, rows, cols, hi, lo, ld_out);
+  CG_CHECK_LAUNCH();
+  ctx->launches++;
+}
+
+void gemm_bf16x3(catgnn_ctx ctx, SplitOperand a, SplitOperand b, uint32_t M, uint32_t N, uint32_t K,
+                 const GemmEpi& epi_in, uint32_t split_k) {
+  if (M == 0 || N == 0) return;
+  GemmEpi epi = epi_in;
+  if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
+  if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  if (epi.store_cols && (epi.store_cols % 4 || epi.store_cols < N || epi.out_col + epi.store_cols > epi.ld_out))
+    throw ConfigError("GEMM store_cols must be a multiple of 4 in [N, ld_out - out_col]");
+  if (K == 0) {
+    const uint64_t total = (uint64_t)M * N;
+    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
+    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(nullptr, 0, M, N, epi);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+    return;
+  }
+  constexpr uint32_t BKE = 64;  // bf16 elements per k-block (128-byte rows)
+  static const int pair_env = [] {
+    const char* v = std::getenv("CATGNN_GEMM_PAIR");
+    return v ? std::atoi(v) : 1;
+  }();
+  const bool pair = pair_env != 0 && M >= 256 && N >= 128;
+  const uint32_t ncta = pair ? 2 : 1;
+  // per-CTA B rows: whole 8-row swizzle groups (K-major) or 64-wide atoms (MN-major)
+  const uint32_t bn_q = (b.mn_major ? 64 : 16) * ncta;
+  const uint32_t BN = N >= 256 ? 256 : round_up(N, bn_q);
+  const uint32_t BNh = BN / ncta;
+  const uint32_t nkb = (K + BKE - 1) / BKE;
+  const uint32_t bm = BM * ncta;
+  const uint32_t mt = (M + bm - 1) / bm, nt = (N + BN - 1) / BN;
+  const uint32_t gsms = ctx->gemm_sms ? std::max<uint32_t>(ncta, (uint32_t)ctx->gemm_sms) : (uint32_t)ctx->num_sms;
+  const uint32_t units = gsms / ncta;
+  uint32_t splits = 1;
+  if (split_k == 0) {
+    const uint32_t tiles = mt * nt;
+    if (tiles < units && nkb >= 8) splits = std::min<uint32_t>(std::max<uint32_t>(1, units / tiles), nkb / 4);
+  } else {
+    splits = std::min<uint32_t>(split_k, std::max<uint32_t>(1, nkb));
+  }
+  splits = std::max<uint32_t>(1, splits);
+  const uint32_t kbps = std::max<uint32_t>(1, (nkb + splits - 1) / splits);
+  splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
+  if (epi.bits_out && splits > 1) throw ConfigError("GEMM bit output needs an unsplit K");
+  if (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15))
+    throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
+  static const int epi_env = [] {
+    const char* v = std::getenv("CATGNN_GEMM_EPI_WARPS");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int epiw = epi_env == 4 || epi_env == 8 ? epi_env : (nkb <= 2 && splits == 1 ? 8 : 4);
+  const size_t kEpiSmem = epi_smem(epiw);
+  const size_t budget = 227 * 1024 - 1024 - kBarBytes(kMaxStages) - kEpiSmem;
+  const size_t stage_bytes = 2 * (size_t)A_STAGE + 2 * (size_t)BNh * 128;
+  const uint32_t stages = (uint32_t)std::min<size_t>(kMaxStages, budget / stage_bytes);
+  if (stages < 2) throw InternalError("GEMM tile does not fit in shared memory");
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + kBarBytes(stages) + kEpiSmem;
+
+  GemmArgs args{};
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.BN = BN;
+  args.bk = BKE;
+  args.stages = stages;
+  args.kb_per_split = kbps;
+  args.tmem_cols = pow2_cols(2 * round_up(BN, 32));
+  args.split3 = 0;
+  args.mt = mt;
+  args.nt = nt;
+  args.splits = splits;
+  args.tiles = mt * nt * splits;
+  args.a_mn = a.mn_major ? 1u : 0u;
+  args.b_mn = b.mn_major ? 1u : 0u;
+  args.bm = bm;
+  // instruction descriptor: D f32, A/B bf16 (kind::f16), majors, N>>3, M>>4
+  args.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (args.a_mn << 15) | (args.b_mn << 16) | ((BN >> 3) << 17) |
+               ((bm >> 4) << 24);
+  float* partial = nullptr;
+  args.epi = epi;
+  args.epi.partial = nullptr;
+  if (splits > 1) {
+    partial = ctx->scratch_buf<float>("gemm_partial", (size_t)splits * M * N);
+    args.epi.partial = partial;
+  }
+  const CUtensorMap tah = a.mn_major ? make_map16_mn(a.hi, M, K, a.ld) : make_map16(a.hi, M, K, a.ld, BM);
+  const CUtensorMap tal = a.mn_major ? make_map16_mn(a.lo, M, K, a.ld) : make_map16(a.lo, M, K, a.ld, BM);
+  const CUtensorMap tbh = b.mn_major ? make_map16_mn(b.hi, N, K, b.ld) : make_map16(b.hi, N, K, b.ld, BNh);
+  const CUtensorMap tbl = b.mn_major ? make_map16_mn(b.lo, N, K, b.ld) : make_map16(b.lo, N, K, b.ld, BNh);
+  static std::mutex attr_mu;
+  static std::map<int, std::array<bool, 4>> attr_set;
+  auto kern = pair ? (epiw == 8 ? gemm_tf32_kernel<2, 8, true> : gemm_tf32_kernel<2, 4, true>)
+                   : (epiw == 8 ? gemm_tf32_kernel<1, 8, true> : gemm_tf32_kernel<1, 4, true>);
+  const int kThreads = epiw == 8 ? threads_for<8>() : threads_for<4>();
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    bool& done = attr_set[ctx->device][(ncta - 1) * 2 + (epiw == 8)];
+    if (!done) {
+      CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      done = true;
+    }
+  }
+  auto dim = [](uint32_t x) { return x > 4096 ? std::string("rows") : std::to_string(x); };
+  int t = ctx->begin_timed(1, ctx->timing ? "K3 gemm bf16x3 M=" + dim(M) + " N=" + dim(N) + " K=" + dim(K) +
+                                             (pair ? " pair" : "") + (splits > 1 ? " split-K" : "")
+                                       : std::string());
+  const unsigned grid = std::min<unsigned>(args.tiles, units) * ncta;
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CG_CUDA(cudaLaunchKernelEx(&cfg, kern, tah, tbh, tbl, tal, args));
+  } else {
+    kern<<<grid, kThreads, smem, ctx->stream>>>(tah, tbh, tbl, tal, args);
   }
   CG_CHECK_LAUNCH();
   ctx->launches++;
@@ -950,7 +1220,8 @@ extern "C" int catgnn_gemm(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, c
   using namespace catgnn;
   return guarded([&] {
     if (!ctx) throw ConfigError("null context");
-    if (precision != 1 && precision != 3) throw ConfigError("precision must be 1 (TF32) or 3 (3xTF32)");
+    if (precision != 1 && precision != 3 && precision != 4)
+      throw ConfigError("precision must be 1 (TF32), 3 (3xTF32) or 4 (bf16x3)");
     CG_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
     auto upload = [&](const char* name, const float* h, uint32_t r, uint32_t c) {
@@ -969,7 +1240,20 @@ extern "C" int catgnn_gemm(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, c
     GemmEpi e{};
     e.out = dC;
     e.ld_out = ldc;
-    gemm(ctx, ga, gb, M, N, K, e, split_k, precision);
+    if (precision == 4) {  // bf16x3: split both operands on the device, then the pre-split GEMM
+      auto split = [&](const char* name, const GemmOperand& o, uint32_t rows, uint32_t cols) {
+        const uint32_t ld8 = round_up(std::max(cols, 1u), 8);
+        __nv_bfloat16* p = ctx->scratch_buf<__nv_bfloat16>(name, 2 * (size_t)std::max(rows, 1u) * ld8 + 64);
+        __nv_bfloat16* lo = p + (size_t)std::max(rows, 1u) * ld8;
+        split_bf16(ctx, o.ptr, o.ld, rows, cols, p, lo, ld8);
+        return SplitOperand{p, lo, ld8, o.mn_major};
+      };
+      SplitOperand sa = a_mn ? split("g_As", ga, K, M) : split("g_As", ga, M, K);
+      SplitOperand sb = b_mn ? split("g_Bs", gb, K, N) : split("g_Bs", gb, N, K);
+      gemm_bf16x3(ctx, sa, sb, M, N, K, e, split_k);
+    } else {
+      gemm(ctx, ga, gb, M, N, K, e, split_k, precision);
+    }
     CG_CUDA(cudaMemcpy2DAsync(Cout, N * 4, dC, ldc * 4, N * 4, M, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
   });
@@ -1026,5 +1310,30 @@ extern "C" int catgnn_debug_gemm_dev(catgnn_ctx ctx, uint32_t M, uint32_t N, uin
     e.bits_out = bits_out;
     e.bits_words = bits_words;
     gemm(ctx, GemmOperand{A, lda, a_mn != 0}, GemmOperand{B, ldb, b_mn != 0}, M, N, K, e, split_k, precision);
+  });
+}
+
+// Diagnostics hook: one bf16x3 GEMM on caller-owned pre-split DEVICE operands.
+extern "C" int catgnn_debug_gemm16_dev(catgnn_ctx ctx, uint32_t M, uint32_t N, uint32_t K, const void* A_hi,
+                                       const void* A_lo, uint32_t lda, int a_mn, const void* B_hi, const void* B_lo,
+                                       uint32_t ldb, int b_mn, float* C, uint32_t ldc, uint32_t split_k,
+                                       const float* rowscale, const float* bias, int relu, const uint32_t* mask_bits,
+                                       uint32_t mask_words, uint32_t store_cols) {
+  using namespace catgnn;
+  return guarded([&] {
+    if (!ctx) throw ConfigError("null context");
+    CG_CUDA(cudaSetDevice(ctx->device));
+    GemmEpi e{};
+    e.out = C;
+    e.ld_out = ldc;
+    e.rowscale = rowscale;
+    e.bias = bias;
+    e.relu = relu;
+    e.mask_bits = mask_bits;
+    e.mask_words = mask_words;
+    e.store_cols = store_cols;
+    auto bf = [](const void* p) { return static_cast<const __nv_bfloat16*>(p); };
+    gemm_bf16x3(ctx, SplitOperand{bf(A_hi), bf(A_lo), lda, a_mn != 0}, SplitOperand{bf(B_hi), bf(B_lo), ldb, b_mn != 0},
+                M, N, K, e, split_k);
   });
 }

@@ -1,5 +1,7 @@
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "common.hpp"
 
 namespace catgnn {
@@ -41,6 +43,27 @@ struct GemmOperand {
 
 void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, uint32_t K, const GemmEpi& epi,
           uint32_t split_k = 1, int precision = 1);
+
+// bf16x3 operand: x = hi + lo with hi = bf16(x), lo = bf16(x - hi) (~16
+// significant bits, relative error ~2^-17), row-major with row stride ld
+// (multiple of 8 elements).  K-major / MN-major as GemmOperand.
+struct SplitOperand {
+  const __nv_bfloat16* hi = nullptr;
+  const __nv_bfloat16* lo = nullptr;
+  uint32_t ld = 0;
+  bool mn_major = false;
+};
+
+// C = A . B^T on pre-split operands: lo*hi + hi*lo + hi*hi on the tcgen05
+// kind::f16 tensor cores (fp32 accumulation in TMEM), no conversion pass in
+// the GEMM; same epilogue / split-K as gemm().
+void gemm_bf16x3(catgnn_ctx ctx, SplitOperand a, SplitOperand b, uint32_t M, uint32_t N, uint32_t K,
+                 const GemmEpi& epi, uint32_t split_k = 1);
+
+// fp32 rows x cols (row stride ld_in) -> (hi, lo) rows x ld_out; columns
+// [cols, ld_out) are written as zeros.
+void split_bf16(catgnn_ctx ctx, const float* in, uint32_t ld_in, uint64_t rows, uint32_t cols, __nv_bfloat16* hi,
+                __nv_bfloat16* lo, uint32_t ld_out);
 
 void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
              uint32_t N, uint32_t K, const GemmEpi& epi, uint32_t split_k = 1, int precision = 1);

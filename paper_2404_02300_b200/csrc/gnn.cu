@@ -417,16 +417,95 @@ const float* bwd_pre(const catgnn_model_s* M, const catgnn_shard_s* S) {
 }
 int bwd_norm(const catgnn_model_s* M) { return M->cfg.kind == CATGNN_MODEL_GCN ? kNormGcn : kNormNone; }
 
+// bf16x3 activation: hi / lo bf16 rows (row stride ld, a multiple of 8)
+struct Split {
+  uint16_t* hi = nullptr;
+  uint16_t* lo = nullptr;
+  uint32_t ld = 0;
+  explicit operator bool() const { return hi != nullptr; }
+};
+SplitOperand op16(const Split& s, bool mn) {
+  return SplitOperand{reinterpret_cast<const __nv_bfloat16*>(s.hi), reinterpret_cast<const __nv_bfloat16*>(s.lo),
+                      s.ld, mn};
+}
+
 struct Bufs {
   const float* in;  // H_{l-1}
   uint32_t in_ld;
   float* mid;       // T / A / cat / P
   uint32_t mid_ld;
-  float* out;       // H_l
+  float* out;       // H_l (nullptr when H_l exists only as `split`)
   uint32_t out_ld;
   uint32_t* bits = nullptr;  // H_l > 0, one bit per column (ReLU layers): the backward's mask
   uint32_t bits_words = 0;
+  Split in_split;  // bf16x3 layers: H_{l-1} (or x) as the GEMMs' pre-split operand
+  Split split;     // H_l written by K2 as the next bf16x3 layer's operand
 };
+
+// bf16x3 GEMM path (default; CATGNN_GEMM_BF16X3=0: 3xTF32 everywhere): the
+// transform-first GCN / GIN / SGC layers, whose GEMM operands are produced by
+// K2 epilogues (H_l, dT_l), the features (split once per upload) or the
+// weights (split per forward) — written straight as bf16 (hi, lo) pairs, so
+// the GEMM has no conversion pass and runs kind::f16 MMAs (2x the tf32 rate,
+// half the shared-memory bytes per MMA); ~2^-16 relative per product.
+const bool kBf16x3 = [] {
+  const char* v = std::getenv("CATGNN_GEMM_BF16X3");
+  return v ? v[0] != '0' : true;
+}();
+bool bf_layer(const catgnn_model_s* M, size_t l) {
+  const int k = M->cfg.kind;
+  return kBf16x3 && l < M->layers.size() && !M->layers[l].agg_first &&
+         (k == CATGNN_MODEL_GCN || k == CATGNN_MODEL_GIN || k == CATGNN_MODEL_SGC);
+}
+
+// Named bf16x3 activation pair, zero-filled whenever its shape changes.
+Split act16(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld) {
+  Split s;
+  s.ld = ld;
+  const size_t n = std::max<uint64_t>(1, rows) * ld;
+  s.hi = ctx->scratch_buf<uint16_t>(name + "_hi", n);
+  s.lo = ctx->scratch_buf<uint16_t>(name + "_lo", n);
+  auto sig = std::make_pair(rows, ld);
+  auto it = ctx->act_shape.find(name + "_s");
+  if (it == ctx->act_shape.end() || it->second != sig) {
+    CG_CUDA(cudaMemsetAsync(s.hi, 0, n * 2, ctx->stream));
+    CG_CUDA(cudaMemsetAsync(s.lo, 0, n * 2, ctx->stream));
+    ctx->act_shape[name + "_s"] = sig;
+  }
+  return s;
+}
+
+// The shard's features as a bf16x3 pair, re-split when they changed.
+Split shard_x_split(catgnn_shard_s* S) {
+  const uint32_t ld = round_up(std::max<uint32_t>(S->dim, 1), 8);
+  if (S->xs_version != S->x_version || S->xs_ld != ld || !S->xs_hi.p) {
+    const size_t n = std::max<uint64_t>(1, S->rows) * ld;
+    if (S->xs_ld != ld || !S->xs_hi.p) {
+      S->xs_hi.alloc(n);
+      S->xs_lo.alloc(n);
+      S->xs_ld = ld;
+    }
+    split_bf16(S->ctx, S->x.p, S->ld, S->rows, S->dim, reinterpret_cast<__nv_bfloat16*>(S->xs_hi.p),
+               reinterpret_cast<__nv_bfloat16*>(S->xs_lo.p), ld);
+    S->xs_version = S->x_version;
+  }
+  return Split{S->xs_hi.p, S->xs_lo.p, ld};
+}
+
+// Weights of layer l as a bf16x3 pair (split from the fp32 master copy).
+Split weight_split(catgnn_model_s* M, size_t l) {
+  const Layer& L = M->layers[l];
+  return Split{M->ws_hi.p + M->ws_off[l], M->ws_lo.p + M->ws_off[l], round_up(L.w_cols, 8)};
+}
+void split_weights(catgnn_model_s* M) {
+  for (size_t l = 0; l < M->layers.size(); ++l) {
+    if (!bf_layer(M, l)) continue;
+    const Layer& L = M->layers[l];
+    const Split w = weight_split(M, l);
+    split_bf16(M->ctx, M->params.p + L.off_w, L.w_cols, L.w_rows, L.w_cols, reinterpret_cast<__nv_bfloat16*>(w.hi),
+               reinterpret_cast<__nv_bfloat16*>(w.lo), w.ld);
+  }
+}
 
 uint32_t* act_bits(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t words) {
   return ctx->scratch_buf<uint32_t>(name, std::max<uint64_t>(1, rows) * words);
@@ -444,18 +523,26 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
   const float* in = S->x.p;
   uint32_t in_ld = S->ld;
   const bool fresh = M->last_rows != rows;
+  split_weights(M);
+  M->h_split_only.assign(M->layers.size(), false);
   for (size_t l = 0; l < M->layers.size(); ++l) {
     const Layer& L = M->layers[l];
     const bool last = l + 1 == M->layers.size();
     Bufs& b = B[l];
     b.in = in;
     b.in_ld = in_ld;
+    // transform-first K2 output consumed only by the next (bf16x3) layer's
+    // GEMMs: written as a bf16x3 pair, no fp32 copy
+    const bool h_split = !L.agg_first && !last && bf_layer(M, l + 1);
     if (L.out_in_next_mid) {  // the next layer's [h | mean], left half
       b.out_ld = 2 * M->layers[l + 1].K_in;
       b.out = act(ctx, nm("mid", l + 1), rows, b.out_ld, fresh);
-    } else {
+    } else if (!h_split) {
       b.out_ld = L.ld_act;
       b.out = act(ctx, nm("H", l), rows, b.out_ld, fresh);
+    } else {
+      b.out_ld = L.ld_act;
+      b.out = nullptr;
     }
     if (!last) {
       b.bits_words = (L.D_out + 31) / 32;
@@ -497,16 +584,37 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       e.bits_out = b.bits; e.bits_words = b.bits_words;
       if (!L.out_in_next_mid) e.store_cols = b.out_ld;  // zero padding (bias is zero-padded)
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
-    } else {  // GCN / GIN transform-first
+    } else {  // GCN / GIN / SGC transform-first
       b.mid_ld = L.ld_act;
       b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
       GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld; e.rowscale = gcn ? S->dinv.p : nullptr;
       e.store_cols = b.mid_ld;  // the padding of T is zero either way: staged stores for the ragged tail
-      gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
+      if (bf_layer(M, l)) {
+        // the layer input as a pre-split pair: the features, the previous K2's
+        // bf16x3 output, or (previous layer on another path) a split of its fp32 rows
+        if (l == 0) b.in_split = shard_x_split(S);
+        else if (B[l - 1].split) b.in_split = B[l - 1].split;
+        else {
+          b.in_split = act16(ctx, nm("Hin", l), rows, round_up(L.K_in, 8));
+          split_bf16(ctx, in, in_ld, rows, L.K_in, reinterpret_cast<__nv_bfloat16*>(b.in_split.hi),
+                     reinterpret_cast<__nv_bfloat16*>(b.in_split.lo), b.in_split.ld);
+        }
+        gemm_bf16x3(ctx, op16(b.in_split, false), op16(weight_split(M, l), false), (uint32_t)rows, L.d_out, L.K_in,
+                    e, 1);
+      } else {
+        gemm_tn(ctx, in, in_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1,
+                kFwdPrecision);
+      }
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
       a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
       a.bits_out = b.bits; a.bits_words = b.bits_words;
+      if (h_split) {  // H_l is only the next bf16x3 layer's GEMM operand
+        b.split = act16(ctx, nm("Hs", l), rows, round_up(L.D_out, 8));
+        a.out = nullptr;
+        a.out_hi = b.split.hi; a.out_lo = b.split.lo; a.out_s_ld = b.split.ld;
+        M->h_split_only[l] = true;
+      }
       aggregate(S, a);
     }
     in = b.out;
@@ -610,6 +718,20 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         a.out = dZprev; a.out_ld = L.K_in; a.width = L.K_in;
         a.mask_bits = hbits; a.mask_words = hwords;
         aggregate(S, a);
+      }
+    } else if (bf_layer(M, li)) {  // GCN / GIN / SGC transform-first, bf16x3 GEMMs
+      // dT = pre (A+I)(post dZ) straight into a bf16x3 pair: both GEMMs' operand
+      const Split dT = act16(ctx, "dTs", rows, round_up(L.ld_act, 8));
+      AggArgs a;
+      a.in = dZ; a.in_ld = dZ_ld; a.pre = bwd_pre(M, S); a.self = 1; a.norm = bwd_norm(M);
+      if (li == nl - 1 && dZs) { a.in = dZs; a.pre = nullptr; }  // pre-scaled by K4
+      a.out = nullptr; a.out_hi = dT.hi; a.out_lo = dT.lo; a.out_s_ld = dT.ld; a.width = L.D_out;
+      aggregate(S, a);
+      GemmEpi e; e.out = gW; e.ld_out = L.w_cols;  // dW = dT^T H_{l-1} (both MN-major, in place)
+      gemm_bf16x3(ctx, op16(dT, true), op16(b.in_split, true), L.d_out, L.w_cols, (uint32_t)rows, e, 0);
+      if (need_dx) {  // dZ_{l-1} = mask (dT W)
+        GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
+        gemm_bf16x3(ctx, op16(dT, false), op16(weight_split(M, li), true), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
       }
     } else {  // GCN / GIN transform-first
       float* dT = act(ctx, "dmid", rows, L.ld_act, false);
@@ -726,6 +848,16 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
     plan_layers(M.get());
     M->params.alloc(M->n_params);
     M->grads.alloc(M->n_params);
+    {  // bf16x3 weight copies (layers on the bf16x3 path only)
+      uint64_t ws = 0;
+      M->ws_off.assign(M->layers.size(), 0);
+      for (size_t l = 0; l < M->layers.size(); ++l) {
+        M->ws_off[l] = ws;
+        if (bf_layer(M.get(), l)) ws += (uint64_t)M->layers[l].w_rows * round_up(M->layers[l].w_cols, 8);
+      }
+      M->ws_hi.alloc(std::max<uint64_t>(1, ws));
+      M->ws_lo.alloc(std::max<uint64_t>(1, ws));
+    }
     M->m.alloc(M->n_params);
     M->v.alloc(M->n_params);
     CG_CUDA(cudaMemsetAsync(M->grads.p, 0, M->n_params * 4, ctx->stream));
@@ -922,6 +1054,23 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
     const Layer& L = m->layers[layer];
     const float* src = nullptr;
     uint32_t ld = 0, w = L.d_out;
+    if (what == 0 && layer < m->h_split_only.size() && m->h_split_only[layer]) {
+      // H_l kept only as the bf16x3 pair: export hi + lo
+      const uint32_t sld = round_up(L.D_out, 8);
+      const uint16_t* hi = m->ctx->scratch_buf<uint16_t>(nm("Hs", layer) + "_hi", 1);
+      const uint16_t* lo = m->ctx->scratch_buf<uint16_t>(nm("Hs", layer) + "_lo", 1);
+      if (width) *width = w;
+      if (out && s->rows) {
+        std::vector<uint16_t> h(s->rows * (size_t)sld), lw(s->rows * (size_t)sld);
+        CG_CUDA(cudaMemcpyAsync(h.data(), hi, h.size() * 2, cudaMemcpyDeviceToHost, m->ctx->stream));
+        CG_CUDA(cudaMemcpyAsync(lw.data(), lo, lw.size() * 2, cudaMemcpyDeviceToHost, m->ctx->stream));
+        CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        auto f = [](uint16_t v) { uint32_t u = (uint32_t)v << 16; float x; std::memcpy(&x, &u, 4); return x; };
+        for (uint64_t r = 0; r < s->rows; ++r)
+          for (uint32_t c = 0; c < w; ++c) out[r * w + c] = f(h[r * sld + c]) + f(lw[r * sld + c]);
+      }
+      return;
+    }
     if (what == 0 && L.out_in_next_mid) {
       src = m->ctx->scratch_buf<float>(nm("mid", layer + 1), 1);
       ld = 2 * m->layers[layer + 1].K_in;

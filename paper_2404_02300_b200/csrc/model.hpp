@@ -41,6 +41,10 @@ struct catgnn_model_s {
   double last_loss = 0.0;
   catgnn::DevBuf<double> loss_dev;  // sum of the last step's per-row losses (read lazily)
   uint64_t loss_rows = 0;   // train rows of that step
+  // bf16x3 copies of the weights (hi / lo per layer at ws_off, rows of round8(w_cols))
+  catgnn::DevBuf<uint16_t> ws_hi, ws_lo;
+  std::vector<uint64_t> ws_off;
+  std::vector<bool> h_split_only;  // layer outputs the last forward kept only as bf16x3 pairs
 };
 
 namespace catgnn {

@@ -37,6 +37,11 @@ struct catgnn_shard_s {
   // features
   uint32_t dim = 0, ld = 0;
   catgnn::DevBuf<float> x, xprop;
+  // bf16x3 copy of x (hi / lo, row stride xs_ld = round8(dim)) for the tensor-core
+  // GEMMs of the GNN layers, re-split whenever x changes (x_version)
+  catgnn::DevBuf<uint16_t> xs_hi, xs_lo;
+  uint32_t xs_ld = 0;
+  uint64_t x_version = 1, xs_version = 0;
   // labels / roles (host copies + device copies)
   std::vector<int32_t> h_labels;
   std::vector<uint32_t> h_train, h_val, h_test;
@@ -78,6 +83,12 @@ struct AggArgs {
   uint32_t mask_words = 0;              // 32-bit words per row
   uint32_t* bits_out = nullptr;         // write out > 0 as bits (forward ReLU layers)
   uint32_t bits_words = 0;
+  // bf16x3 output: out[r][c] also (or, with out == nullptr, only) written as the
+  // pair hi = bf16(v), lo = bf16(v - hi) at column c of rows out_s_ld apart — the
+  // pre-split operand of the next tensor-core GEMM (gemm_bf16x3)
+  void* out_hi = nullptr;
+  void* out_lo = nullptr;
+  uint32_t out_s_ld = 0;
 };
 
 // K1: CSR builder (stable radix sort by source row, bit-exact with

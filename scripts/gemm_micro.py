@@ -100,4 +100,51 @@ for name, (M, N, K, A, lda, amn, B, ldb, bmn, oshape, kw, refn) in cases.items()
                      tflops=round(2 * M * N * K / us / 1e6, 1), rel_err=err)
     print(f"{name:30s} {us:8.1f} us  floor {floor:6.1f} us  ({floor / us:4.2f})  "
           f"{2 * M * N * K / us / 1e6:6.1f} TFLOP/s  err {err}", flush=True)
+# bf16x3 (precision 4 through catgnn_debug_gemm_dev: operands split on the
+# device into hi/lo pairs first — the split is timed separately and excluded)
+lib.catgnn_debug_gemm16_dev.restype = C.c_int
+lib.catgnn_debug_gemm16_dev.argtypes = [vp, u32, u32, u32, vp, vp, u32, C.c_int, vp, vp, u32, C.c_int, vp, u32, u32,
+                                        vp, vp, C.c_int, vp, u32, u32]
+
+
+def split(t):
+    rows, cols = t.shape
+    ld8 = (cols + 7) // 8 * 8
+    hi = torch.zeros(rows, ld8, device=dev, dtype=torch.bfloat16)
+    hi[:, :cols] = t.to(torch.bfloat16)
+    lo = torch.zeros(rows, ld8, device=dev, dtype=torch.bfloat16)
+    lo[:, :cols] = (t - hi[:, :cols].float()).to(torch.bfloat16)
+    return hi, lo, ld8
+
+
+for name, (M, N, K, A, lda, amn, B, ldb, bmn, oshape, kw, refn) in cases.items():
+    Cm = torch.zeros(*oshape, device=dev)
+    mk = mask if kw.get("mask") else None
+    Ah, Al, la = split(A[:, :(M if amn else K)])
+    Bh, Bl, lb = split(B[:, :(N if bmn else K)])
+
+    def run16():
+        check(lib.catgnn_debug_gemm16_dev(ctx.handle, M, N, K, p(Ah), p(Al), la, amn, p(Bh), p(Bl), lb, bmn, p(Cm),
+                                          oshape[1], 0 if kw.get("split") == 0 else 1, p(kw.get("rowscale")), None,
+                                          0, p(mk), bits_words if mk is not None else 0, kw.get("store", 0)))
+    run16()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(REPS):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream); run16(); e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    ts.sort()
+    us = ts[len(ts) // 2]
+    err = None
+    if refn is not None:
+        ref = refn()
+        got = Cm[:, :ref.shape[1]].double() if Cm.shape[1] != ref.shape[1] else Cm.double()
+        err = float((got - ref).norm() / ref.norm())
+    floor = out[name]["floor_us"]
+    out[name + " bf16x3"] = dict(us=round(us, 1), floor_us=floor, frac_of_floor=round(floor / us, 2),
+                                 tflops=round(2 * M * N * K / us / 1e6, 1), rel_err=err)
+    print(f"{name + ' bf16x3':37s} {us:8.1f} us  floor {floor:6.1f} us  ({floor / us:4.2f})  "
+          f"{2 * M * N * K / us / 1e6:6.1f} TFLOP/s  err {err}", flush=True)
 print(json.dumps({"rows": R, "gemm": out}))

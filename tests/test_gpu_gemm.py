@@ -89,3 +89,35 @@ def test_gemm_mn_major(ctx, a_mn, b_mn, M, N, K, split, prec):
 def test_gemm_k_zero(ctx):
     A = np.zeros((5, 0), np.float32); B = np.zeros((16, 0), np.float32)
     assert np.all(gemm(ctx, A, B) == 0)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1), (0, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K,split", [(200, 48, 256, 1), (4096, 256, 604, 1), (256, 604, 20000, 0),
+                                         (41, 256, 3000, 0), (2000, 256, 41, 1), (513, 41, 100, 1),
+                                         (1100, 602, 256, 1), (3000, 256, 1000, 4), (128, 16, 64, 1),
+                                         (777, 130, 200, 1)])
+def test_gemm_bf16x3(ctx, a_mn, b_mn, M, N, K, split):
+    """bf16x3 path (pre-split hi/lo operands, kind::f16 MMAs, no conversion pass):
+    every operand layout the GNN uses, tails in M / N / K, split-K and CTA pairs."""
+    rng = np.random.default_rng(M * 5 + N * 3 + K + 7 * a_mn + 11 * b_mn)
+    A = rng.standard_normal((K, M) if a_mn else (M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N) if b_mn else (N, K)).astype(np.float32)
+    Al = A.T if a_mn else A
+    Bl = B.T if b_mn else B
+    want = Al.astype(np.float64) @ Bl.astype(np.float64).T
+    got = gemm_general(ctx, A, a_mn, B, b_mn, split, 4)
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 5e-5, err
+
+
+def test_gemm_bf16x3_cancellation(ctx):
+    # the weight-gradient cancellation case: bf16x3 stays ~1e-4 of the (1000x smaller) result
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((64, 20000)).astype(np.float32)
+    B = rng.standard_normal((96, 20000)).astype(np.float32)
+    B[:, 10000:] = -B[:, :10000] * np.float32(0.999)
+    A[:, 10000:] = A[:, :10000]
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    err1 = np.linalg.norm(gemm(ctx, A, B, 0, 1) - want) / np.linalg.norm(want)
+    err4 = np.linalg.norm(gemm_general(ctx, A, 0, B, 0, 0, 4) - want) / np.linalg.norm(want)
+    assert err4 < err1 / 20 and err4 < 2e-2, (err1, err4)
