@@ -687,6 +687,11 @@ def main():
 
     # end-to-end through the C ABI: global features re-uploaded from pinned host memory each step, loss read back
     e2e = None
+    # the first layer's GEMMs read the bf16x3 feature copy: gathers write only that
+    split_only = w.model in ("gcn", "gin") and w.dim > w.hidden and os.environ.get("CATGNN_GEMM_BF16X3", "1") != "0"
+    if not args.no_e2e and split_only:
+        for s in shards:
+            s.set_feature_layout(True)
     if not args.no_e2e:
         for t in range(2):
             step(True, t, 2)
@@ -715,6 +720,7 @@ def main():
         e2e = {"value": edges_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * w.partitions, "ms_per_step": e2e_ms,
                "graph": "two steps per CUDA graph replay (device stores alternate)" if e2e_graph else None,
+               "feature_layout": "bf16x3 (hi, lo) rows written by the gather" if split_only else "fp32 rows",
                "path": "catgnn_features_upload (global features, pinned H2D on a copy stream, double-buffered; "
                        "N > 1: 1/N of the rows per rank + catgnn_features_allgather over NVLink; "
                        "step t+1's copy overlaps step t) + per partition catgnn_shard_gather_features + "

@@ -157,6 +157,12 @@ int catgnn_features_reset_deps(catgnn_features f);
 int catgnn_split_features(catgnn_ctx ctx, catgnn_artifact a, const char* features, const char* out_dir,
                           uint32_t* files_written);
 int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f);
+/* Device feature layout (no reference counterpart).  split_only = 1: gathers
+ * write only the bf16x3 (hi, lo) copy that the GNN layers' tensor-core GEMMs
+ * read (half the write traffic of keeping fp32 rows too); calls needing the
+ * fp32 rows (SGC propagation, feature export, a model whose first layer is not
+ * on the bf16x3 path) fail with ConfigError until the next upload. */
+int catgnn_shard_set_feature_layout(catgnn_shard s, int split_only);
 /* Multi-GPU refresh of a feature store: rank r uploads rows [r*R, (r+1)*R)
  * (catgnn_features_upload with row_begin = r*R), then this in-place NCCL
  * all-gather over NVLink completes every rank's copy (store rows >= R x ranks)

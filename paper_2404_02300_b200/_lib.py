@@ -69,6 +69,7 @@ def _load():
         "catgnn_features_destroy": (C.c_int, [vp]),
         "catgnn_features_upload": (C.c_int, [vp, vp, u64, u64]),
         "catgnn_shard_gather_features": (C.c_int, [vp, vp]),
+        "catgnn_shard_set_feature_layout": (C.c_int, [vp, C.c_int]),
         "catgnn_features_allgather": (C.c_int, [vp, vp, u64]),
         "catgnn_complete_edges": (C.c_int, [vp, vp, u64, vp, vp, u64, u32, u32, P(vp)]),
         "catgnn_complete_edges_indexed": (C.c_int, [vp, vp, vp, u64, vp, vp, u32, u32, P(vp)]),

@@ -112,6 +112,7 @@ void h2d(T* dst, const T* src, size_t n, cudaStream_t st) {
 void copy_features_in(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   cudaStream_t st = s->ctx->stream;
   s->x_version++;  // the bf16x3 copy (gnn.cu) is re-split on next use
+  s->x_fp32_valid = true;
   const size_t bytes = s->rows * (size_t)dim * sizeof(float);
   if (s->ld == dim) {
     CG_CUDA(cudaMemcpyAsync(s->x.p, feats, bytes, cudaMemcpyHostToDevice, st));
@@ -128,6 +129,7 @@ void upload_features(catgnn_shard_s* s, const float* feats, uint32_t dim) {
   s->ld = round_up(std::max<uint32_t>(dim, 1), 4);
   s->x.alloc(std::max<uint64_t>(1, s->rows) * s->ld);
   s->x_version++;
+  s->x_fp32_valid = true;
   s->xprop.release();
   if (s->rows == 0 || dim == 0) return;
   if (s->ld != dim) CG_CUDA(cudaMemsetAsync(s->x.p, 0, s->x.bytes(), s->ctx->stream));
@@ -638,6 +640,8 @@ int catgnn_shard_labels(catgnn_shard s, int32_t* labels) {
 int catgnn_shard_export_features(catgnn_shard s, int which, float* out) {
   return guarded([&] {
     check_shard(s);
+    if (which == 0 && !s->x_fp32_valid)
+      throw ConfigError("shard features are held as bf16x3 only (catgnn_shard_set_feature_layout)");
     const float* src = which == 0 ? s->x.p : s->xprop.p;
     if (!src) throw ConfigError("requested feature buffer is not materialised");
     if (s->rows && s->dim)
@@ -655,6 +659,8 @@ int catgnn_sgc_propagate(catgnn_shard s, uint32_t hops) {
     catgnn_ctx ctx = s->ctx;
     const size_t n = std::max<uint64_t>(1, s->rows) * s->ld;
     s->xprop.reserve(n);
+    if (!s->x_fp32_valid)
+      throw ConfigError("shard features are held as bf16x3 only (catgnn_shard_set_feature_layout); upload them");
     if (hops == 0 || s->rows == 0) {  // k = 0 is the identity (train.hpp:29-32)
       if (s->rows) copy_rows(ctx, s->x.p, s->ld, s->xprop.p, s->ld, s->rows, s->ld);
       return;

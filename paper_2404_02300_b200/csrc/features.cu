@@ -13,6 +13,8 @@
 #include <filesystem>
 #include <map>
 
+#include <cuda_bf16.h>
+
 #include "artifact.hpp"
 #include "comm.hpp"
 #include "shard.hpp"
@@ -46,13 +48,19 @@ namespace {
 template <int V>
 __global__ void __launch_bounds__(256) gather_rows_kernel(const float* __restrict__ src, uint32_t dim,
                                                           const uint64_t* __restrict__ ext, uint64_t rows,
-                                                          float* __restrict__ dst, uint32_t ld) {
+                                                          float* __restrict__ dst, uint32_t ld,
+                                                          __nv_bfloat16* __restrict__ hi,
+                                                          __nv_bfloat16* __restrict__ lo, uint32_t sld) {
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (uint64_t r = warp; r < rows; r += nwarps) {
     const float* s = src + __ldg(ext + r) * dim;
-    float* d = dst + r * ld;
+    float* d = dst ? dst + r * ld : nullptr;
+    // bf16x3 copy for the GNN's tensor-core GEMMs (hi = bf16(x), lo = bf16(x - hi)),
+    // written from the same registers instead of a separate split pass
+    __nv_bfloat16* dh = hi ? hi + r * sld : nullptr;
+    __nv_bfloat16* dl = lo ? lo + r * sld : nullptr;
     // U vector loads in flight per lane before their stores (a 602-wide row is
     // 10 float2 per lane: one round trip instead of ten)
     constexpr int U = 8;
@@ -65,7 +73,18 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const float* __restric
           if (c0 + u * step < dim) v[u] = __ldg(reinterpret_cast<const float4*>(s + c0 + u * step));
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (c0 + u * step < dim) *reinterpret_cast<float4*>(d + c0 + u * step) = v[u];
+          if (c0 + u * step < dim) {
+            if (d) *reinterpret_cast<float4*>(d + c0 + u * step) = v[u];
+            if (dh) {
+              const __nv_bfloat162 h0 = __floats2bfloat162_rn(v[u].x, v[u].y), h1 = __floats2bfloat162_rn(v[u].z, v[u].w);
+              const __nv_bfloat162 l0 = __floats2bfloat162_rn(v[u].x - __low2float(h0), v[u].y - __high2float(h0));
+              const __nv_bfloat162 l1 = __floats2bfloat162_rn(v[u].z - __low2float(h1), v[u].w - __high2float(h1));
+              reinterpret_cast<__nv_bfloat162*>(dh + c0 + u * step)[0] = h0;
+              reinterpret_cast<__nv_bfloat162*>(dh + c0 + u * step)[1] = h1;
+              reinterpret_cast<__nv_bfloat162*>(dl + c0 + u * step)[0] = l0;
+              reinterpret_cast<__nv_bfloat162*>(dl + c0 + u * step)[1] = l1;
+            }
+          }
       } else if (V == 2) {
         float2 v[U];
 #pragma unroll
@@ -73,7 +92,15 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const float* __restric
           if (c0 + u * step < dim) v[u] = __ldg(reinterpret_cast<const float2*>(s + c0 + u * step));
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (c0 + u * step < dim) *reinterpret_cast<float2*>(d + c0 + u * step) = v[u];
+          if (c0 + u * step < dim) {
+            if (d) *reinterpret_cast<float2*>(d + c0 + u * step) = v[u];
+            if (dh) {
+              const __nv_bfloat162 h = __floats2bfloat162_rn(v[u].x, v[u].y);
+              *reinterpret_cast<__nv_bfloat162*>(dh + c0 + u * step) = h;
+              *reinterpret_cast<__nv_bfloat162*>(dl + c0 + u * step) =
+                  __floats2bfloat162_rn(v[u].x - __low2float(h), v[u].y - __high2float(h));
+            }
+          }
       } else {
         float v[U];
 #pragma unroll
@@ -81,7 +108,14 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const float* __restric
           if (c0 + u * step < dim) v[u] = __ldg(s + c0 + u * step);
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (c0 + u * step < dim) d[c0 + u * step] = v[u];
+          if (c0 + u * step < dim) {
+            if (d) d[c0 + u * step] = v[u];
+            if (dh) {
+              const __nv_bfloat16 h = __float2bfloat16_rn(v[u]);
+              dh[c0 + u * step] = h;
+              dl[c0 + u * step] = __float2bfloat16_rn(v[u] - __bfloat162float(h));
+            }
+          }
       }
     }
   }
@@ -201,12 +235,29 @@ int catgnn_shard_gather_features(catgnn_shard s, catgnn_features f) {
     if (f->ctx->stream != st && f->has_upload) CG_CUDA(cudaStreamWaitEvent(st, f->uploaded, 0));
     const unsigned grid = (unsigned)std::min<uint64_t>((s->rows + 7) / 8, (uint64_t)s->ctx->num_sms * 8);
     const int t = s->ctx->begin_timed(2, s->ctx->timing ? "K6 feature gather d" + std::to_string(f->dim) : std::string());
+    // a shard a bf16x3 model has read keeps its split copy current from here;
+    // with the split-only layout it is the only copy written
+    const uint32_t sld = round_up(f->dim, 8);
+    if (s->x_split_only && (!s->xs_hi.p || s->xs_ld != sld)) {
+      const size_t n = std::max<uint64_t>(1, s->rows) * sld;
+      s->xs_hi.alloc(n);
+      s->xs_lo.alloc(n);
+      s->xs_ld = sld;
+      CG_CUDA(cudaMemsetAsync(s->xs_hi.p, 0, n * 2, st));  // zero padding columns
+      CG_CUDA(cudaMemsetAsync(s->xs_lo.p, 0, n * 2, st));
+    }
+    const bool split = s->xs_hi.p && s->xs_ld == sld;
+    float* xdst = (s->x_split_only && split) ? nullptr : s->x.p;
+    auto* hi = split ? reinterpret_cast<__nv_bfloat16*>(s->xs_hi.p) : nullptr;
+    auto* lo = split ? reinterpret_cast<__nv_bfloat16*>(s->xs_lo.p) : nullptr;
     if (f->dim % 4 == 0)
-      gather_rows_kernel<4><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
+      gather_rows_kernel<4><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, xdst, ld, hi, lo, s->xs_ld);
     else if (f->dim % 2 == 0)
-      gather_rows_kernel<2><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
+      gather_rows_kernel<2><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, xdst, ld, hi, lo, s->xs_ld);
     else
-      gather_rows_kernel<1><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, s->x.p, ld);
+      gather_rows_kernel<1><<<grid, 256, 0, st>>>(f->x.p, f->dim, s->d_ext.p, s->rows, xdst, ld, hi, lo, s->xs_ld);
+    if (split) s->xs_version = s->x_version;
+    s->x_fp32_valid = xdst != nullptr;
     CG_CHECK_LAUNCH();
     s->ctx->end_timed(t);
     s->ctx->launches++;
@@ -269,11 +320,11 @@ int catgnn_split_features(catgnn_ctx ctx, catgnn_artifact a, const char* feature
         CG_CUDA(cudaMemcpyAsync(ids.p, ext.data(), rows * 8, cudaMemcpyHostToDevice, st));
         const unsigned grid = (unsigned)std::min<uint64_t>((rows + 7) / 8, (uint64_t)ctx->num_sms * 8);
         if (h.dim % 4 == 0)
-          gather_rows_kernel<4><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim);
+          gather_rows_kernel<4><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim, nullptr, nullptr, 0);
         else if (h.dim % 2 == 0)
-          gather_rows_kernel<2><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim);
+          gather_rows_kernel<2><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim, nullptr, nullptr, 0);
         else
-          gather_rows_kernel<1><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim);
+          gather_rows_kernel<1><<<grid, 256, 0, st>>>(src.p, h.dim, ids.p, rows, dst.p, h.dim, nullptr, nullptr, 0);
         CG_CHECK_LAUNCH();
         ctx->launches++;
         CG_CUDA(cudaMemcpyAsync(pinned, dst.p, rows * (size_t)h.dim * 4, cudaMemcpyDeviceToHost, st));
@@ -294,5 +345,19 @@ int catgnn_split_features(catgnn_ctx ctx, catgnn_artifact a, const char* feature
       ++written;
     }
     if (files_written) *files_written = written;
+  });
+}
+
+// Feature layout of a shard (no reference counterpart: a device-memory layout
+// choice).  split_only = 1: catgnn_shard_gather_features writes only the
+// bf16x3 (hi, lo) copy the GNN layers' tensor-core GEMMs read, not the fp32
+// rows; calls that need fp32 features (SGC propagation, feature export, a
+// model whose first layer is not on the bf16x3 path) fail with ConfigError
+// until the next catgnn_shard_upload_features.
+int catgnn_shard_set_feature_layout(catgnn_shard s, int split_only) {
+  return guarded([&] {
+    if (!s) throw ConfigError("null shard");
+    CG_CUDA(cudaSetDevice(s->ctx->device));
+    s->x_split_only = split_only != 0;
   });
 }

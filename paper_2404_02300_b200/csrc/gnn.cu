@@ -479,6 +479,7 @@ Split act16(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld)
 Split shard_x_split(catgnn_shard_s* S) {
   const uint32_t ld = round_up(std::max<uint32_t>(S->dim, 1), 8);
   if (S->xs_version != S->x_version || S->xs_ld != ld || !S->xs_hi.p) {
+    if (!S->x_fp32_valid) throw InternalError("bf16x3 feature copy is stale and the fp32 rows are not held");
     const size_t n = std::max<uint64_t>(1, S->rows) * ld;
     if (S->xs_ld != ld || !S->xs_hi.p) {
       S->xs_hi.alloc(n);
@@ -525,6 +526,8 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
   const bool fresh = M->last_rows != rows;
   split_weights(M);
   M->h_split_only.assign(M->layers.size(), false);
+  if (!S->x_fp32_valid && !bf_layer(M, 0))
+    throw ConfigError("shard features are held as bf16x3 only; this model's first layer reads fp32 features");
   for (size_t l = 0; l < M->layers.size(); ++l) {
     const Layer& L = M->layers[l];
     const bool last = l + 1 == M->layers.size();

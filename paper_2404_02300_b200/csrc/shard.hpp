@@ -42,6 +42,9 @@ struct catgnn_shard_s {
   catgnn::DevBuf<uint16_t> xs_hi, xs_lo;
   uint32_t xs_ld = 0;
   uint64_t x_version = 1, xs_version = 0;
+  // catgnn_shard_set_feature_layout(split_only): feature gathers write only the
+  // bf16x3 copy; fp32 x is then stale (x_fp32_valid) until the next upload
+  bool x_split_only = false, x_fp32_valid = true;
   // labels / roles (host copies + device copies)
   std::vector<int32_t> h_labels;
   std::vector<uint32_t> h_train, h_val, h_test;

@@ -246,6 +246,10 @@ class Shard:
         f = np.ascontiguousarray(features, np.float32)
         check(lib.catgnn_shard_upload_features(self.handle, _ptr(f), f.shape[1]))
 
+    def set_feature_layout(self, split_only: bool):
+        """catgnn_shard_set_feature_layout: gathers write only the bf16x3 copy."""
+        check(lib.catgnn_shard_set_feature_layout(self.handle, int(split_only)))
+
     def gather_features(self, store: "FeatureStore"):
         """x[r] = F[ext_id(r)] on the device (train.cpp:277-283)."""
         check(lib.catgnn_shard_gather_features(self.handle, store.handle))

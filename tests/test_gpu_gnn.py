@@ -180,17 +180,34 @@ def test_e2e_feature_gather_path_identical(tmp_path_factory):
     store = gp.FeatureStore(X.shape[0], X.shape[1], copy_ctx)
     store.upload(X)
     res = []
-    for mode in ("resident", "gathered"):
+    for mode in ("resident", "gathered", "gathered_split", "split_only"):
         data = gp.load_training_data(art, ctx=ctx)
-        if mode == "gathered":
+        if mode == "split_only":  # gathers write only the bf16x3 copy
+            for s in data.shards:
+                s.set_feature_layout(True)
+        if mode == "gathered_split":
+            # a bf16x3 model has read the shards: from then on the gather writes
+            # their (hi, lo) copy itself (no separate split pass)
+            warm = gnn.GNNModel("gcn", 2, X.shape[1], 32, 5, seed=2, ctx=ctx)
+            for s in data.shards:
+                warm.forward(s)
+        if mode != "resident":
             for s in data.shards:
                 s.upload_features(np.zeros((s.rows, X.shape[1]), np.float32))
                 s.gather_features(store)
         counts = [int(s.info.n_train) for s in data.shards]
         r = gnn.distributed_train("gcn", data.shards, counts, 1, 3, 2, 32, 5, seed=2, ctx=ctx)
         res.append(r)
-    assert res[0].losses == res[1].losses
-    assert np.array_equal(res[0].params, res[1].params)
+    for r in res[1:]:
+        assert res[0].losses == r.losses
+        assert np.array_equal(res[0].params, r.params)
+    # fp32 features are not held in the split-only layout: fp32 consumers refuse
+    with pytest.raises(gp.ConfigError, match="bf16x3"):
+        gp.sgc_propagate(data.shards[0], 1)
+    with pytest.raises(gp.ConfigError, match="bf16x3"):
+        gnn.GNNModel("sage", 2, X.shape[1], 32, 5, ctx=ctx).forward(data.shards[0])
+    data.shards[0].upload_features(np.zeros((data.shards[0].rows, X.shape[1]), np.float32))
+    gp.sgc_propagate(data.shards[0], 1)  # fp32 rows held again after an upload
 
 
 def test_last_loss_matches_synchronous_loss(graph):
