@@ -307,6 +307,11 @@ typedef struct {
 } catgnn_model_config;
 int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_model* out);
 int catgnn_model_destroy(catgnn_model m);
+/* Storage of the aggregation inputs (no reference counterpart; numerics only):
+ * on (default, env CATGNN_ACT_F16=0 turns it off) the GCN backward gradients
+ * and last-layer logits inputs are gathered as fp16 rows (fp32 accumulation,
+ * ~2e-4 relative on gradients), off keeps every K2 input fp32. */
+int catgnn_model_set_act_f16(catgnn_model m, int on);
 uint64_t catgnn_model_num_params(catgnn_model m);
 /* Flat parameter vector: per layer W (row-major, shape given by
  * catgnn_model_layer_shape) followed by b. */

@@ -97,6 +97,7 @@ def _load():
         "catgnn_distributed_train": (C.c_int, [u32, vp, vp, u32, u32, vp, vp]),
         "catgnn_model_create": (C.c_int, [vp, vp, P(vp)]),
         "catgnn_model_destroy": (C.c_int, [vp]),
+        "catgnn_model_set_act_f16": (C.c_int, [vp, C.c_int]),
         "catgnn_model_num_params": (u64, [vp]),
         "catgnn_model_layer_shape": (C.c_int, [vp, u32, P(u32), P(u32), P(u64), P(u64)]),
         "catgnn_model_get_params": (C.c_int, [vp, vp]),

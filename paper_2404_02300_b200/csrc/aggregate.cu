@@ -25,6 +25,7 @@
 #include <string>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "shard.hpp"
 
@@ -43,7 +44,9 @@ struct AggKernelArgs {
   float* __restrict__ partials;  // [n_chunks][w4*4]
   uint32_t U;
   const float* __restrict__ in;
+  const __half* __restrict__ in_h;  // fp16 input rows instead of `in` (in_ld / in_col in halves)
   uint32_t in_ld, in_col;
+  float in_scale;                   // folded into the post scale (fp16 inputs stored scaled by 1/in_scale)
   float* __restrict__ out;
   uint32_t out_ld, out_col;
   uint32_t w4;
@@ -87,6 +90,46 @@ __device__ __forceinline__ void add4(float4& a, const float4& v) {
   add2(a.x, a.y, v.x, v.y);
   add2(a.z, a.w, v.z, v.w);
 }
+// 8 fp16 columns -> two float4 (exact)
+__device__ __forceinline__ void h8_to_f4(const uint4& r, float4& a, float4& b) {
+  const float2 x0 = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+  const float2 x1 = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+  const float2 x2 = __half22float2(*reinterpret_cast<const __half2*>(&r.z));
+  const float2 x3 = __half22float2(*reinterpret_cast<const __half2*>(&r.w));
+  a = make_float4(x0.x, x0.y, x1.x, x1.y);
+  b = make_float4(x2.x, x2.y, x3.x, x3.y);
+}
+// One gathered 16-byte vector (CPV = 1: 4 fp32 columns, 2: 8 fp16 columns)
+// into the accumulators a[0, CPV).
+template <int CPV, bool PRE>
+__device__ __forceinline__ void acc_raw(float4* a, const uint4& r, float s) {
+  if constexpr (CPV == 1) {
+    const float4 v = make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
+    if (PRE) fma4(a[0], s, v);
+    else add4(a[0], v);
+  } else {
+    float4 v0, v1;
+    h8_to_f4(r, v0, v1);
+    if (PRE) { fma4(a[0], s, v0); fma4(a[1], s, v1); }
+    else { add4(a[0], v0); add4(a[1], v1); }
+  }
+}
+template <int CPV>
+__device__ __forceinline__ void raw_to_f4(float4* a, const uint4& r) {
+  if constexpr (CPV == 1) a[0] = make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
+  else h8_to_f4(r, a[0], a[1]);
+}
+// The row's own input columns [4 c4, 4 c4 + 4) (fp32 or fp16 rows)
+__device__ __forceinline__ float4 self4(const AggKernelArgs& p, int64_t r, uint32_t c4) {
+  if (p.in_h) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p.in_h + (size_t)r * p.in_ld + p.in_col + c4 * 4));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  return __ldg(reinterpret_cast<const float4*>(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4));
+}
+
 __device__ __forceinline__ float4 shfl_xor4(const float4& v, int m) {
   return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
@@ -108,98 +151,109 @@ __device__ __forceinline__ float post_scale(int norm, float deg) {
 }
 
 // Final epilogue for one output row.  `acc` holds the neighbour sum for the
-// float4 columns c4 = li + LPN*q.
+// float4 columns c4 = (li + LPN*q)*CPV + h at acc[q*CPV + h] (CPV = 2 for fp16
+// input rows: a 16-byte vector then carries 8 columns).
 // selfv: the row's own input columns when already loaded (light units).
-template <int VPL, int LPN, bool BITS>
+template <int VPL, int LPN, bool BITS, int CPV>
 __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, float deg,
-                                             const float4 (&acc)[VPL], int li,
-                                             const float4 (*selfv)[VPL] = nullptr) {
+                                             const float4 (&acc)[VPL * CPV], int li,
+                                             const float4 (*selfv)[VPL * CPV] = nullptr) {
   // lanes [0, LPN) run this together (bit words are assembled across them)
   constexpr unsigned kLanes = LPN == 32 ? 0xffffffffu : ((1u << LPN) - 1u);
-  constexpr int kGroup = LPN < 8 ? LPN : 8;  // lanes whose nibbles form one 32-bit word
-  const float post = post_scale(p.norm, deg);
+  constexpr int kGroup = LPN < 8 / CPV ? LPN : 8 / CPV;  // lanes whose nibbles form one 32-bit word
+  const float post = post_scale(p.norm, deg) * p.in_scale;
   const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
-  uint32_t nib[VPL];  // (out > 0) per column of each float4, for bits_out
+  uint32_t nib[VPL * CPV];  // (out > 0) per column of each float4, for bits_out
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) {
-    const uint32_t c4 = li + LPN * q;
-    nib[q] = 0;
-    if (c4 >= p.w4) continue;
-    float4 a = acc[q];
-    if (p.self) fma4(a, selfs, selfv ? (*selfv)[q] : ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4));
-    a.x *= post; a.y *= post; a.z *= post; a.w *= post;
-    if (p.residual) add4(a, ldg4(p.residual + (size_t)r * p.res_ld + p.res_col + c4 * 4));
-    if (p.bias) add4(a, ldg4(p.bias + c4 * 4));
-    if (p.relu) {
-      a.x = fmaxf(a.x, 0.f); a.y = fmaxf(a.y, 0.f); a.z = fmaxf(a.z, 0.f); a.w = fmaxf(a.w, 0.f);
+  for (int q = 0; q < VPL; ++q)
+#pragma unroll
+    for (int h = 0; h < CPV; ++h) {
+      const int k = q * CPV + h;
+      const uint32_t c4 = (li + LPN * q) * CPV + h;
+      nib[k] = 0;
+      if (c4 >= p.w4) continue;
+      float4 a = acc[k];
+      if (p.self) fma4(a, selfs, selfv ? (*selfv)[k] : self4(p, r, c4));
+      a.x *= post; a.y *= post; a.z *= post; a.w *= post;
+      if (p.residual) add4(a, ldg4(p.residual + (size_t)r * p.res_ld + p.res_col + c4 * 4));
+      if (p.bias) add4(a, ldg4(p.bias + c4 * 4));
+      if (p.relu) {
+        a.x = fmaxf(a.x, 0.f); a.y = fmaxf(a.y, 0.f); a.z = fmaxf(a.z, 0.f); a.w = fmaxf(a.w, 0.f);
+      }
+      if (BITS && p.mask_bits) {  // ReLU backward: bit (r, col) of the forward activation
+        const uint32_t m = __ldg(p.mask_bits + (size_t)r * p.mask_words + c4 / 8) >> ((c4 % 8) * 4);
+        a.x = (m & 1u) ? a.x : 0.f; a.y = (m & 2u) ? a.y : 0.f;
+        a.z = (m & 4u) ? a.z : 0.f; a.w = (m & 8u) ? a.w : 0.f;
+      }
+      if (BITS) nib[k] = (a.x > 0.f) | ((a.y > 0.f) << 1) | ((a.z > 0.f) << 2) | ((a.w > 0.f) << 3);
+      if (p.out) {
+        float4* dst = reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4);
+        if (p.stream_hint) __stcs(dst, a);  // evict-first: keep L2 for the gathered rows
+        else *dst = a;
+      }
+      if (p.out_hi) {  // hi = bf16(v), lo = bf16(v - hi): the next GEMM's pre-split operand
+        const __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+        const __nv_bfloat162 l0 = __floats2bfloat162_rn(a.x - __low2float(h0), a.y - __high2float(h0));
+        const __nv_bfloat162 l1 = __floats2bfloat162_rn(a.z - __low2float(h1), a.w - __high2float(h1));
+        const size_t o = ((size_t)r * p.out_s_ld + c4 * 4) / 4;
+        p.out_hi[o] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+        p.out_lo[o] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+      }
     }
-    if (BITS && p.mask_bits) {  // ReLU backward: bit (r, col) of the forward activation
-      const uint32_t m = __ldg(p.mask_bits + (size_t)r * p.mask_words + c4 / 8) >> ((c4 % 8) * 4);
-      a.x = (m & 1u) ? a.x : 0.f; a.y = (m & 2u) ? a.y : 0.f;
-      a.z = (m & 4u) ? a.z : 0.f; a.w = (m & 8u) ? a.w : 0.f;
-    }
-    if (BITS) nib[q] = (a.x > 0.f) | ((a.y > 0.f) << 1) | ((a.z > 0.f) << 2) | ((a.w > 0.f) << 3);
-    if (p.out) {
-      float4* dst = reinterpret_cast<float4*>(p.out + (size_t)r * p.out_ld + p.out_col + c4 * 4);
-      if (p.stream_hint) __stcs(dst, a);  // evict-first: keep L2 for the gathered rows
-      else *dst = a;
-    }
-    if (p.out_hi) {  // hi = bf16(v), lo = bf16(v - hi): the next GEMM's pre-split operand
-      const __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
-      const __nv_bfloat162 l0 = __floats2bfloat162_rn(a.x - __low2float(h0), a.y - __high2float(h0));
-      const __nv_bfloat162 l1 = __floats2bfloat162_rn(a.z - __low2float(h1), a.w - __high2float(h1));
-      const size_t o = ((size_t)r * p.out_s_ld + c4 * 4) / 4;
-      p.out_hi[o] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
-      p.out_lo[o] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
-    }
-  }
   if (BITS && p.bits_out) {  // 1 bit per output element (> 0): the next backward's ReLU mask
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
-      const uint32_t c4 = li + LPN * q;
-      uint32_t w = nib[q] << ((c4 % 8) * 4);
+      const uint32_t c40 = (li + LPN * q) * CPV;
+      uint32_t w = 0;
+#pragma unroll
+      for (int h = 0; h < CPV; ++h) w |= nib[q * CPV + h] << (((c40 + h) % 8) * 4);
 #pragma unroll
       for (int m = 1; m < kGroup; m <<= 1) w |= __shfl_xor_sync(kLanes, w, m);
-      if (c4 < p.w4 && c4 % 8 == 0) p.bits_out[(size_t)r * p.bits_words + c4 / 8] = w;
+      if (c40 < p.w4 && c40 % 8 == 0) p.bits_out[(size_t)r * p.bits_words + c40 / 8] = w;
     }
   }
 }
 
-// Lane base address of the gathered rows: row j's float4 column c4 = li +
-// LPN*q sits at base + j*ldb + q*LPN*16 (one IMAD.WIDE per neighbour, the q
-// offset an immediate).
+// Lane base address of the gathered rows: row j's 16-byte vector li + LPN*q
+// sits at base + j*ldb + q*LPN*16 (one IMAD.WIDE per neighbour, the q offset
+// an immediate).  fp16 rows (CPV = 2) hold 8 columns per vector.
+template <int CPV>
 __device__ __forceinline__ const char* lane_base(const AggKernelArgs& p, int li) {
-  return reinterpret_cast<const char*>(p.in + p.in_col) + li * 16;
+  if constexpr (CPV == 2) return reinterpret_cast<const char*>(p.in_h + p.in_col) + li * 16;
+  else return reinterpret_cast<const char*>(p.in + p.in_col) + li * 16;
 }
+template <int CPV>
+__device__ __forceinline__ uint32_t row_bytes(const AggKernelArgs& p) { return p.in_ld * (CPV == 2 ? 2u : 4u); }
+template <int CPV>
+__device__ __forceinline__ uint32_t n_vec(const AggKernelArgs& p) { return CPV == 2 ? (p.w4 + 1) / 2 : p.w4; }
 template <int VPL, int LPN>
-__device__ __forceinline__ float4 ld_nbr(const char* base, uint32_t ldb, int j, int q) {
-  return __ldg(reinterpret_cast<const float4*>(base + (uint64_t)(uint32_t)j * ldb + q * LPN * 16));
+__device__ __forceinline__ uint4 ld_nbr(const char* base, uint32_t ldb, int j, int q) {
+  return __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)(uint32_t)j * ldb + q * LPN * 16));
 }
 
 // Sum of pre[j]*in[j] over edges [e0, e1) into acc (reduced across groups).
 // Loads past the end of the range, and by lanes whose columns lie past the
 // row width, are skipped and contribute zeros.
-template <int VPL, int LPN, bool PRE>
+template <int VPL, int LPN, bool PRE, int CPV>
 __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64_t e1,
-                                       float4 (&acc)[VPL], int lane) {
+                                       float4 (&acc)[VPL * CPV], int lane) {
   constexpr int G = 32 / LPN;  // neighbours processed side by side
-  constexpr int UNROLL = VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8);
+  constexpr int UNROLL = VPL * CPV >= 4 ? 2 : (VPL * CPV >= 2 ? 4 : 8);
   const int g = lane / LPN, li = lane % LPN;
-  const char* base = lane_base(p, li);
-  const uint32_t ldb = p.in_ld * 4;
+  const char* base = lane_base<CPV>(p, li);
+  const uint32_t ldb = row_bytes<CPV>(p);
   bool colok[VPL];
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) {
-    colok[q] = li + LPN * q < (int)p.w4;
-    acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  for (int q = 0; q < VPL; ++q) colok[q] = li + LPN * q < (int)n_vec<CPV>(p);
+#pragma unroll
+  for (int k = 0; k < VPL * CPV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t e = e0; e < e1; e += 32) {
     const int n = (int)((e1 - e) < 32 ? (e1 - e) : 32);
     const int myj = lane < n ? ld_col(p, e + lane) : 0;
     float mys = 1.0f;
     if (PRE) mys = lane < n ? __ldg(p.pre + myj) : 0.0f;
     for (int kb = 0; kb < n; kb += G * UNROLL) {
-      float4 v[UNROLL][VPL];
+      uint4 v[UNROLL][VPL];
       float s[UNROLL];
       bool ok[UNROLL];
 #pragma unroll
@@ -210,21 +264,18 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
         ok[u] = kk < n;
 #pragma unroll
         for (int q = 0; q < VPL; ++q)
-          v[u][q] = (ok[u] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u][q] = (ok[u] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          if (PRE) fma4(acc[q], s[u], v[u][q]);
-          else add4(acc[q], v[u][q]);
-        }
+        for (int q = 0; q < VPL; ++q) acc_raw<CPV, PRE>(acc + q * CPV, v[u][q], s[u]);
     }
   }
 #pragma unroll
   for (int m = LPN; m < 32; m <<= 1)
 #pragma unroll
-    for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], m));
+    for (int k = 0; k < VPL * CPV; ++k) add4(acc[k], shfl_xor4(acc[k], m));
 }
 
 // A light unit (whole rows [r0, r1), edges contiguous in col[]) walked as one
@@ -234,7 +285,7 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
 // 32 rows per coalesced load and each row's own input row (self term) is
 // requested together with its first neighbour batch.  Per row the G lane
 // groups split the neighbours, UNROLL batches in flight, xor-shuffle reduce.
-template <int VPL, int LPN, bool PRE, bool BITS>
+template <int VPL, int LPN, bool PRE, bool BITS, int CPV>
 __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, int64_t r1, int lane) {
   constexpr int G = 32 / LPN;
 #ifndef AGG_NARROW_UNROLL
@@ -243,7 +294,11 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 #ifndef AGG_WIDE_UNROLL
 #define AGG_WIDE_UNROLL 6
 #endif
-  constexpr int UNROLL0 = (LPN < 32 && VPL == 2) ? AGG_NARROW_UNROLL
+#ifndef AGG_H16_WIDE_UNROLL
+#define AGG_H16_WIDE_UNROLL 8
+#endif
+  constexpr int UNROLL0 = CPV == 2 ? (LPN < 32 ? AGG_NARROW_UNROLL : (VPL == 1 ? AGG_H16_WIDE_UNROLL : (VPL == 2 ? AGG_WIDE_UNROLL : 2)))
+                          : (LPN < 32 && VPL == 2) ? AGG_NARROW_UNROLL
                           : (LPN == 32 && VPL == 2) ? AGG_WIDE_UNROLL
                                                     : (VPL >= 4 ? 2 : (VPL >= 2 ? 4 : 8));
   constexpr int UNROLL = G * UNROLL0 > 32 ? 32 / G : UNROLL0;
@@ -260,11 +315,11 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
     curs = (cb + lane < E1) ? __ldg(p.pre + cur) : 0.f;
     nxts = (cb + 32 + lane < E1) ? __ldg(p.pre + nxt) : 0.f;
   }
-  const char* base = lane_base(p, li);
-  const uint32_t ldb = p.in_ld * 4;
+  const char* base = lane_base<CPV>(p, li);
+  const uint32_t ldb = row_bytes<CPV>(p);
   bool colok[VPL];
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) colok[q] = li + LPN * q < (int)p.w4;
+  for (int q = 0; q < VPL; ++q) colok[q] = li + LPN * q < (int)n_vec<CPV>(p);
   for (int64_t rb = r0; rb < r1; rb += 32) {
     const int64_t rr = rb + lane;
     const int64_t rpa = rr < r1 ? __ldg(p.row_ptr + rr) : 0;
@@ -276,16 +331,15 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 #ifdef AGG_SKIP_SHORT  // diagnostics build: the cost of short rows (wrong results)
       if (e1 - e0 < AGG_SKIP_SHORT) continue;
 #endif
-      float4 selfv[VPL];
+      float4 selfv[VPL * CPV];
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
-        const uint32_t c4 = li + LPN * q;
-        selfv[q] = (p.self && writer && c4 < p.w4) ? ldg4(p.in + (size_t)r * p.in_ld + p.in_col + c4 * 4)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        const uint4 sv = (p.self && writer && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, (int)r, q) : make_uint4(0u, 0u, 0u, 0u);
+        raw_to_f4<CPV>(selfv + q * CPV, sv);
       }
-      float4 acc[VPL];
+      float4 acc[VPL * CPV];
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < VPL * CPV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int64_t e = e0; e < e1; e += B) {
         while (e >= cb + 32) {  // warp-uniform: advance the index window by one chunk
           cb += 32;
@@ -295,7 +349,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
           nxt = ok ? ld_col(p, cb + 32 + lane) : 0;
           if (PRE) nxts = ok ? __ldg(p.pre + nxt) : 0.f;
         }
-        float4 v[UNROLL][VPL];
+        uint4 v[UNROLL][VPL];
         float s[UNROLL];
         bool ok[UNROLL];
         if constexpr (G == 1) {
@@ -319,7 +373,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             ok[uu] = uu < rem;
 #pragma unroll
             for (int q = 0; q < VPL; ++q)
-              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
           }
         } else {
           // lane groups: two shuffles per neighbour keep the register budget
@@ -341,29 +395,26 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             ok[uu] = ee < e1;
 #pragma unroll
             for (int q = 0; q < VPL; ++q)
-              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
           }
         }
 #pragma unroll
         for (int uu = 0; uu < UNROLL; ++uu)
 #pragma unroll
-          for (int q = 0; q < VPL; ++q) {
-            if (PRE) fma4(acc[q], s[uu], v[uu][q]);
-            else add4(acc[q], v[uu][q]);
-          }
+          for (int q = 0; q < VPL; ++q) acc_raw<CPV, PRE>(acc + q * CPV, v[uu][q], s[uu]);
       }
 #pragma unroll
       for (int m = LPN; m < 32; m <<= 1)
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) add4(acc[q], shfl_xor4(acc[q], m));
-      if (writer) epilogue_row<VPL, LPN, BITS>(p, r, (float)(e1 - e0), acc, li, &selfv);
+        for (int k = 0; k < VPL * CPV; ++k) add4(acc[k], shfl_xor4(acc[k], m));
+      if (writer) epilogue_row<VPL, LPN, BITS, CPV>(p, r, (float)(e1 - e0), acc, li, &selfv);
     }
   }
 }
 
 // Persistent unit loop shared by both aggregation kernels: warps pull work
 // units from the atomic counter (the next one prefetched by lane 0).
-template <int VPL, int LPN, bool PRE, bool BITS>
+template <int VPL, int LPN, bool PRE, bool BITS, int CPV>
 __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
   const int lane = threadIdx.x & 31;
   const int li = lane % LPN;
@@ -376,21 +427,23 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
     if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
     const int4 w = __ldg(p.units + u);
     if (w.z < 0) {
-      light_unit<VPL, LPN, PRE, BITS>(p, w.x, w.y, lane);
+      light_unit<VPL, LPN, PRE, BITS, CPV>(p, w.x, w.y, lane);
     } else {
-      float4 acc[VPL];
+      float4 acc[VPL * CPV];
       const int64_t r = w.x;
       const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
       const int64_t e0 = rb + (int64_t)w.y * p.U;
       const int64_t e1 = (re < e0 + (int64_t)p.U) ? re : e0 + (int64_t)p.U;
-      gather<VPL, LPN, PRE>(p, e0, e1, acc, lane);
+      gather<VPL, LPN, PRE, CPV>(p, e0, e1, acc, lane);
       if (writer) {
         float* dst = p.partials + (size_t)w.z * p.w4 * 4;
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          const uint32_t c4 = li + LPN * q;
-          if (c4 < p.w4) *reinterpret_cast<float4*>(dst + c4 * 4) = acc[q];
-        }
+        for (int q = 0; q < VPL; ++q)
+#pragma unroll
+          for (int h = 0; h < CPV; ++h) {
+            const uint32_t c4 = (li + LPN * q) * CPV + h;
+            if (c4 < p.w4) *reinterpret_cast<float4*>(dst + c4 * 4) = acc[q * CPV + h];
+          }
       }
     }
     u = __shfl_sync(0xffffffffu, next, 0);
@@ -399,9 +452,10 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
 
 // BITS: the epilogue reads / writes ReLU bit masks (a separate instantiation
 // keeps the plain passes' register budget: the narrow kernel runs at 64).
-template <int VPL, int LPN, bool PRE, int MINB, bool BITS>
+// CPV = 2: fp16 input rows.
+template <int VPL, int LPN, bool PRE, int MINB, bool BITS, int CPV>
 __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
-  unit_loop<VPL, LPN, PRE, BITS>(p);
+  unit_loop<VPL, LPN, PRE, BITS, CPV>(p);
 }
 
 // One CTA per split row.  Warp w sums the row's chunk partials c = w, w+8,
@@ -457,7 +511,7 @@ __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
         acc[q] = t;
       }
       const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
-      epilogue_row<VPL, 32, true>(p, r, deg, acc, lane);
+      epilogue_row<VPL, 32, true, 1>(p, r, deg, acc, lane);
     }
     __syncthreads();
   }
@@ -480,15 +534,34 @@ AggFn pick_pre(bool pre, bool bits) {
 #define AGG_WIDE_MINB 3
 #endif
   constexpr int MINB = LPN < 32 ? AGG_NARROW_MINB : AGG_WIDE_MINB;
-  if (bits) return pre ? agg_kernel<VPL, LPN, true, 3, true> : agg_kernel<VPL, LPN, false, 3, true>;
-  return pre ? agg_kernel<VPL, LPN, true, MINB, false> : agg_kernel<VPL, LPN, false, MINB, false>;
+  if (bits) return pre ? agg_kernel<VPL, LPN, true, 3, true, 1> : agg_kernel<VPL, LPN, false, 3, true, 1>;
+  return pre ? agg_kernel<VPL, LPN, true, MINB, false, 1> : agg_kernel<VPL, LPN, false, MINB, false, 1>;
+}
+// fp16 input rows (the source scale is folded into the producer: no PRE)
+template <int VPL, int LPN>
+AggFn pick_h16(bool bits) {
+  constexpr int MINB = LPN < 32 ? AGG_NARROW_MINB : AGG_WIDE_MINB;
+  return bits ? agg_kernel<VPL, LPN, false, 3, true, 2> : agg_kernel<VPL, LPN, false, MINB, false, 2>;
 }
 
 // Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
 constexpr uint32_t kMaxSlab4 = 256;
 
 
-AggFn pick_kernel(uint32_t w4, bool pre, bool bits, int* lpn_out) {
+AggFn pick_kernel(uint32_t w4, bool pre, bool bits, bool h16, int* lpn_out) {
+  if (h16) {  // 16-byte vectors of 8 halves: 48-wide class rows = 6 of 8 lanes (4 neighbours per load)
+    const uint32_t w8 = (w4 + 1) / 2;
+    if (w8 <= 4) { *lpn_out = 4; return pick_h16<1, 4>(bits); }
+    if (w8 <= 8) { *lpn_out = 8; return pick_h16<1, 8>(bits); }
+    if (w8 <= 16) { *lpn_out = 16; return pick_h16<1, 16>(bits); }
+    *lpn_out = 32;
+    switch ((w8 + 31) / 32) {
+      case 1: return pick_h16<1, 32>(bits);
+      case 2: return pick_h16<2, 32>(bits);
+      case 3: return pick_h16<3, 32>(bits);
+      default: return pick_h16<4, 32>(bits);
+    }
+  }
   // lanes per neighbour x float4 per lane; the narrow class rows (41-48 floats)
   // use 8 lanes x 2 float4 (4 neighbours per load instruction)
   if (w4 <= 4) { *lpn_out = 4; return pick_pre<1, 4>(pre, bits); }
@@ -553,6 +626,8 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
   if (a.in == a.out && a.in && a.in_ld != a.out_ld) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
   if (!a.out && !a.out_hi) throw ConfigError("aggregation needs an output");
+  if (a.in_h && (a.in || a.pre || a.in_ld % 8 || a.in_col % 8 || a.in_ld < a.in_col + round_up(a.width, 8)))
+    throw ConfigError("fp16 aggregation input: no fp32 input / source scale, row stride and column a multiple of 8");
   if (a.out_hi && (!a.out_lo || a.out_s_ld % 8 || a.out_s_ld < a.width))
     throw ConfigError("bf16 aggregation output needs hi and lo rows of >= width elements, a multiple of 8");
   const uint32_t W4 = a.width / 4;
@@ -570,6 +645,8 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
                              : nullptr;
     p.U = s->unit_cost;
     p.in = a.in;
+    p.in_h = static_cast<const __half*>(a.in_h);
+    p.in_scale = a.in_scale;
     p.in_ld = a.in_ld;
     p.in_col = a.in_col + c4 * 4;
     p.out = a.out;
@@ -596,10 +673,11 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     static const int hint = env_int("CATGNN_AGG_HINT", 1);
     p.stream_hint = hint;
     int lpn = 32;
-    AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, &lpn);
+    AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, a.in_h != nullptr, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
     static const int detail = env_int("CATGNN_TIMING_DETAIL", 0);  // label per shard (rows)
-    int t = ctx->begin_timed(0, ctx->timing ? "K2 agg w" + std::to_string(w4 * 4) + (a.pre ? " pre" : "") +
+    int t = ctx->begin_timed(0, ctx->timing ? "K2 agg w" + std::to_string(w4 * 4) + (a.in_h ? " f16" : "") +
+                                                   (a.pre ? " pre" : "") +
                                                    (a.mask_bits || a.bits_out ? " bits" : "") +
                                                    (detail ? " rows=" + std::to_string(s->rows) : std::string())
                                              : std::string());

@@ -314,7 +314,15 @@ __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint3
   if (e.bias) v += __ldg(e.bias + col);
   if (e.relu) v = fmaxf(v, 0.f);
   if (e.mask_bits && !((__ldg(e.mask_bits + (size_t)row * e.mask_words + col / 32) >> (col % 32)) & 1u)) v = 0.f;
-  return v;
+  return v * e.out_scale;
+}
+__device__ __forceinline__ void store_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
+  if (e.out_h) e.out_h[(size_t)row * e.ld_out + e.out_col + col] = __float2half_rn(v);
+  else e.out[(size_t)row * e.ld_out + e.out_col + col] = v;
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, uint32_t t, uint32_t& m0, uint32_t& n0,
@@ -629,7 +637,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
         // written (a multiple of 4 columns)
         const uint32_t ns = max(args.N, e.store_cols);
         const uint32_t nc = min(32u, ns - col0);
-        if (!e.partial && (nc == 32 || (e.store_cols && nc % 4 == 0))) {
+        if (!e.partial && (nc == 32 || (e.store_cols && nc % (e.out_h ? 8 : 4) == 0))) {
           const uint32_t mw = mrow ? mw_cur : 0xffffffffu;
           uint32_t bw = 0;
 #pragma unroll
@@ -648,13 +656,24 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
               o.x = (nib & 1u) ? o.x : 0.f; o.y = (nib & 2u) ? o.y : 0.f;
               o.z = (nib & 4u) ? o.z : 0.f; o.w = (nib & 8u) ? o.w : 0.f;
             }
+            o.x *= e.out_scale; o.y *= e.out_scale; o.z *= e.out_scale; o.w *= e.out_scale;
             bw |= ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3)) << (4 * i);
             T[lane * kTileLd4 + i] = o;
           }
           if (nc < 32) bw &= (1u << nc) - 1u;  // staged columns past the stored ones are not results
           if (e.bits_out && row_ok) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
           __syncwarp();
-          if (nc == 32) {
+          if (e.out_h) {  // fp16 rows: nc/8 16-byte vectors per row, consecutive lanes along the row
+            const uint32_t n8 = nc / 8;
+            for (uint32_t f = lane; f < 32 * n8; f += 32) {
+              const uint32_t rr = f / n8, cc = f % n8, grow = rbase + rr;
+              if (grow < args.M) {
+                const float4 a = T[rr * kTileLd4 + 2 * cc], b = T[rr * kTileLd4 + 2 * cc + 1];
+                reinterpret_cast<uint4*>(e.out_h + (size_t)grow * e.ld_out + e.out_col + col0)[cc] =
+                    make_uint4(pack_h2(a.x, a.y), pack_h2(a.z, a.w), pack_h2(b.x, b.y), pack_h2(b.z, b.w));
+              }
+            }
+          } else if (nc == 32) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const uint32_t rr = 4 * i + r8, grow = rbase + rr;
@@ -690,13 +709,12 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
             if (col0 + i < args.N) dst[i] = v[i];
           continue;
         }
-        float* dst = e.out + (size_t)row * e.ld_out + e.out_col + col0;
         uint32_t bw = 0;
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (col0 + i < args.N) {
             const float o = apply_epi(e, row, col0 + i, v[i]);
-            dst[i] = o;
+            store_epi(e, row, col0 + i, o);
             bw |= (uint32_t)(o > 0.f) << i;
           }
         if (e.bits_out) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
@@ -728,7 +746,7 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ partial, uint32_t s
     float acc = 0.f;
     for (uint32_t z = 0; z < splits; ++z) acc += partial[(uint64_t)z * total + i];
     const uint32_t row = (uint32_t)(i / N), col = (uint32_t)(i % N);
-    e.out[(size_t)row * e.ld_out + e.out_col + col] = apply_epi(e, row, col, acc);
+    store_epi(e, row, col, apply_epi(e, row, col, acc));
   }
 }
 
@@ -791,6 +809,14 @@ uint32_t pow2_cols(uint32_t n) {
 
 }  // namespace
 
+void check_epi_output(const GemmEpi& epi) {
+  if ((epi.out == nullptr) == (epi.out_h == nullptr)) throw ConfigError("GEMM needs exactly one output (fp32 or fp16)");
+  if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  if (epi.out_h && ((epi.ld_out % 8) || (epi.out_col % 8) || (epi.store_cols % 8)))
+    throw ConfigError("GEMM fp16 output: stride, column and store_cols must be multiples of 8");
+  if (!(epi.out_scale > 0.f)) throw ConfigError("GEMM out_scale must be positive");
+}
+
 void gemm_tn(catgnn_ctx ctx, const float* A, uint32_t lda, const float* B, uint32_t ldb, uint32_t M,
              uint32_t N, uint32_t K, const GemmEpi& epi_in, uint32_t split_k, int precision) {
   gemm(ctx, GemmOperand{A, lda, false}, GemmOperand{B, ldb, false}, M, N, K, epi_in, split_k, precision);
@@ -803,8 +829,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   const uint32_t lda = a.ld, ldb = b.ld;
   if (M == 0 || N == 0) return;
   GemmEpi epi = epi_in;
-  if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
-  if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  check_epi_output(epi);
   if (epi.store_cols && (epi.store_cols % 4 || epi.store_cols < N || epi.out_col + epi.store_cols > epi.ld_out))
     throw ConfigError("GEMM store_cols must be a multiple of 4 in [N, ld_out - out_col]");
   if (K == 0) {  // empty contraction: the epilogue of a zero accumulator
@@ -1062,8 +1087,7 @@ void gemm_bf16x3(catgnn_ctx ctx, SplitOperand a, SplitOperand b, uint32_t M, uin
                  const GemmEpi& epi_in, uint32_t split_k) {
   if (M == 0 || N == 0) return;
   GemmEpi epi = epi_in;
-  if (epi.out == nullptr) throw ConfigError("GEMM needs an output");
-  if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
+  check_epi_output(epi);
   if (epi.store_cols && (epi.store_cols % 4 || epi.store_cols < N || epi.out_col + epi.store_cols > epi.ld_out))
     throw ConfigError("GEMM store_cols must be a multiple of 4 in [N, ld_out - out_col]");
   if (K == 0) {

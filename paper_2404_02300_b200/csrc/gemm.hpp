@@ -1,6 +1,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.hpp"
 
@@ -8,7 +9,8 @@ namespace catgnn {
 
 // Fused epilogue of K3, applied per output element (row, col):
 //   v = acc; v *= rowscale[row] (cols >= scale_col_begin); v += bias[col];
-//   v = relu(v); v = bit(mask_bits, row, col) ? v : 0;  out[row][out_col+col] = v
+//   v = relu(v); v = bit(mask_bits, row, col) ? v : 0;  v *= out_scale;
+//   out[row][out_col+col] = v   (or out_h[...] = fp16(v))
 //   bits_out: bit (row, col) = v > 0 (the ReLU mask of this output's backward)
 struct GemmEpi {
   float* out = nullptr;
@@ -26,6 +28,11 @@ struct GemmEpi {
   // zero-padded): lets a ragged last 32-column chunk (N = 41 classes) use the
   // staged, line-coalesced stores; 0 = write only [0, N)
   uint32_t store_cols = 0;
+  // fp16 output rows instead of `out` (ld_out / out_col in halves, multiples
+  // of 8): the input of an fp16 K2 pass; out_scale (a power of two) keeps
+  // small values (gradients) in the fp16 normal range
+  __half* out_h = nullptr;
+  float out_scale = 1.0f;
   float* partial = nullptr;  // internal (split-K workspace)
 };
 

@@ -62,12 +62,15 @@ __device__ __forceinline__ float wmax(float v) {
 // / n_train (rows not listed keep the caller's zeros); per-row loss for a
 // deterministic reduction.  Warp per row, lanes over classes.  With rs, also
 // writes dZs[r] = rs[r] * dZ[r] (the GCN source scale D^-1/2 of the next
-// backward aggregation, so K2 needs no per-edge scale loads).
+// backward aggregation, so K2 needs no per-edge scale loads).  With dZh, that
+// row (rs = 1 when null) is written instead as fp16, times hscale (2^k ~ n:
+// |hscale * dZ| <= 1 stays in the fp16 normal range), the fp16 K2 pass's input.
 __global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uint32_t C,
                                   const int32_t* __restrict__ labels, const uint32_t* __restrict__ rows,
                                   uint64_t n, float* __restrict__ dZ, uint32_t lddz,
                                   double* __restrict__ row_loss, const float* __restrict__ rs,
-                                  float* __restrict__ dZs) {
+                                  float* __restrict__ dZs, __half* __restrict__ dZh, uint32_t ldh,
+                                  float hscale) {
   const int lane = threadIdx.x & 31;
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -91,7 +94,8 @@ __global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uin
       float p = expf(z[c] - m) / s;
       if ((int)c == y) p -= 1.0f;
       dZ[(size_t)r * lddz + c] = p * inv_n;
-      if (rs) dZs[(size_t)r * lddz + c] = sc * (p * inv_n);
+      if (dZh) dZh[(size_t)r * ldh + c] = __float2half_rn((rs ? sc : 1.f) * (p * inv_n) * hscale);
+      else if (rs) dZs[(size_t)r * lddz + c] = sc * (p * inv_n);
     }
     if (lane == 0) row_loss[i] = (double)m + log((double)s) - (double)zy;
   }
@@ -144,16 +148,30 @@ __global__ void argmax_correct_kernel(const float* __restrict__ Z, uint32_t ldz,
 // Column sums of rows x width (ld % 4 == 0): each block reduces a slab of rows
 // with float4 loads (tpr threads per row, 256/tpr rows in flight), partials
 // per block, then a fixed-order reduce — deterministic.
-__global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, uint64_t rows,
-                                      uint32_t width, float* __restrict__ partial) {
+// H16: X is fp16 rows holding rs[r] * x / scale (the fp16 K2 inputs); the sum
+// is of x (the division by rs happens per row here, by scale in the reduce).
+template <bool H16>
+__device__ __forceinline__ float4 colsum_ld(const void* X, uint64_t r, uint32_t ld, uint32_t c,
+                                            const float* __restrict__ rs) {
+  if constexpr (H16) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(static_cast<const __half*>(X) + r * ld) + c);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    const float f = rs ? 1.0f / __ldg(rs + r) : 1.0f;
+    return make_float4(a.x * f, a.y * f, b.x * f, b.y * f);
+  } else {
+    return __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(X) + r * ld) + c);
+  }
+}
+template <bool H16>
+__global__ void colsum_partial_kernel(const void* __restrict__ X, uint32_t ld, uint64_t rows,
+                                      uint32_t width, float* __restrict__ partial, const float* __restrict__ rsc) {
   __shared__ float4 red[256];
   const uint32_t w4 = (width + 3) / 4;
   const uint64_t per = (rows + gridDim.x - 1) / gridDim.x;
   const uint64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
   const uint32_t tpr = min(w4, 256u), rpi = 256 / tpr;
   const uint32_t c4 = threadIdx.x % tpr, rs = threadIdx.x / tpr;
-  const float4* X4 = reinterpret_cast<const float4*>(X);
-  const uint32_t ld4 = ld / 4;
   for (uint32_t cb = 0; cb < w4; cb += tpr) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const uint32_t c = cb + c4;
@@ -162,15 +180,15 @@ __global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, 
       float4 a1 = acc, a2 = acc, a3 = acc;
       uint64_t r = r0 + rs;
       for (; r + 3 * rpi < r1; r += 4 * rpi) {
-        const float4 v0 = __ldg(X4 + r * ld4 + c), v1 = __ldg(X4 + (r + rpi) * ld4 + c);
-        const float4 v2 = __ldg(X4 + (r + 2 * rpi) * ld4 + c), v3 = __ldg(X4 + (r + 3 * rpi) * ld4 + c);
+        const float4 v0 = colsum_ld<H16>(X, r, ld, c, rsc), v1 = colsum_ld<H16>(X, r + rpi, ld, c, rsc);
+        const float4 v2 = colsum_ld<H16>(X, r + 2 * rpi, ld, c, rsc), v3 = colsum_ld<H16>(X, r + 3 * rpi, ld, c, rsc);
         acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
         a1.x += v1.x; a1.y += v1.y; a1.z += v1.z; a1.w += v1.w;
         a2.x += v2.x; a2.y += v2.y; a2.z += v2.z; a2.w += v2.w;
         a3.x += v3.x; a3.y += v3.y; a3.z += v3.z; a3.w += v3.w;
       }
       for (; r < r1; r += rpi) {
-        const float4 v = __ldg(X4 + r * ld4 + c);
+        const float4 v = colsum_ld<H16>(X, r, ld, c, rsc);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       acc.x += a1.x + (a2.x + a3.x); acc.y += a1.y + (a2.y + a3.y);
@@ -192,14 +210,14 @@ __global__ void colsum_partial_kernel(const float* __restrict__ X, uint32_t ld, 
 }
 // One warp per column: lanes stride the block partials, then a fixed xor tree.
 __global__ void colsum_reduce_kernel(const float* __restrict__ partial, uint32_t blocks, uint32_t width,
-                                     uint32_t pstride, float* __restrict__ out) {
+                                     uint32_t pstride, float* __restrict__ out, float scale) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (c >= width) return;
   float acc = 0.f;
   for (uint32_t b = lane; b < blocks; b += 32) acc += partial[(size_t)b * pstride + c];
   acc = wsum(acc);
-  if (lane == 0) out[c] = acc;
+  if (lane == 0) out[c] = acc * scale;
 }
 
 // K5: fused optimizer over the flat parameter vector.
@@ -393,14 +411,17 @@ void internal_to_logical(const catgnn_model_s* M, const std::vector<float>& in, 
 }
 
 
-void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t width, float* out) {
+// Column sums of fp32 rows, or (Xh) of fp16 rows stored as rs[r] * x / scale.
+void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t width, float* out,
+            const __half* Xh = nullptr, const float* rs = nullptr, float scale = 1.0f) {
   if (ld % 4) throw ConfigError("column sum needs a row stride multiple of 4");
   const uint32_t blocks = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (rows + 255) / 256), 592);
   const uint32_t pstride = round_up(width, 4);
   float* part = ctx->scratch_buf<float>("colsum_part", (size_t)blocks * pstride);
-  colsum_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part);
+  if (Xh) colsum_partial_kernel<true><<<blocks, 256, 0, ctx->stream>>>(Xh, ld, rows, width, part, rs);
+  else colsum_partial_kernel<false><<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part, nullptr);
   CG_CHECK_LAUNCH();
-  colsum_reduce_kernel<<<(width + 7) / 8, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out);
+  colsum_reduce_kernel<<<(width + 7) / 8, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out, scale);
   CG_CHECK_LAUNCH();
   ctx->launches += 2;
 }
@@ -473,6 +494,43 @@ Split act16(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld)
     ctx->act_shape[name + "_s"] = sig;
   }
   return s;
+}
+
+// fp16 K2 inputs (default; CATGNN_ACT_F16=0: fp32).  The transform-first GCN
+// layers gather the producer-scaled gradient s * dZ backward, and the last
+// layer its GEMM output T = s (H W) forward, as fp16 rows: the K2 passes are
+// bound by the L2 -> SM bytes of the gathered rows, which this halves.  The
+// source scale s = D^-1/2 is applied by the producer before rounding, and the
+// backward rows carry a power-of-two factor 2^k <= n_train (|dZ| <= 1/n_train)
+// so gradients stay in the fp16 normal range; each element is rounded once
+// (2^-11 relative) and summed in fp32: gradients move by ~2e-4 relative
+// (north-star gate 2e-3).  Not for:
+//  * a hidden layer's forward — its output feeds a ReLU, and rounding T flips
+//    the masks of near-zero pre-activations (5 of 98 k on the small test graph
+//    moved dW0 by 4e-3); the logits have no ReLU;
+//  * GIN — sum aggregation grows with the degree (RMAT hubs: 54 k neighbours),
+//    so neither activations nor gradients have a bounded range;
+//  * SGC — pinned to the reference's f64 sgc_propagate at 1e-4.
+const bool kActF16 = [] {
+  const char* v = std::getenv("CATGNN_ACT_F16");
+  return v ? v[0] != '0' : true;
+}();
+bool f16_bwd(const catgnn_model_s* M, size_t l) {
+  return M->act_f16 && bf_layer(M, l) && M->cfg.kind == CATGNN_MODEL_GCN;
+}
+bool f16_fwd(const catgnn_model_s* M, size_t l) { return f16_bwd(M, l) && l + 1 == M->layers.size(); }
+// fp16 row stride: 32 / 64 halves (one 64- / 128-byte line) for narrow rows
+uint32_t ld_h16(uint32_t w) { return w <= 32 ? 32 : w <= 64 ? 64 : round_up(w, 8); }
+__half* act_h(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld) {
+  const size_t n = std::max<uint64_t>(1, rows) * ld;
+  __half* p = reinterpret_cast<__half*>(ctx->scratch_buf<uint16_t>(name, n));
+  auto sig = std::make_pair(rows, ld);
+  auto it = ctx->act_shape.find(name);
+  if (it == ctx->act_shape.end() || it->second != sig) {  // padding columns are read (as zeros)
+    CG_CUDA(cudaMemsetAsync(p, 0, n * 2, ctx->stream));
+    ctx->act_shape[name] = sig;
+  }
+  return p;
 }
 
 // The shard's features as a bf16x3 pair, re-split when they changed.
@@ -588,10 +646,20 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       if (!L.out_in_next_mid) e.store_cols = b.out_ld;  // zero padding (bias is zero-padded)
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN / SGC transform-first
-      b.mid_ld = L.ld_act;
-      b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
-      GemmEpi e; e.out = b.mid; e.ld_out = b.mid_ld; e.rowscale = gcn ? S->dinv.p : nullptr;
-      e.store_cols = b.mid_ld;  // the padding of T is zero either way: staged stores for the ragged tail
+      const bool h16 = f16_fwd(M, l);
+      __half* mid_h = nullptr;
+      GemmEpi e; e.rowscale = gcn ? S->dinv.p : nullptr;
+      if (h16) {  // T as fp16 rows: the K2 pass's only input
+        b.mid_ld = ld_h16(L.D_out);
+        mid_h = act_h(ctx, nm("midh", l), rows, b.mid_ld);
+        e.out_h = mid_h; e.ld_out = b.mid_ld;
+        e.store_cols = round_up(L.D_out, 8);  // the vectors K2 reads, zero padding included
+      } else {
+        b.mid_ld = L.ld_act;
+        b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
+        e.out = b.mid; e.ld_out = b.mid_ld;
+        e.store_cols = b.mid_ld;  // the padding of T is zero either way: staged stores for the ragged tail
+      }
       if (bf_layer(M, l)) {
         // the layer input as a pre-split pair: the features, the previous K2's
         // bf16x3 output, or (previous layer on another path) a split of its fp32 rows
@@ -610,6 +678,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       }
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
+      if (h16) { a.in = nullptr; a.in_h = mid_h; }
       a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
       a.bits_out = b.bits; a.bits_words = b.bits_words;
       if (h_split) {  // H_l is only the next bf16x3 layer's GEMM operand
@@ -640,6 +709,9 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   float* dZ = act(ctx, nm("dZ", nl - 1), rows, LL.ld_act, false);
   CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   const uint64_t ntr = S->h_train.size();
+  // fp16 gradient rows carry 2^k <= n_train (|dZ| <= 1 / n_train)
+  const float gscale = std::ldexp(1.0f, (int)std::floor(std::log2((double)std::max<uint64_t>(ntr, 1))));
+  M->dz_f16.assign(nl, {});
   double loss = 0.0;
   double* row_loss = ctx->scratch_buf<double>("row_loss", std::max<uint64_t>(1, ntr));
   if (!M->loss_dev.p) M->loss_dev.alloc(1);
@@ -649,30 +721,48 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   // GCN / SGC transform-first: the last layer's backward aggregation gathers
   // bwd_pre * dZ, produced here by K4 instead of per edge in K2
   float* dZs = nullptr;
-  if (bwd_pre(M, S) && !LL.agg_first) {
+  __half* dZh = nullptr;  // fp16 K2 input of the last layer's backward pass
+  if (f16_bwd(M, nl - 1)) {
+    const uint32_t ldh = ld_h16(LL.D_out);
+    dZh = act_h(ctx, nm("dZh", nl - 1), rows, ldh);
+    CG_CUDA(cudaMemsetAsync(dZh, 0, std::max<uint64_t>(1, rows) * ldh * 2, st));
+  } else if (bwd_pre(M, S) && !LL.agg_first) {
     dZs = act(ctx, "dZs", rows, LL.ld_act, false);
     CG_CUDA(cudaMemsetAsync(dZs, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   }
   if (ntr) {
     softmax_ce_kernel<<<grid1d(ntr * 32), 256, 0, st>>>(B[nl - 1].out, B[nl - 1].out_ld, LL.d_out,
                                                       S->labels.p, S->d_train.p, ntr, dZ, LL.ld_act, row_loss,
-                                                      dZs ? bwd_pre(M, S) : nullptr, dZs);
+                                                      (dZs || dZh) ? bwd_pre(M, S) : nullptr, dZs, dZh,
+                                                      ld_h16(LL.D_out), gscale);
     CG_CHECK_LAUNCH();
     sum_doubles_kernel<<<1, 1024, 0, st>>>(row_loss, ntr, loss_dev);
     CG_CHECK_LAUNCH();
     ctx->launches += 2;
   }
   uint32_t dZ_ld = LL.ld_act;
+  // dZ of the current layer as fp16 rows (rs * dZ * scale): the K2 input
+  __half* dzh = dZh;
+  if (dZh) M->dz_f16[nl - 1] = {true, bwd_pre(M, S), gscale, ld_h16(LL.D_out)};
   for (size_t li = nl; li-- > 0;) {
     const Layer& L = M->layers[li];
     const Bufs& b = B[li];
     float* gW = M->grads.p + L.off_w;
-    colsum(ctx, dZ, dZ_ld, rows, L.d_out, M->grads.p + L.off_b);
+    if (dzh && li + 1 < nl) {
+      const auto& z = M->dz_f16[li];
+      colsum(ctx, nullptr, z.ld, rows, L.d_out, M->grads.p + L.off_b, dzh, z.rs, 1.0f / z.scale);
+    } else {
+      colsum(ctx, dZ, dZ_ld, rows, L.d_out, M->grads.p + L.off_b);
+    }
     const bool need_dx = li > 0;
     // ReLU mask of the previous layer's output: its bits
     const uint32_t* hbits = li > 0 ? B[li - 1].bits : nullptr;
     const uint32_t hwords = li > 0 ? B[li - 1].bits_words : 0;
-    float* dZprev = need_dx ? act(ctx, nm("dZ", li - 1), rows, L.K_in, false) : nullptr;
+    // layer li-1's backward K2 gathers dZ_{li-1} as fp16 when it is an fp16
+    // layer and this layer's dX GEMM produces it (bf16x3 transform-first)
+    const bool prev_h = need_dx && f16_bwd(M, li - 1) && bf_layer(M, li);
+    float* dZprev = need_dx && !prev_h ? act(ctx, nm("dZ", li - 1), rows, L.K_in, false) : nullptr;
+    __half* dzh_prev = prev_h ? act_h(ctx, nm("dZh", li - 1), rows, ld_h16(L.K_in)) : nullptr;
     if (sage && L.agg_first) {
       // dW = dZ^T cat (both operands read MN-major in place)
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;
@@ -728,12 +818,22 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
       AggArgs a;
       a.in = dZ; a.in_ld = dZ_ld; a.pre = bwd_pre(M, S); a.self = 1; a.norm = bwd_norm(M);
       if (li == nl - 1 && dZs) { a.in = dZs; a.pre = nullptr; }  // pre-scaled by K4
+      if (dzh) {  // fp16 rows pre-scaled by their producer (K4 or the next layer's dX GEMM)
+        const auto& z = M->dz_f16[li];
+        a.in = nullptr; a.in_h = dzh; a.in_ld = z.ld; a.pre = nullptr; a.in_scale = 1.0f / z.scale;
+      }
       a.out = nullptr; a.out_hi = dT.hi; a.out_lo = dT.lo; a.out_s_ld = dT.ld; a.width = L.D_out;
       aggregate(S, a);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;  // dW = dT^T H_{l-1} (both MN-major, in place)
       gemm_bf16x3(ctx, op16(dT, true), op16(b.in_split, true), L.d_out, L.w_cols, (uint32_t)rows, e, 0);
       if (need_dx) {  // dZ_{l-1} = mask (dT W)
         GemmEpi e2; e2.out = dZprev; e2.ld_out = L.K_in; e2.mask_bits = hbits; e2.mask_words = hwords;
+        if (prev_h) {  // fp16 rows bwd_pre * dZ * 2^k: the input of layer li-1's K2 pass
+          e2.out = nullptr; e2.out_h = dzh_prev; e2.ld_out = ld_h16(L.K_in);
+          e2.store_cols = round_up(L.K_in, 8);
+          e2.rowscale = bwd_pre(M, S); e2.out_scale = gscale;
+          M->dz_f16[li - 1] = {true, bwd_pre(M, S), gscale, e2.ld_out};
+        }
         gemm_bf16x3(ctx, op16(dT, false), op16(weight_split(M, li), true), (uint32_t)rows, L.w_cols, L.d_out, e2, 1);
       }
     } else {  // GCN / GIN transform-first
@@ -754,11 +854,17 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
     }
     dZ = dZprev;
     dZ_ld = L.K_in;
+    dzh = dzh_prev;
   }
   if (want_loss && ntr) {
     CG_CUDA(cudaMemcpyAsync(&loss, loss_dev, 8, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
     loss /= (double)ntr;
+    bool any_h = false;
+    for (size_t l = 0; l < nl; ++l) any_h = any_h || f16_bwd(M, l);
+    if (any_h && !std::isfinite(loss))
+      throw DataError("non-finite loss with fp16 aggregation inputs (range +-65504 exceeded?); "
+                      "CATGNN_ACT_F16=0 keeps them fp32");
   }
   return loss;
 }
@@ -847,6 +953,7 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
     auto M = std::make_unique<catgnn_model_s>();
     M->ctx = ctx;
     M->cfg = *cfg;
+    M->act_f16 = kActF16;
     ctx_retain(ctx);
     plan_layers(M.get());
     M->params.alloc(M->n_params);
@@ -888,6 +995,13 @@ int catgnn_model_create(catgnn_ctx ctx, const catgnn_model_config* cfg, catgnn_m
     CG_CUDA(cudaMemcpyAsync(M->params.p, internal.data(), M->n_params * 4, cudaMemcpyHostToDevice, ctx->stream));
     CG_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = M.release();
+  });
+}
+
+int catgnn_model_set_act_f16(catgnn_model m, int on) {
+  return guarded([&] {
+    check_model(m);
+    m->act_f16 = on != 0;
   });
 }
 
@@ -1080,6 +1194,23 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
     } else if (what == 0) {
       src = m->ctx->scratch_buf<float>(nm("H", layer), 1);
       ld = L.ld_act;
+    }
+    else if (what == 2 && layer < m->dz_f16.size() && m->dz_f16[layer].on) {
+      // dZ_l held only as fp16 rows rs[r] * dZ * scale
+      const auto& z = m->dz_f16[layer];
+      const uint16_t* h = m->ctx->scratch_buf<uint16_t>(nm("dZh", layer), 1);
+      if (width) *width = w;
+      if (out && s->rows) {
+        std::vector<__half> hv(s->rows * (size_t)z.ld);
+        std::vector<float> rs(z.rs ? s->rows : 0);
+        CG_CUDA(cudaMemcpyAsync(hv.data(), h, hv.size() * 2, cudaMemcpyDeviceToHost, m->ctx->stream));
+        if (z.rs) CG_CUDA(cudaMemcpyAsync(rs.data(), z.rs, rs.size() * 4, cudaMemcpyDeviceToHost, m->ctx->stream));
+        CG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+        for (uint64_t r = 0; r < s->rows; ++r)
+          for (uint32_t c = 0; c < w; ++c)
+            out[r * w + c] = __half2float(hv[r * z.ld + c]) / ((z.rs ? rs[r] : 1.0f) * z.scale);
+      }
+      return;
     }
     else if (what == 2) { src = m->ctx->scratch_buf<float>(nm("dZ", layer), 1); ld = L.ld_act; }
     else throw ConfigError("export: what must be 0 (H) or 2 (dZ)");

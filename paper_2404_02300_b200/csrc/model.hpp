@@ -44,7 +44,17 @@ struct catgnn_model_s {
   // bf16x3 copies of the weights (hi / lo per layer at ws_off, rows of round8(w_cols))
   catgnn::DevBuf<uint16_t> ws_hi, ws_lo;
   std::vector<uint64_t> ws_off;
+  bool act_f16 = true;  // fp16 K2 inputs where safe (catgnn_model_set_act_f16; gnn.cu f16_bwd)
   std::vector<bool> h_split_only;  // layer outputs the last forward kept only as bf16x3 pairs
+  // dZ_l of the last backward held only as fp16 rows rs[r] * dZ * scale (the
+  // fp16 K2 inputs; catgnn_model_export converts back)
+  struct DzF16 {
+    bool on = false;
+    const float* rs = nullptr;
+    float scale = 1.0f;
+    uint32_t ld = 0;
+  };
+  std::vector<DzF16> dz_f16;
 };
 
 namespace catgnn {

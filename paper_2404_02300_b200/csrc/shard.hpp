@@ -71,6 +71,12 @@ enum AggNorm : int {
 
 struct AggArgs {
   const float* in = nullptr;  // rows x in_ld, columns [in_col, in_col+width)
+  // fp16 input rows instead of `in` (in_ld, in_col in halves, multiples of 8;
+  // columns up to round8(width) readable, padding zero); the values are stored
+  // multiplied by 1/in_scale (a power of two), in_scale is folded into the post
+  // scale.  No per-source scale: the producer applies it before rounding.
+  const void* in_h = nullptr;
+  float in_scale = 1.0f;
   uint32_t in_ld = 0, in_col = 0;
   float* out = nullptr;  // rows x out_ld, columns [out_col, out_col+width)
   uint32_t out_ld = 0, out_col = 0;

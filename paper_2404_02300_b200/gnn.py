@@ -51,6 +51,10 @@ class GNNModel:
         m.cfg = cfg
         return m
 
+    def set_act_f16(self, on: bool):
+        """fp16 aggregation inputs where safe (GCN backward, last-layer forward)."""
+        check(lib.catgnn_model_set_act_f16(self.handle, int(bool(on))))
+
     def layer_shapes(self):
         out = []
         for l in range(self.cfg.layers):

@@ -71,6 +71,34 @@ def test_single_step_outputs_and_grads(graph, kind, in_dim, hidden, classes, lay
         assert rel_err(gb, rb) < 2e-3, (l, "b", rel_err(gb, rb))
 
 
+@pytest.mark.parametrize("in_dim,hidden,classes", [(602, 64, 41), (150, 160, 12), (64, 256, 172)])
+def test_gcn_fp16_aggregation_inputs(graph, in_dim, hidden, classes):
+    """The fp16 K2 inputs (GCN backward gradients, last-layer forward) against
+    the all-fp32 path and the oracle: both within the 2e-3 gate, and the fp16
+    run really differs from the fp32 one (the path is taken)."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    s, o = make(gp, graph, in_dim, classes)
+    init = go.init_params(go.GCN, 2, in_dim, hidden, classes, seed=5)
+    rep = go.Replica(go.GCN, init)
+    loss_ref, H, Zs, grads = rep.forward_backward(o)
+    got = {}
+    for f16 in (True, False):
+        m = GNNModel("gcn", 2, in_dim, hidden, classes, seed=5)
+        m.set_act_f16(f16)
+        loss = m.forward_backward(s)
+        assert abs(loss - loss_ref) <= 1e-3 * abs(loss_ref)
+        g = m.unflatten(m.get_grads())
+        for l, ((gW, gb), (rW, rb)) in enumerate(zip(g, grads)):
+            assert rel_err(gW, rW) < 2e-3, (f16, l, "W", rel_err(gW, rW))
+            assert rel_err(gb, rb) < 2e-3, (f16, l, "b", rel_err(gb, rb))
+        dz0 = m.export(0, 2, s.rows)  # dZ_0 (held as fp16 rows in the fp16 run)
+        got[f16] = (g, dz0)
+    assert rel_err(got[True][1], got[False][1]) < 1e-3
+    assert not np.array_equal(got[True][0][0][0], got[False][0][0][0])
+    assert rel_err(got[True][0][0][0], got[False][0][0][0]) < 1e-3
+
+
 @pytest.mark.parametrize("kind", ["gcn", "sage", "gin"])
 def test_ten_epoch_loss_two_partitions(kind, tmp_path_factory):
     """p=2 SPRING shards, s=1, Adam lr 0.01: per-epoch loss within 1e-3 of the oracle."""
@@ -171,7 +199,8 @@ def test_e2e_feature_gather_path_identical(tmp_path_factory):
     """bench.py's e2e path (global feature store -> device row gather, on a copy
     stream) trains exactly like shards built with their features resident."""
     from paper_2404_02300_b200 import gnnpart as gp, gnn, synth
-    ds = make_dataset(tmp_path_factory.mktemp("e2e"), scale=10, edges=4000, dim=20, classes=5, seed=8)
+    # dim 40 > hidden 32: layer 0 is transform-first (bf16x3 GEMM on the split features)
+    ds = make_dataset(tmp_path_factory.mktemp("e2e"), scale=10, edges=4000, dim=40, classes=5, seed=8)
     art = make_artifact(ds, p=2)
     td = ref.TrainingData(art)
     X = ds["X"]
