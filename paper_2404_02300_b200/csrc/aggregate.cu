@@ -47,6 +47,7 @@ struct AggKernelArgs {
   const __half* __restrict__ in_h;  // fp16 input rows instead of `in` (in_ld / in_col in halves)
   uint32_t in_ld, in_col;
   float in_scale;                   // folded into the post scale (fp16 inputs stored scaled by 1/in_scale)
+  int zero_row;                     // fp16 inputs: index of an all-zero row (= rows), the target of idle loads
   float* __restrict__ out;
   uint32_t out_ld, out_col;
   uint32_t w4;
@@ -101,9 +102,18 @@ __device__ __forceinline__ void h8_to_f4(const uint4& r, float4& a, float4& b) {
 }
 // One gathered 16-byte vector (CPV = 1: 4 fp32 columns, 2: 8 fp16 columns)
 // into the accumulators a[0, CPV).
+// f32 += f16, one instruction (sm_100 FHADD): exact conversion, IEEE RN add
+__device__ __forceinline__ void fhadd(float& a, uint32_t h2, bool hi) {
+  unsigned short h0, h1;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(h0), "=h"(h1) : "r"(h2));
+  asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(a) : "h"(hi ? h1 : h0));
+}
 template <int CPV, bool PRE>
 __device__ __forceinline__ void acc_raw(float4* a, const uint4& r, float s) {
-  if constexpr (CPV == 1) {
+  if constexpr (CPV == 2 && !PRE) {
+    fhadd(a[0].x, r.x, false); fhadd(a[0].y, r.x, true); fhadd(a[0].z, r.y, false); fhadd(a[0].w, r.y, true);
+    fhadd(a[1].x, r.z, false); fhadd(a[1].y, r.z, true); fhadd(a[1].z, r.w, false); fhadd(a[1].w, r.w, true);
+  } else if constexpr (CPV == 1) {
     const float4 v = make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z), __uint_as_float(r.w));
     if (PRE) fma4(a[0], s, v);
     else add4(a[0], v);
@@ -219,8 +229,11 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
 // an immediate).  fp16 rows (CPV = 2) hold 8 columns per vector.
 template <int CPV>
 __device__ __forceinline__ const char* lane_base(const AggKernelArgs& p, int li) {
-  if constexpr (CPV == 2) return reinterpret_cast<const char*>(p.in_h + p.in_col) + li * 16;
-  else return reinterpret_cast<const char*>(p.in + p.in_col) + li * 16;
+  const char* b = CPV == 2 ? reinterpret_cast<const char*>(p.in_h + p.in_col) + li * 16
+                           : reinterpret_cast<const char*>(p.in + p.in_col) + li * 16;
+  // opaque: each neighbour address is then one IMAD.WIDE (j * row bytes + base)
+  asm volatile("" : "+l"(b));
+  return b;
 }
 template <int CPV>
 __device__ __forceinline__ uint32_t row_bytes(const AggKernelArgs& p) { return p.in_ld * (CPV == 2 ? 2u : 4u); }
@@ -234,7 +247,7 @@ __device__ __forceinline__ uint4 ld_nbr(const char* base, uint32_t ldb, int j, i
 // Sum of pre[j]*in[j] over edges [e0, e1) into acc (reduced across groups).
 // Loads past the end of the range, and by lanes whose columns lie past the
 // row width, are skipped and contribute zeros.
-template <int VPL, int LPN, bool PRE, int CPV>
+template <int VPL, int LPN, bool PRE, int CPV, bool FULLW, bool ZR>
 __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64_t e1,
                                        float4 (&acc)[VPL * CPV], int lane) {
   constexpr int G = 32 / LPN;  // neighbours processed side by side
@@ -244,7 +257,7 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
   const uint32_t ldb = row_bytes<CPV>(p);
   bool colok[VPL];
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) colok[q] = li + LPN * q < (int)n_vec<CPV>(p);
+  for (int q = 0; q < VPL; ++q) colok[q] = FULLW || li + LPN * q < (int)n_vec<CPV>(p);
 #pragma unroll
   for (int k = 0; k < VPL * CPV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t e = e0; e < e1; e += 32) {
@@ -263,8 +276,12 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
         s[u] = PRE ? __shfl_sync(0xffffffffu, mys, kk & 31) : 1.0f;
         ok[u] = kk < n;
 #pragma unroll
-        for (int q = 0; q < VPL; ++q)
-          v[u][q] = (ok[u] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
+        for (int q = 0; q < VPL; ++q) {
+          if constexpr (ZR)  // idle slots load the zero row
+            v[u][q] = colok[q] ? ld_nbr<VPL, LPN>(base, ldb, ok[u] ? j : p.zero_row, q) : make_uint4(0u, 0u, 0u, 0u);
+          else
+            v[u][q] = (ok[u] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
+        }
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u)
@@ -285,7 +302,7 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
 // 32 rows per coalesced load and each row's own input row (self term) is
 // requested together with its first neighbour batch.  Per row the G lane
 // groups split the neighbours, UNROLL batches in flight, xor-shuffle reduce.
-template <int VPL, int LPN, bool PRE, bool BITS, int CPV>
+template <int VPL, int LPN, bool PRE, bool BITS, int CPV, bool FULLW, bool ZR>
 __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, int64_t r1, int lane) {
   constexpr int G = 32 / LPN;
 #ifndef AGG_NARROW_UNROLL
@@ -319,7 +336,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   const uint32_t ldb = row_bytes<CPV>(p);
   bool colok[VPL];
 #pragma unroll
-  for (int q = 0; q < VPL; ++q) colok[q] = li + LPN * q < (int)n_vec<CPV>(p);
+  for (int q = 0; q < VPL; ++q) colok[q] = FULLW || li + LPN * q < (int)n_vec<CPV>(p);
   for (int64_t rb = r0; rb < r1; rb += 32) {
     const int64_t rr = rb + lane;
     const int64_t rpa = rr < r1 ? __ldg(p.row_ptr + rr) : 0;
@@ -372,8 +389,12 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             s[uu] = PRE ? __shfl_sync(0xffffffffu, wins, uu) : 1.f;
             ok[uu] = uu < rem;
 #pragma unroll
-            for (int q = 0; q < VPL; ++q)
-              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
+            for (int q = 0; q < VPL; ++q) {
+              if constexpr (ZR)  // idle slots load the zero row
+                v[uu][q] = colok[q] ? ld_nbr<VPL, LPN>(base, ldb, ok[uu] ? j : p.zero_row, q) : make_uint4(0u, 0u, 0u, 0u);
+              else
+                v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
+            }
           }
         } else {
           // lane groups: two shuffles per neighbour keep the register budget
@@ -394,8 +415,12 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             }
             ok[uu] = ee < e1;
 #pragma unroll
-            for (int q = 0; q < VPL; ++q)
-              v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
+            for (int q = 0; q < VPL; ++q) {
+              if constexpr (ZR)  // idle slots load the zero row
+                v[uu][q] = colok[q] ? ld_nbr<VPL, LPN>(base, ldb, ok[uu] ? j : p.zero_row, q) : make_uint4(0u, 0u, 0u, 0u);
+              else
+                v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
+            }
           }
         }
 #pragma unroll
@@ -414,7 +439,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 
 // Persistent unit loop shared by both aggregation kernels: warps pull work
 // units from the atomic counter (the next one prefetched by lane 0).
-template <int VPL, int LPN, bool PRE, bool BITS, int CPV>
+template <int VPL, int LPN, bool PRE, bool BITS, int CPV, bool FULLW, bool ZR>
 __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
   const int lane = threadIdx.x & 31;
   const int li = lane % LPN;
@@ -427,14 +452,14 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
     if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
     const int4 w = __ldg(p.units + u);
     if (w.z < 0) {
-      light_unit<VPL, LPN, PRE, BITS, CPV>(p, w.x, w.y, lane);
+      light_unit<VPL, LPN, PRE, BITS, CPV, FULLW, ZR>(p, w.x, w.y, lane);
     } else {
       float4 acc[VPL * CPV];
       const int64_t r = w.x;
       const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
       const int64_t e0 = rb + (int64_t)w.y * p.U;
       const int64_t e1 = (re < e0 + (int64_t)p.U) ? re : e0 + (int64_t)p.U;
-      gather<VPL, LPN, PRE, CPV>(p, e0, e1, acc, lane);
+      gather<VPL, LPN, PRE, CPV, FULLW, ZR>(p, e0, e1, acc, lane);
       if (writer) {
         float* dst = p.partials + (size_t)w.z * p.w4 * 4;
 #pragma unroll
@@ -453,9 +478,12 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
 // BITS: the epilogue reads / writes ReLU bit masks (a separate instantiation
 // keeps the plain passes' register budget: the narrow kernel runs at 64).
 // CPV = 2: fp16 input rows.
-template <int VPL, int LPN, bool PRE, int MINB, bool BITS, int CPV>
+// FULLW: the row width fills every lane's vectors (no column predicate).
+// ZR: the input has a zero row at index rows (fp16 inputs always): idle
+// neighbour slots load it instead of being predicated off and zeroed.
+template <int VPL, int LPN, bool PRE, int MINB, bool BITS, int CPV, bool FULLW = false, bool ZR = (CPV == 2)>
 __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
-  unit_loop<VPL, LPN, PRE, BITS, CPV>(p);
+  unit_loop<VPL, LPN, PRE, BITS, CPV, FULLW, ZR>(p);
 }
 
 // One CTA per split row.  Warp w sums the row's chunk partials c = w, w+8,
@@ -538,23 +566,30 @@ AggFn pick_pre(bool pre, bool bits) {
   return pre ? agg_kernel<VPL, LPN, true, MINB, false, 1> : agg_kernel<VPL, LPN, false, MINB, false, 1>;
 }
 // fp16 input rows (the source scale is folded into the producer: no PRE)
-template <int VPL, int LPN>
+template <int VPL, int LPN, bool FULLW = false>
 AggFn pick_h16(bool bits) {
   constexpr int MINB = LPN < 32 ? AGG_NARROW_MINB : AGG_WIDE_MINB;
-  return bits ? agg_kernel<VPL, LPN, false, 3, true, 2> : agg_kernel<VPL, LPN, false, MINB, false, 2>;
+  return bits ? agg_kernel<VPL, LPN, false, 3, true, 2, FULLW> : agg_kernel<VPL, LPN, false, MINB, false, 2, FULLW>;
 }
 
 // Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
 constexpr uint32_t kMaxSlab4 = 256;
 
 
-AggFn pick_kernel(uint32_t w4, bool pre, bool bits, bool h16, int* lpn_out) {
+AggFn pick_kernel(uint32_t w4, bool pre, bool bits, bool h16, bool zr, int* lpn_out) {
+  if (!h16 && zr && w4 == 64) {  // 256 fp32 columns, zero row: no predicates in the gather
+    *lpn_out = 32;
+    if (bits) return pre ? agg_kernel<2, 32, true, 3, true, 1, true, true> : agg_kernel<2, 32, false, 3, true, 1, true, true>;
+    return pre ? agg_kernel<2, 32, true, AGG_WIDE_MINB, false, 1, true, true>
+               : agg_kernel<2, 32, false, AGG_WIDE_MINB, false, 1, true, true>;
+  }
   if (h16) {  // 16-byte vectors of 8 halves: 48-wide class rows = 6 of 8 lanes (4 neighbours per load)
     const uint32_t w8 = (w4 + 1) / 2;
     if (w8 <= 4) { *lpn_out = 4; return pick_h16<1, 4>(bits); }
     if (w8 <= 8) { *lpn_out = 8; return pick_h16<1, 8>(bits); }
     if (w8 <= 16) { *lpn_out = 16; return pick_h16<1, 16>(bits); }
     *lpn_out = 32;
+    if (w8 == 32) return pick_h16<1, 32, true>(bits);  // 256 columns
     switch ((w8 + 31) / 32) {
       case 1: return pick_h16<1, 32>(bits);
       case 2: return pick_h16<2, 32>(bits);
@@ -647,6 +682,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.in = a.in;
     p.in_h = static_cast<const __half*>(a.in_h);
     p.in_scale = a.in_scale;
+    p.zero_row = (int)s->rows;
     p.in_ld = a.in_ld;
     p.in_col = a.in_col + c4 * 4;
     p.out = a.out;
@@ -673,7 +709,8 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     static const int hint = env_int("CATGNN_AGG_HINT", 1);
     p.stream_hint = hint;
     int lpn = 32;
-    AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, a.in_h != nullptr, &lpn);
+    AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, a.in_h != nullptr,
+                           a.in_zero_row && W4 == w4, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
     static const int detail = env_int("CATGNN_TIMING_DETAIL", 0);  // label per shard (rows)
     int t = ctx->begin_timed(0, ctx->timing ? "K2 agg w" + std::to_string(w4 * 4) + (a.in_h ? " f16" : "") +

@@ -521,8 +521,9 @@ bool f16_bwd(const catgnn_model_s* M, size_t l) {
 bool f16_fwd(const catgnn_model_s* M, size_t l) { return f16_bwd(M, l) && l + 1 == M->layers.size(); }
 // fp16 row stride: 32 / 64 halves (one 64- / 128-byte line) for narrow rows
 uint32_t ld_h16(uint32_t w) { return w <= 32 ? 32 : w <= 64 ? 64 : round_up(w, 8); }
+// (rows + 1) x ld: row `rows` stays zero (K2's idle-slot target)
 __half* act_h(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld) {
-  const size_t n = std::max<uint64_t>(1, rows) * ld;
+  const size_t n = (rows + 1) * ld;
   __half* p = reinterpret_cast<__half*>(ctx->scratch_buf<uint16_t>(name, n));
   auto sig = std::make_pair(rows, ld);
   auto it = ctx->act_shape.find(name);
@@ -656,7 +657,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
         e.store_cols = round_up(L.D_out, 8);  // the vectors K2 reads, zero padding included
       } else {
         b.mid_ld = L.ld_act;
-        b.mid = act(ctx, nm("mid", l), rows, b.mid_ld, fresh);
+        b.mid = act(ctx, nm("mid", l), rows + 1, b.mid_ld, fresh);  // + zero row (K2's idle-slot target)
         e.out = b.mid; e.ld_out = b.mid_ld;
         e.store_cols = b.mid_ld;  // the padding of T is zero either way: staged stores for the ragged tail
       }
@@ -679,6 +680,7 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
       if (h16) { a.in = nullptr; a.in_h = mid_h; }
+      else a.in_zero_row = true;
       a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
       a.bits_out = b.bits; a.bits_words = b.bits_words;
       if (h_split) {  // H_l is only the next bf16x3 layer's GEMM operand

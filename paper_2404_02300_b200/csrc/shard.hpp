@@ -75,8 +75,11 @@ struct AggArgs {
   // columns up to round8(width) readable, padding zero); the values are stored
   // multiplied by 1/in_scale (a power of two), in_scale is folded into the post
   // scale.  No per-source scale: the producer applies it before rounding.
+  // Row `rows` must exist and be zero (idle gather slots load it instead of
+  // being predicated off).
   const void* in_h = nullptr;
   float in_scale = 1.0f;
+  bool in_zero_row = false;  // fp32 input: row `rows` exists and is zero (fp16: always required)
   uint32_t in_ld = 0, in_col = 0;
   float* out = nullptr;  // rows x out_ld, columns [out_col, out_col+width)
   uint32_t out_ld = 0, out_col = 0;
