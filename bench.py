@@ -139,9 +139,11 @@ def act_width(d):
     return (d + 15) // 16 * 16 if d < 128 else (d + 3) // 4 * 4
 
 
-def agg_bytes(nnz, rows, width, self_term):
-    """nnz*(4 + 4d) + N*(4d*(1+self) + 8)."""
-    return nnz * (4 + 4 * width) + rows * (4 * width * (1 + self_term) + 8)
+def agg_bytes(nnz, rows, width, self_term, eb=4):
+    """nnz*(4 + 4d) + N*(4d*(1+self) + 8), with the gathered
+    input rows at eb bytes per element (2: fp16 passes): nnz*(4 + eb*d) +
+    N*(eb*d*self + 4d + 8)."""
+    return nnz * (4 + eb * width) + rows * (eb * width * self_term + 4 * width + 8)
 
 
 def load_ncu_traffic(w):
@@ -167,9 +169,10 @@ def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step
       else "l2" when the effective rate exceeds the HBM peak (the gathers are
       served from L2: the ceiling is the measured L2 read rate), else "hbm"."""
     self_term = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
-    widths = w.passes()
-    algo = sum(agg_bytes(nz, rw, wd, self_term) for nz, rw in zip(part_nnz, part_rows) for wd in widths)
-    comp = sum(2 * 4 * wd * rw + 4 * nz + 8 * (rw + 1) for nz, rw in zip(part_nnz, part_rows) for wd in widths)
+    widths = list(zip(w.passes(), w.pass_elem_bytes()))
+    algo = sum(agg_bytes(nz, rw, wd, self_term, eb) for nz, rw in zip(part_nnz, part_rows) for wd, eb in widths)
+    comp = sum((eb + 4) * wd * rw + 4 * nz + 8 * (rw + 1)
+               for nz, rw in zip(part_nnz, part_rows) for wd, eb in widths)
     t = agg_ms_step / 1e3
     eff = algo / t / 1e9 if t > 0 else None
     ncu = load_ncu_traffic(w)

@@ -114,52 +114,143 @@ uint32_t env_unit_cost() {
   return 512;
 }
 
-// Aggregation work plan.  Light units pack consecutive rows until their cost
-// (deg + 2 per row) reaches U; a row with deg > U is split into ceil(deg/U)
-// chunk units whose partial sums a fix-up pass combines in chunk order, so the
-// result is deterministic run to run.
-void build_plan(catgnn_shard_s* s, const std::vector<int64_t>& rp) {
+// Aggregation work plan, built on the device.  A row with deg > U is split
+// into ceil(deg/U) chunk units whose partial sums a fix-up pass combines in
+// chunk order; the other (light) rows are packed into units of consecutive
+// rows by their cost deg + row_cost: with P_r the exclusive prefix of those
+// costs, a light row starts a unit when floor(P_r / U) differs from its light
+// predecessor's or a heavy row lies in between, so units carry ~U cost each.
+// Units are listed in row order (the persistent K2 grid pulls them in that
+// order).  A light row's sum never depends on where its unit starts or ends
+// (each row is one warp's edge walk from its own first edge), and chunking is
+// fixed by U, so the plan changes no result bit.
+//
+// plan_rows_kernel: per row, the units it emits (1 for a unit start, nch for a
+// heavy row, else 0), its heavy flag and its chunk count.
+__global__ void plan_rows_kernel(const int64_t* __restrict__ row_ptr, uint64_t rows, uint32_t U,
+                                 uint64_t row_cost, uint64_t* __restrict__ cost, uint32_t* __restrict__ nch) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t deg = (uint64_t)(row_ptr[r + 1] - row_ptr[r]);
+    const bool heavy = deg > U;
+    cost[r] = heavy ? 0 : deg + row_cost;
+    nch[r] = heavy ? (uint32_t)((deg + U - 1) / U) : 0;
+  }
+}
+// emit[r]: units row r opens (needs the exclusive cost prefix P)
+__global__ void plan_emit_kernel(const uint64_t* __restrict__ P, const uint32_t* __restrict__ nch, uint64_t rows,
+                                 uint32_t U, uint32_t* __restrict__ emit, uint32_t* __restrict__ is_heavy) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = nch[r];
+    is_heavy[r] = h ? 1u : 0u;
+    uint32_t e = h;
+    if (!h) {  // light: a unit start after a heavy row, at row 0, or at a new cost bucket
+      const bool start = r == 0 || nch[r - 1] != 0 || (P[r] / U) != (P[r - 1] / U);
+      e = start ? 1u : 0u;
+    }
+    emit[r] = e;
+  }
+}
+// scatter: light unit starts (end filled by plan_ends_kernel), chunk units and
+// the heavy table
+__global__ void plan_scatter_kernel(const uint32_t* __restrict__ nch, const uint32_t* __restrict__ emit,
+                                    const uint64_t* __restrict__ upos, const uint64_t* __restrict__ hpos,
+                                    const uint64_t* __restrict__ cpos, uint64_t rows, int4* __restrict__ units,
+                                    int4* __restrict__ heavy) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = nch[r];
+    if (h) {
+      const uint64_t c0 = cpos[r];
+      heavy[hpos[r]] = make_int4((int)r, (int)c0, (int)h, 0);
+      for (uint32_t c = 0; c < h; ++c) units[upos[r] + c] = make_int4((int)r, (int)c, (int)(c0 + c), 0);
+    } else if (emit[r]) {
+      units[upos[r]] = make_int4((int)r, -1, -1, 0);
+    }
+  }
+}
+// a light unit ends where the next unit (light start or heavy row) begins
+__global__ void plan_ends_kernel(int4* __restrict__ units, uint64_t n_units, uint64_t rows) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_units;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    int4 u = units[i];
+    if (u.z >= 0) continue;
+    u.y = i + 1 < n_units ? units[i + 1].x : (int)rows;
+    units[i] = u;
+  }
+}
+
+template <typename InIt, typename Out>
+void exclusive_scan(catgnn_ctx ctx, InIt in, Out* out, uint64_t n) {
+  size_t tmp_bytes = 0;
+  CG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, in, out, (int64_t)n, ctx->stream));
+  void* tmp = ctx->scratch_buf<unsigned char>("k1_cub", tmp_bytes);
+  CG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, (int64_t)n, ctx->stream));
+  ctx->launches += 2;
+}
+
+struct U32ToU64 {
+  __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+};
+
+void build_plan(catgnn_shard_s* s) {
+  catgnn_ctx ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
   const uint32_t U = env_unit_cost();
   static const uint64_t row_cost = [] {  // per-row overhead in edge units (A/B knob)
     const char* v = std::getenv("CATGNN_ROW_COST");
     return (uint64_t)(v && *v ? std::max(1L, std::strtol(v, nullptr, 10)) : 32L);  // 32: measured best on the reddit shards (scripts/plan_sweep.sh)
   }();
-  std::vector<int4> units, heavy;
-  uint64_t chunks = 0, cost = 0, begin = 0;
-  for (uint64_t r = 0; r < s->rows; ++r) {
-    uint64_t deg = (uint64_t)(rp[r + 1] - rp[r]);
-    if (deg > U) {
-      if (r > begin) units.push_back(make_int4((int)begin, (int)r, -1, 0));
-      uint64_t nch = (deg + U - 1) / U;
-      heavy.push_back(make_int4((int)r, (int)chunks, (int)nch, 0));
-      for (uint64_t c = 0; c < nch; ++c)
-        units.push_back(make_int4((int)r, (int)c, (int)(chunks + c), 0));
-      chunks += nch;
-      begin = r + 1;
-      cost = 0;
-    } else {
-      cost += deg + row_cost;
-      if (cost >= U) {
-        units.push_back(make_int4((int)begin, (int)(r + 1), -1, 0));
-        begin = r + 1;
-        cost = 0;
-      }
-    }
-  }
-  if (begin < s->rows) units.push_back(make_int4((int)begin, (int)s->rows, -1, 0));
+  const uint64_t rows = s->rows;
   s->unit_cost = U;
-  s->n_units = units.size();
-  s->n_heavy = heavy.size();
-  s->n_chunks = chunks;
-  s->units.alloc(std::max<size_t>(1, units.size()));
-  s->heavy.alloc(std::max<size_t>(1, heavy.size()));
-  if (!units.empty())
-    CG_CUDA(cudaMemcpyAsync(s->units.p, units.data(), units.size() * sizeof(int4),
-                            cudaMemcpyHostToDevice, s->ctx->stream));
-  if (!heavy.empty())
-    CG_CUDA(cudaMemcpyAsync(s->heavy.p, heavy.data(), heavy.size() * sizeof(int4),
-                            cudaMemcpyHostToDevice, s->ctx->stream));
-  CG_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  if (rows == 0) {
+    s->n_units = s->n_heavy = s->n_chunks = 0;
+    s->units.alloc(1);
+    s->heavy.alloc(1);
+    return;
+  }
+  const uint64_t n1 = rows + 1;  // one extra slot: the scans' totals
+  uint64_t* cost = ctx->scratch_buf<uint64_t>("k1_plan_cost", n1);
+  uint64_t* P = ctx->scratch_buf<uint64_t>("k1_plan_P", n1);
+  uint32_t* nch = ctx->scratch_buf<uint32_t>("k1_plan_nch", n1);
+  uint32_t* emit = ctx->scratch_buf<uint32_t>("k1_plan_emit", n1);
+  uint32_t* ish = ctx->scratch_buf<uint32_t>("k1_plan_heavy", n1);
+  uint64_t* upos = ctx->scratch_buf<uint64_t>("k1_plan_upos", n1);
+  uint64_t* hpos = ctx->scratch_buf<uint64_t>("k1_plan_hpos", n1);
+  uint64_t* cpos = ctx->scratch_buf<uint64_t>("k1_plan_cpos", n1);
+  CG_CUDA(cudaMemsetAsync(cost + rows, 0, 8, st));
+  CG_CUDA(cudaMemsetAsync(nch + rows, 0, 4, st));
+  CG_CUDA(cudaMemsetAsync(emit + rows, 0, 4, st));
+  CG_CUDA(cudaMemsetAsync(ish + rows, 0, 4, st));
+  plan_rows_kernel<<<grid_for(rows), 256, 0, st>>>(s->row_ptr.p, rows, U, row_cost, cost, nch);
+  CG_CHECK_LAUNCH();
+  exclusive_scan(ctx, cost, P, n1);
+  plan_emit_kernel<<<grid_for(rows), 256, 0, st>>>(P, nch, rows, U, emit, ish);
+  CG_CHECK_LAUNCH();
+  auto e64 = thrust::make_transform_iterator(emit, U32ToU64());
+  auto h64 = thrust::make_transform_iterator(ish, U32ToU64());
+  auto c64 = thrust::make_transform_iterator(nch, U32ToU64());
+  exclusive_scan(ctx, e64, upos, n1);
+  exclusive_scan(ctx, h64, hpos, n1);
+  exclusive_scan(ctx, c64, cpos, n1);
+  uint64_t tot[3];
+  CG_CUDA(cudaMemcpyAsync(&tot[0], upos + rows, 8, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaMemcpyAsync(&tot[1], hpos + rows, 8, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaMemcpyAsync(&tot[2], cpos + rows, 8, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+  s->n_units = tot[0];
+  s->n_heavy = tot[1];
+  s->n_chunks = tot[2];
+  if (s->n_units >= 0x7fffffffull || s->n_chunks >= 0x7fffffffull)
+    throw ConfigError("aggregation plan exceeds the int32 unit range");
+  s->units.alloc(std::max<uint64_t>(1, s->n_units));
+  s->heavy.alloc(std::max<uint64_t>(1, s->n_heavy));
+  plan_scatter_kernel<<<grid_for(rows), 256, 0, st>>>(nch, emit, upos, hpos, cpos, rows, s->units.p, s->heavy.p);
+  CG_CHECK_LAUNCH();
+  plan_ends_kernel<<<grid_for(s->n_units), 256, 0, st>>>(s->units.p, s->n_units, rows);
+  CG_CHECK_LAUNCH();
+  ctx->launches += 4;
 }
 
 }  // namespace
@@ -195,11 +286,10 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
     CG_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, it, s->row_ptr.p + 1, (int)rows, st));
     ctx->launches += 2;
   }
-  std::vector<int64_t> rp(rows + 1);
-  CG_CUDA(cudaMemcpyAsync(rp.data(), s->row_ptr.p, sizeof(int64_t) * (rows + 1),
-                          cudaMemcpyDeviceToHost, st));
+  int64_t nnz = 0;
+  CG_CUDA(cudaMemcpyAsync(&nnz, s->row_ptr.p + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CG_CUDA(cudaStreamSynchronize(st));
-  s->nnz = (uint64_t)rp[rows];
+  s->nnz = (uint64_t)nnz;
   if (s->nnz >= 0x7fffffffull * 2) throw ConfigError("shard nnz exceeds the sort index range");
 
   s->col.alloc(std::max<uint64_t>(1, s->nnz));
@@ -233,7 +323,7 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
     CG_CHECK_LAUNCH();
     ctx->launches++;
   }
-  build_plan(s, rp);
+  build_plan(s);
 }
 
 void map_ext_edges(catgnn_ctx ctx, const uint64_t* d_ext_ids, uint64_t rows,

@@ -317,8 +317,8 @@ __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint3
   return v * e.out_scale;
 }
 __device__ __forceinline__ void store_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
-  if (e.out_h) e.out_h[(size_t)row * e.ld_out + e.out_col + col] = __float2half_rn(v);
-  else e.out[(size_t)row * e.ld_out + e.out_col + col] = v;
+  if (e.out_h) e.out_h[(size_t)row * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col] = __float2half_rn(v);
+  if (e.out) e.out[(size_t)row * e.ld_out + e.out_col + col] = v;
 }
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
       // (a whole-tile prefetch with the chunk loop unrolled measured slower)
       const uint32_t* mrow = (e.mask_bits && row_ok) ? e.mask_bits + (size_t)row * e.mask_words : nullptr;
       const uint32_t cfirst = 32 * chalf;
+      float rmax = 0.f;  // max |v| of this row over the chunks this warp stores (e.rowmax)
       uint32_t mw_next = (mrow && cfirst < BN && n0 + cfirst < args.N) ? __ldg(mrow + (n0 + cfirst) / 32) : 0xffffffffu;
       for (uint32_t c = cfirst; c < BN; c += kCStep) {
         const uint32_t mw_cur = mw_next;
@@ -658,6 +659,8 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
             }
             o.x *= e.out_scale; o.y *= e.out_scale; o.z *= e.out_scale; o.w *= e.out_scale;
             bw |= ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3)) << (4 * i);
+            if (e.rowmax && 4 * i < nc)
+              rmax = fmaxf(rmax, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
             T[lane * kTileLd4 + i] = o;
           }
           if (nc < 32) bw &= (1u << nc) - 1u;  // staged columns past the stored ones are not results
@@ -669,18 +672,19 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
               const uint32_t rr = f / n8, cc = f % n8, grow = rbase + rr;
               if (grow < args.M) {
                 const float4 a = T[rr * kTileLd4 + 2 * cc], b = T[rr * kTileLd4 + 2 * cc + 1];
-                reinterpret_cast<uint4*>(e.out_h + (size_t)grow * e.ld_out + e.out_col + col0)[cc] =
+                reinterpret_cast<uint4*>(e.out_h + (size_t)grow * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col0)[cc] =
                     make_uint4(pack_h2(a.x, a.y), pack_h2(a.z, a.w), pack_h2(b.x, b.y), pack_h2(b.z, b.w));
               }
             }
-          } else if (nc == 32) {
+          }
+          if (e.out && nc == 32) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const uint32_t rr = 4 * i + r8, grow = rbase + rr;
               if (grow < args.M)
                 reinterpret_cast<float4*>(e.out + (size_t)grow * e.ld_out + e.out_col + col0)[c4] = T[rr * kTileLd4 + c4];
             }
-          } else {  // ragged tail: nc/4 float4 per row, consecutive lanes along the row
+          } else if (e.out) {  // ragged tail: nc/4 float4 per row, consecutive lanes along the row
             const uint32_t n4 = nc / 4;
             for (uint32_t f = lane; f < 32 * n4; f += 32) {
               const uint32_t rr = f / n4, cc = f % n4, grow = rbase + rr;
@@ -719,6 +723,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
           }
         if (e.bits_out) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
       }
+      if (e.rowmax && row_ok && rmax > 0.f) atomicMax(reinterpret_cast<int*>(e.rowmax) + row, __float_as_int(rmax));
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
@@ -810,9 +815,11 @@ uint32_t pow2_cols(uint32_t n) {
 }  // namespace
 
 void check_epi_output(const GemmEpi& epi) {
-  if ((epi.out == nullptr) == (epi.out_h == nullptr)) throw ConfigError("GEMM needs exactly one output (fp32 or fp16)");
+  if (!epi.out && !epi.out_h) throw ConfigError("GEMM needs an output");
+  if (epi.out && epi.out_h && !epi.store_cols) throw ConfigError("GEMM fp32 + fp16 outputs need store_cols");
+  if (epi.rowmax && !epi.store_cols) throw ConfigError("GEMM row max needs store_cols (staged epilogue)");
   if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
-  if (epi.out_h && ((epi.ld_out % 8) || (epi.out_col % 8) || (epi.store_cols % 8)))
+  if (epi.out_h && (((epi.ld_h ? epi.ld_h : epi.ld_out) % 8) || (epi.out_col % 8) || (epi.store_cols % 8)))
     throw ConfigError("GEMM fp16 output: stride, column and store_cols must be multiples of 8");
   if (!(epi.out_scale > 0.f)) throw ConfigError("GEMM out_scale must be positive");
 }
@@ -873,7 +880,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   splits = std::max<uint32_t>(1, splits);
   const uint32_t kbps = std::max<uint32_t>(1, (nkb + splits - 1) / splits);
   splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
-  if (epi.bits_out && splits > 1) throw ConfigError("GEMM bit output needs an unsplit K");
+  if ((epi.bits_out || epi.rowmax) && splits > 1) throw ConfigError("GEMM bit / row-max output needs an unsplit K");
   if (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15))
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
@@ -1124,7 +1131,7 @@ void gemm_bf16x3(catgnn_ctx ctx, SplitOperand a, SplitOperand b, uint32_t M, uin
   splits = std::max<uint32_t>(1, splits);
   const uint32_t kbps = std::max<uint32_t>(1, (nkb + splits - 1) / splits);
   splits = std::max<uint32_t>(1, (nkb + kbps - 1) / kbps);
-  if (epi.bits_out && splits > 1) throw ConfigError("GEMM bit output needs an unsplit K");
+  if ((epi.bits_out || epi.rowmax) && splits > 1) throw ConfigError("GEMM bit / row-max output needs an unsplit K");
   if (epi.bias && (reinterpret_cast<uintptr_t>(epi.bias) & 15))
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
   static const int epi_env = [] {

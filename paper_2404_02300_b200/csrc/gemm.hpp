@@ -31,8 +31,13 @@ struct GemmEpi {
   // fp16 output rows instead of `out` (ld_out / out_col in halves, multiples
   // of 8): the input of an fp16 K2 pass; out_scale (a power of two) keeps
   // small values (gradients) in the fp16 normal range
+  // (out and out_h may both be set: the staged path writes both copies)
   __half* out_h = nullptr;
+  uint32_t ld_h = 0;  // out_h row stride in halves when both outputs are set (0: ld_out)
   float out_scale = 1.0f;
+  // per output row: max |v| over its columns, merged with atomicMax on the
+  // float bits (caller zero-fills; order-independent, so deterministic)
+  float* rowmax = nullptr;
   float* partial = nullptr;  // internal (split-K workspace)
 };
 

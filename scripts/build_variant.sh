@@ -16,5 +16,5 @@ s = s.replace("$(CURDIR)/../include", f"{root}/include").replace("../include/cat
 s = s.replace("NVFLAGS  := ", f"NVFLAGS  := {defs} ", 1)
 open(f"{out}/Makefile", "w").write(s)
 PY
-make -C "$out" -j8 > "$out/build.log" 2>&1 || { tail -20 "$out/build.log"; exit 1; }
+make -C "$out" -j8 libcatgnn.so > "$out/build.log" 2>&1 || { tail -20 "$out/build.log"; exit 1; }
 echo "$out/libcatgnn.so"

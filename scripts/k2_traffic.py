@@ -28,11 +28,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
          "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6, "%": 1, "": 1}
 
 
-def compulsory_bytes(nnz, rows, width, self_term):
-    """Each distinct input row read once, column indices and row offsets once,
-    each output row written once (what an infinite cache would move)."""
-    del self_term  # the self term reads a row that is already counted
-    return 4 * width * rows * 2 + 4 * nnz + 8 * (rows + 1)
+def compulsory_bytes(nnz, rows, width, eb):
+    """Each distinct input row read once (eb bytes per element), column indices
+    and row offsets once, each output row written once (what an infinite cache
+    would move)."""
+    return (eb + 4) * width * rows + 4 * nnz + 8 * (rows + 1)
 
 
 def main():
@@ -62,6 +62,7 @@ def main():
     seq = [launches[k] for k in sorted(launches)]
     seq = seq[len(seq) // 2:]  # the timed step (warm-up and timed steps launch the same sequence)
     widths = w.passes()
+    ebs = w.pass_elem_bytes()
     self_term = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
     passes, cur = [], None
     for d in seq:
@@ -73,23 +74,23 @@ def main():
             continue
         i = len(passes)
         part, pi = i // len(widths), i % len(widths)
-        width = widths[pi]
+        width, eb = widths[pi], ebs[pi]
         nnz, rows = meta["part_nnz"][part], meta["part_rows"][part]
-        cur = {"partition": part, "pass": pi, "width": width, "kernel": d["kernel"],
+        cur = {"partition": part, "pass": pi, "width": width, "elem_bytes": eb, "kernel": d["kernel"],
                "time_us": d["gpu__time_duration.sum"],
                "dram_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
                "dram_read": d["dram__bytes_read.sum"], "dram_write": d["dram__bytes_write.sum"],
                "l2_bytes": d["lts__t_bytes.sum"], "l2_hit_pct": d["lts__t_sector_hit_rate.pct"],
                "l1_hit_pct": d["l1tex__t_sector_hit_rate.pct"], "fixups": 0,
-               "algorithmic_bytes": nnz * (4 + 4 * width) + rows * (4 * width * (1 + self_term) + 8),
-               "compulsory_bytes": compulsory_bytes(nnz, rows, width, self_term)}
+               "algorithmic_bytes": nnz * (4 + eb * width) + rows * (eb * width * self_term + 4 * width + 8),
+               "compulsory_bytes": compulsory_bytes(nnz, rows, width, eb)}
         passes.append(cur)
     assert len(passes) == w.partitions * len(widths), (len(passes), w.partitions, widths)
     tot = {k: sum(p[k] for p in passes) for k in ("time_us", "dram_bytes", "l2_bytes", "algorithmic_bytes",
                                                   "compulsory_bytes")}
     by_width = {}
     for p in passes:
-        b = by_width.setdefault(str(p["width"]), {"launches": 0, "time_us": 0.0, "dram_bytes": 0.0,
+        b = by_width.setdefault(f'{p["width"]} {"f16" if p["elem_bytes"] == 2 else "f32"}', {"launches": 0, "time_us": 0.0, "dram_bytes": 0.0,
                                                   "algorithmic_bytes": 0.0, "compulsory_bytes": 0.0})
         b["launches"] += 1
         for k in ("time_us", "dram_bytes", "algorithmic_bytes", "compulsory_bytes"):
