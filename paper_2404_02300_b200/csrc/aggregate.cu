@@ -19,6 +19,7 @@
 // more than U neighbours are chunked; chunk partials are combined in chunk
 // order by agg_fixup_kernel, so results are deterministic.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -48,6 +49,18 @@ struct AggKernelArgs {
   uint32_t in_ld, in_col;
   float in_scale;                   // folded into the post scale (fp16 inputs stored scaled by 1/in_scale)
   int zero_row;                     // fp16 inputs: index of an all-zero row (= rows), the target of idle loads
+  // guarded fp16 forward (GUARD): per-row max |T_j| of the fp16-rounded rows,
+  // flagged-column bits, the rows with flags and their count, the threshold
+  // factor (see epilogue_row)
+  const float* __restrict__ gsmax;
+  uint32_t* __restrict__ flag_bits;
+  uint32_t* __restrict__ fix_rows;     // flagged light rows (warp-per-row fix)
+  unsigned int* fix_count;
+  uint32_t* __restrict__ fix_heavy;    // flagged split rows (block-per-row fix)
+  unsigned int* fix_hcount;
+  float* __restrict__ guard_part;      // per chunk: its neighbours' sum of squared row maxima
+  float* __restrict__ guard_pre;       // rows x 256: the fp16-path pre-activation of each flagged element
+  float guard_k;
   float* __restrict__ out;
   uint32_t out_ld, out_col;
   uint32_t w4;
@@ -164,16 +177,33 @@ __device__ __forceinline__ float post_scale(int norm, float deg) {
 // float4 columns c4 = (li + LPN*q)*CPV + h at acc[q*CPV + h] (CPV = 2 for fp16
 // input rows: a 16-byte vector then carries 8 columns).
 // selfv: the row's own input columns when already loaded (light units).
-template <int VPL, int LPN, bool BITS, int CPV>
+// GUARD (fp16 forward of a ReLU layer): s2 = sum over the row's gathered rows
+// (self included) of max_c |T_j[c]|^2.  Rounding T_j[c] to fp16 moves it by at
+// most 2^-11 |T_j[c]| (RN, uniform in +-half an ulp: variance <= 2^-22 T^2 / 3),
+// so the pre-activation a = post * sum + b carries an error of standard
+// deviation <= post * 2^-11 * sqrt(s2 / 3) (max_c |T_j[c]| over-estimates each
+// element's scale, so this bounds the true deviation).  Elements with |a| <
+// guard_k * post * sqrt(s2) (guard_k = 6 * 2^-11 / sqrt(3): 6 bounding standard
+// deviations, a tail probability < 2e-9; for rows with <= 12 terms also the
+// worst case n * 2^-11 * max) could have the other sign in exact arithmetic:
+// they are flagged (flag_bits), their fp16-path pre-activation kept
+// (guard_pre) and their row listed (fix_rows / fix_heavy) for the exact fix.
+template <int VPL, int LPN, bool BITS, int CPV, bool GUARD = false>
 __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, float deg,
                                              const float4 (&acc)[VPL * CPV], int li,
-                                             const float4 (*selfv)[VPL * CPV] = nullptr) {
+                                             const float4 (*selfv)[VPL * CPV] = nullptr, float s2 = 0.f) {
   // lanes [0, LPN) run this together (bit words are assembled across them)
   constexpr unsigned kLanes = LPN == 32 ? 0xffffffffu : ((1u << LPN) - 1u);
   constexpr int kGroup = LPN < 8 / CPV ? LPN : 8 / CPV;  // lanes whose nibbles form one 32-bit word
   const float post = post_scale(p.norm, deg) * p.in_scale;
   const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
   uint32_t nib[VPL * CPV];  // (out > 0) per column of each float4, for bits_out
+  uint32_t fnib[VPL * CPV];  // GUARD: flagged columns
+  float tau = 0.f;
+  if (GUARD) {  // + (deg + 1) * 2^-28: fp16 subnormals round to an absolute 2^-25
+    const float sm = __ldg(p.gsmax + r);
+    tau = p.guard_k * post * sqrtf(s2 + sm * sm + (deg + 1.f) * 0x1p-28f);
+  }
 #pragma unroll
   for (int q = 0; q < VPL; ++q)
 #pragma unroll
@@ -181,12 +211,18 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
       const int k = q * CPV + h;
       const uint32_t c4 = (li + LPN * q) * CPV + h;
       nib[k] = 0;
+      fnib[k] = 0;
       if (c4 >= p.w4) continue;
       float4 a = acc[k];
       if (p.self) fma4(a, selfs, selfv ? (*selfv)[k] : self4(p, r, c4));
       a.x *= post; a.y *= post; a.z *= post; a.w *= post;
       if (p.residual) add4(a, ldg4(p.residual + (size_t)r * p.res_ld + p.res_col + c4 * 4));
       if (p.bias) add4(a, ldg4(p.bias + c4 * 4));
+      if (GUARD) {
+        fnib[k] = (fabsf(a.x) < tau) | ((fabsf(a.y) < tau) << 1) | ((fabsf(a.z) < tau) << 2) | ((fabsf(a.w) < tau) << 3);
+        if (fnib[k])  // kept for the exact fix: it only adds the rounding residuals' contribution
+          *reinterpret_cast<float4*>(p.guard_pre + (size_t)r * 256 + c4 * 4) = a;
+      }
       if (p.relu) {
         a.x = fmaxf(a.x, 0.f); a.y = fmaxf(a.y, 0.f); a.z = fmaxf(a.z, 0.f); a.w = fmaxf(a.w, 0.f);
       }
@@ -211,15 +247,30 @@ __device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, 
       }
     }
   if (BITS && p.bits_out) {  // 1 bit per output element (> 0): the next backward's ReLU mask
+    bool anyf = false;
 #pragma unroll
     for (int q = 0; q < VPL; ++q) {
       const uint32_t c40 = (li + LPN * q) * CPV;
-      uint32_t w = 0;
+      uint32_t w = 0, fw = 0;
 #pragma unroll
-      for (int h = 0; h < CPV; ++h) w |= nib[q * CPV + h] << (((c40 + h) % 8) * 4);
+      for (int h = 0; h < CPV; ++h) {
+        w |= nib[q * CPV + h] << (((c40 + h) % 8) * 4);
+        if (GUARD) fw |= fnib[q * CPV + h] << (((c40 + h) % 8) * 4);
+      }
 #pragma unroll
-      for (int m = 1; m < kGroup; m <<= 1) w |= __shfl_xor_sync(kLanes, w, m);
-      if (c40 < p.w4 && c40 % 8 == 0) p.bits_out[(size_t)r * p.bits_words + c40 / 8] = w;
+      for (int m = 1; m < kGroup; m <<= 1) {
+        w |= __shfl_xor_sync(kLanes, w, m);
+        if (GUARD) fw |= __shfl_xor_sync(kLanes, fw, m);
+      }
+      if (c40 < p.w4 && c40 % 8 == 0) {
+        p.bits_out[(size_t)r * p.bits_words + c40 / 8] = w;
+        if (GUARD) p.flag_bits[(size_t)r * p.bits_words + c40 / 8] = fw;
+      }
+      anyf |= fw != 0;
+    }
+    if (GUARD && __any_sync(kLanes, anyf) && li == 0) {
+      if (deg > (float)p.U) p.fix_heavy[atomicAdd(p.fix_hcount, 1u)] = (uint32_t)r;
+      else p.fix_rows[atomicAdd(p.fix_count, 1u)] = (uint32_t)r;
     }
   }
 }
@@ -247,9 +298,10 @@ __device__ __forceinline__ uint4 ld_nbr(const char* base, uint32_t ldb, int j, i
 // Sum of pre[j]*in[j] over edges [e0, e1) into acc (reduced across groups).
 // Loads past the end of the range, and by lanes whose columns lie past the
 // row width, are skipped and contribute zeros.
-template <int VPL, int LPN, bool PRE, int CPV, bool FULLW, bool ZR>
+template <int VPL, int LPN, bool PRE, int CPV, bool FULLW, bool ZR, bool GUARD>
 __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64_t e1,
-                                       float4 (&acc)[VPL * CPV], int lane) {
+                                       float4 (&acc)[VPL * CPV], int lane, float* ss_out = nullptr) {
+  float ss = 0.f;  // GUARD: this chunk's sum of squared row maxima
   constexpr int G = 32 / LPN;  // neighbours processed side by side
   constexpr int UNROLL = VPL * CPV >= 4 ? 2 : (VPL * CPV >= 2 ? 4 : 8);
   const int g = lane / LPN, li = lane % LPN;
@@ -265,6 +317,10 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
     const int myj = lane < n ? ld_col(p, e + lane) : 0;
     float mys = 1.0f;
     if (PRE) mys = lane < n ? __ldg(p.pre + myj) : 0.0f;
+    if (GUARD) {
+      const float sj = lane < n ? __ldg(p.gsmax + myj) : 0.0f;
+      ss = fmaf(sj, sj, ss);
+    }
     for (int kb = 0; kb < n; kb += G * UNROLL) {
       uint4 v[UNROLL][VPL];
       float s[UNROLL];
@@ -293,6 +349,11 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
   for (int m = LPN; m < 32; m <<= 1)
 #pragma unroll
     for (int k = 0; k < VPL * CPV; ++k) add4(acc[k], shfl_xor4(acc[k], m));
+  if (GUARD) {
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+    *ss_out = ss;
+  }
 }
 
 // A light unit (whole rows [r0, r1), edges contiguous in col[]) walked as one
@@ -302,9 +363,14 @@ __device__ __forceinline__ void gather(const AggKernelArgs& p, int64_t e0, int64
 // 32 rows per coalesced load and each row's own input row (self term) is
 // requested together with its first neighbour batch.  Per row the G lane
 // groups split the neighbours, UNROLL batches in flight, xor-shuffle reduce.
-template <int VPL, int LPN, bool PRE, bool BITS, int CPV, bool FULLW, bool ZR>
+template <int VPL, int LPN, bool PRE, bool BITS, int CPV, bool FULLW, bool ZR, bool GUARD>
 __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, int64_t r1, int lane) {
   constexpr int G = 32 / LPN;
+  static_assert(!GUARD || (G == 1 && !PRE && BITS), "guarded passes: whole-warp rows, no source scale, ReLU bits");
+  // per-neighbour scalar streamed with the column indices: the source scale
+  // (PRE) or the guard's row max (GUARD)
+  constexpr bool SC = PRE || GUARD;
+  const float* __restrict__ sarr = PRE ? p.pre : p.gsmax;
 #ifndef AGG_NARROW_UNROLL
 #define AGG_NARROW_UNROLL 4
 #endif
@@ -328,9 +394,9 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   int cur = (cb + lane < E1) ? ld_col(p, cb + lane) : 0;
   int nxt = (cb + 32 + lane < E1) ? ld_col(p, cb + 32 + lane) : 0;
   float curs = 1.f, nxts = 1.f;
-  if (PRE) {
-    curs = (cb + lane < E1) ? __ldg(p.pre + cur) : 0.f;
-    nxts = (cb + 32 + lane < E1) ? __ldg(p.pre + nxt) : 0.f;
+  if (SC) {
+    curs = (cb + lane < E1) ? __ldg(sarr + cur) : 0.f;
+    nxts = (cb + 32 + lane < E1) ? __ldg(sarr + nxt) : 0.f;
   }
   const char* base = lane_base<CPV>(p, li);
   const uint32_t ldb = row_bytes<CPV>(p);
@@ -357,6 +423,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
       float4 acc[VPL * CPV];
 #pragma unroll
       for (int k = 0; k < VPL * CPV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      float ss = 0.f;  // GUARD: sum of the gathered rows' squared maxima (same on every lane)
       for (int64_t e = e0; e < e1; e += B) {
         while (e >= cb + 32) {  // warp-uniform: advance the index window by one chunk
           cb += 32;
@@ -364,7 +431,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
           curs = nxts;
           const bool ok = cb + 32 + lane < E1;
           nxt = ok ? ld_col(p, cb + 32 + lane) : 0;
-          if (PRE) nxts = ok ? __ldg(p.pre + nxt) : 0.f;
+          if (SC) nxts = ok ? __ldg(sarr + nxt) : 0.f;
         }
         uint4 v[UNROLL][VPL];
         float s[UNROLL];
@@ -377,7 +444,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
           const int wb = __shfl_sync(0xffffffffu, nxt, off & 31);
           const int win = off < 32 ? wa : wb;
           float wins = 1.f;
-          if (PRE) {
+          if (SC) {
             const float sa = __shfl_sync(0xffffffffu, curs, off & 31);
             const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
             wins = off < 32 ? sa : sb;
@@ -386,8 +453,9 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 #pragma unroll
           for (int uu = 0; uu < UNROLL; ++uu) {
             const int j = __shfl_sync(0xffffffffu, win, uu);
-            s[uu] = PRE ? __shfl_sync(0xffffffffu, wins, uu) : 1.f;
+            s[uu] = SC ? __shfl_sync(0xffffffffu, wins, uu) : 1.f;
             ok[uu] = uu < rem;
+            if (GUARD && ok[uu]) ss = fmaf(s[uu], s[uu], ss);
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
               if constexpr (ZR)  // idle slots load the zero row
@@ -432,14 +500,14 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
       for (int m = LPN; m < 32; m <<= 1)
 #pragma unroll
         for (int k = 0; k < VPL * CPV; ++k) add4(acc[k], shfl_xor4(acc[k], m));
-      if (writer) epilogue_row<VPL, LPN, BITS, CPV>(p, r, (float)(e1 - e0), acc, li, &selfv);
+      if (writer) epilogue_row<VPL, LPN, BITS, CPV, GUARD>(p, r, (float)(e1 - e0), acc, li, &selfv, ss);
     }
   }
 }
 
 // Persistent unit loop shared by both aggregation kernels: warps pull work
 // units from the atomic counter (the next one prefetched by lane 0).
-template <int VPL, int LPN, bool PRE, bool BITS, int CPV, bool FULLW, bool ZR>
+template <int VPL, int LPN, bool PRE, bool BITS, int CPV, bool FULLW, bool ZR, bool GUARD>
 __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
   const int lane = threadIdx.x & 31;
   const int li = lane % LPN;
@@ -452,14 +520,16 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
     if (lane == 0) next = atomicAdd(p.counter, 1u);  // prefetch the next unit
     const int4 w = __ldg(p.units + u);
     if (w.z < 0) {
-      light_unit<VPL, LPN, PRE, BITS, CPV, FULLW, ZR>(p, w.x, w.y, lane);
+      light_unit<VPL, LPN, PRE, BITS, CPV, FULLW, ZR, GUARD>(p, w.x, w.y, lane);
     } else {
       float4 acc[VPL * CPV];
       const int64_t r = w.x;
       const int64_t rb = __ldg(p.row_ptr + r), re = __ldg(p.row_ptr + r + 1);
       const int64_t e0 = rb + (int64_t)w.y * p.U;
       const int64_t e1 = (re < e0 + (int64_t)p.U) ? re : e0 + (int64_t)p.U;
-      gather<VPL, LPN, PRE, CPV, FULLW, ZR>(p, e0, e1, acc, lane);
+      float ss = 0.f;
+      gather<VPL, LPN, PRE, CPV, FULLW, ZR, GUARD>(p, e0, e1, acc, lane, &ss);
+      if (GUARD && lane == 0) p.guard_part[w.z] = ss;
       if (writer) {
         float* dst = p.partials + (size_t)w.z * p.w4 * 4;
 #pragma unroll
@@ -481,9 +551,11 @@ __device__ __forceinline__ void unit_loop(const AggKernelArgs& p) {
 // FULLW: the row width fills every lane's vectors (no column predicate).
 // ZR: the input has a zero row at index rows (fp16 inputs always): idle
 // neighbour slots load it instead of being predicated off and zeroed.
-template <int VPL, int LPN, bool PRE, int MINB, bool BITS, int CPV, bool FULLW = false, bool ZR = (CPV == 2)>
+// GUARD: guarded fp16 forward of a ReLU layer (epilogue_row).
+template <int VPL, int LPN, bool PRE, int MINB, bool BITS, int CPV, bool FULLW = false, bool ZR = (CPV == 2),
+          bool GUARD = false>
 __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
-  unit_loop<VPL, LPN, PRE, BITS, CPV, FULLW, ZR>(p);
+  unit_loop<VPL, LPN, PRE, BITS, CPV, FULLW, ZR, GUARD>(p);
 }
 
 // One CTA per split row.  Warp w sums the row's chunk partials c = w, w+8,
@@ -493,13 +565,19 @@ __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
 // result is deterministic run to run.  Hub rows with ~100 chunks finish in
 // ~7 dependent loads instead of ~25 with one warp per row.
 constexpr int kFixWarps = 8;
-template <int VPL>
+template <int VPL, bool GUARD = false>
 __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
   __shared__ float4 part[kFixWarps][32 * VPL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint64_t h = blockIdx.x; h < p.n_heavy; h += gridDim.x) {
     const int4 hv = __ldg(p.heavy + h);
     const int64_t r = hv.x;
+    float ss = 0.f;
+    if (GUARD) {  // the guard's sum over the row's chunks (fixed order)
+      for (int c = lane; c < hv.z; c += 32) ss += __ldcg(p.guard_part + hv.y + c);
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+    }
     float4 acc[VPL], acc2[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = acc2[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -539,9 +617,131 @@ __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
         acc[q] = t;
       }
       const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
-      epilogue_row<VPL, 32, true, 1>(p, r, deg, acc, lane);
+      epilogue_row<VPL, 32, true, 1, GUARD>(p, r, deg, acc, lane, nullptr, ss);
     }
     __syncthreads();
+  }
+}
+
+// Exact recomputation of the guard's flagged elements (epilogue_row GUARD).
+// The producing GEMM wrote lo = (T - fp16(T)) * 2^11 next to the fp16 T K2
+// gathered, so the exact pre-activation is the fp16 path's (kept in
+// guard_pre by the epilogue) plus post * 2^-11 * (sum of lo over the row's
+// neighbours and itself): per flagged row, its flagged columns in groups of
+// four, each group one walk over the row's edges (one column-index load and up
+// to four residual loads per edge), lanes strided over the edges and a fixed
+// xor / warp-order reduction — deterministic.  Then bias is already in, ReLU;
+// the value replaces the fp16-path result in the bf16x3 output pair (and fp32
+// output) and its ReLU bit is set or cleared.  Light rows: a warp each; split
+// (heavy) rows: a 256-thread block each.
+__device__ __forceinline__ void fix_store(const AggKernelArgs& p, uint32_t r, uint32_t c, float lo_sum,
+                                          const __half* __restrict__ lo, float post) {
+  const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
+  float s = lo_sum;
+  if (p.self) s = fmaf(selfs, __half2float(__ldg(lo + (size_t)r * p.in_ld + p.in_col + c)), s);
+  float v = fmaf(post * 0x1p-11f, s, p.guard_pre[(size_t)r * 256 + c]);
+  if (p.relu) v = fmaxf(v, 0.f);
+  if (p.out) p.out[(size_t)r * p.out_ld + p.out_col + c] = v;
+  if (p.out_hi) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+    reinterpret_cast<__nv_bfloat16*>(p.out_hi)[(size_t)r * p.out_s_ld + c] = h;
+    reinterpret_cast<__nv_bfloat16*>(p.out_lo)[(size_t)r * p.out_s_ld + c] = l;
+  }
+  uint32_t* bw = p.bits_out + (size_t)r * p.bits_words + c / 32;
+  if (v > 0.f) atomicOr(bw, 1u << (c % 32));
+  else atomicAnd(bw, ~(1u << (c % 32)));
+}
+// the next up-to-4 flagged columns of row r at or after word w / remaining bits fw
+__device__ __forceinline__ int next_cols(const AggKernelArgs& p, uint32_t r, uint32_t& w, uint32_t& fw,
+                                         uint32_t (&cols)[4]) {
+  int nc = 0;
+  while (nc < 4) {
+    while (!fw) {
+      if (++w >= p.bits_words) return nc;
+      fw = p.flag_bits[(size_t)r * p.bits_words + w];
+    }
+    cols[nc++] = w * 32 + (__ffs(fw) - 1);
+    fw &= fw - 1;
+  }
+  return nc;
+}
+__device__ __forceinline__ float lo_at(const __half* __restrict__ lo, size_t i) { return __half2float(__ldg(lo + i)); }
+__global__ void __launch_bounds__(256) agg_exact_fix_kernel(const AggKernelArgs p, const __half* __restrict__ lo) {
+  const int lane = threadIdx.x & 31;
+  const unsigned n = *p.fix_count;
+  for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t r = p.fix_rows[i];
+    const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
+    const float post = post_scale(p.norm, (float)(e1 - e0));
+    uint32_t w = 0, fw = p.flag_bits[(size_t)r * p.bits_words];
+    uint32_t cols[4];
+    for (int nc; (nc = next_cols(p, r, w, fw, cols)) > 0;) {
+      float a[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int64_t e = e0 + lane; e < e1; e += 32) {
+        const size_t jb = (size_t)__ldg(p.col + e) * p.in_ld + p.in_col;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < nc) a[k] += lo_at(lo, jb + cols[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], m);
+      if (lane < nc) {
+        float mine = a[0];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) mine = lane == k ? a[k] : mine;
+        fix_store(p, r, cols[lane], mine, lo, post);
+      }
+    }
+  }
+}
+__global__ void __launch_bounds__(256) agg_exact_fix_heavy_kernel(const AggKernelArgs p,
+                                                                  const __half* __restrict__ lo) {
+  __shared__ float red[8][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned n = *p.fix_hcount;
+  for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t r = p.fix_heavy[i];
+    const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
+    const float post = post_scale(p.norm, (float)(e1 - e0));
+    uint32_t w = 0, fw = p.flag_bits[(size_t)r * p.bits_words];
+    uint32_t cols[4];
+    for (int nc; (nc = next_cols(p, r, w, fw, cols)) > 0;) {
+      float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+      int64_t e = e0 + threadIdx.x;
+      for (; e + 256 < e1; e += 512) {  // two edges in flight per thread
+        const size_t ja = (size_t)__ldg(p.col + e) * p.in_ld + p.in_col;
+        const size_t jb = (size_t)__ldg(p.col + e + 256) * p.in_ld + p.in_col;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < nc) { a[k] += lo_at(lo, ja + cols[k]); b[k] += lo_at(lo, jb + cols[k]); }
+      }
+      if (e < e1) {
+        const size_t ja = (size_t)__ldg(p.col + e) * p.in_ld + p.in_col;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < nc) a[k] += lo_at(lo, ja + cols[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a[k] += b[k];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], m);
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) red[warp][k] = a[k];
+      __syncthreads();
+      if (warp == 0 && lane < nc) {
+        float s = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][lane];
+        fix_store(p, r, cols[lane], s, lo, post);
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -572,11 +772,18 @@ AggFn pick_h16(bool bits) {
   return bits ? agg_kernel<VPL, LPN, false, 3, true, 2, FULLW> : agg_kernel<VPL, LPN, false, MINB, false, 2, FULLW>;
 }
 
+// 6 standard deviations of the fp16 rounding error (epilogue_row GUARD)
+constexpr float kGuardK = 6.0f * 0x1p-11f / 1.7320508f;
+
 // Width slab handled by one launch: at most 32 lanes x 8 float4 = 1024 floats.
 constexpr uint32_t kMaxSlab4 = 256;
 
 
-AggFn pick_kernel(uint32_t w4, bool pre, bool bits, bool h16, bool zr, int* lpn_out) {
+AggFn pick_kernel(uint32_t w4, bool pre, bool bits, bool h16, bool zr, bool guard, int* lpn_out) {
+  if (guard) {  // guarded fp16 forward: 256 columns, ReLU bits (checked by aggregate())
+    *lpn_out = 32;
+    return agg_kernel<1, 32, false, 3, true, 2, true, true, true>;
+  }
   if (!h16 && zr && w4 == 64) {  // 256 fp32 columns, zero row: no predicates in the gather
     *lpn_out = 32;
     if (bits) return pre ? agg_kernel<2, 32, true, 3, true, 1, true, true> : agg_kernel<2, 32, false, 3, true, 1, true, true>;
@@ -661,6 +868,9 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
   if (a.in == a.out && a.in && a.in_ld != a.out_ld) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
   if (!a.out && !a.out_hi) throw ConfigError("aggregation needs an output");
+  if (a.guard_smax && (!a.in_h || a.width != 256 || !a.bits_out || !a.relu || a.pre || a.mask_bits || a.residual ||
+                       !a.guard_flags || !a.guard_lo || a.bits_words != 8))
+    throw ConfigError("guarded fp16 aggregation: fp16 input, 256 columns, ReLU with bit output, fp16 residual");
   if (a.in_h && (a.in || a.pre || a.in_ld % 8 || a.in_col % 8 || a.in_ld < a.in_col + round_up(a.width, 8)))
     throw ConfigError("fp16 aggregation input: no fp32 input / source scale, row stride and column a multiple of 8");
   if (a.out_hi && (!a.out_lo || a.out_s_ld % 8 || a.out_s_ld < a.width))
@@ -709,8 +919,25 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     static const int hint = env_int("CATGNN_AGG_HINT", 1);
     p.stream_hint = hint;
     int lpn = 32;
+    const bool guard = a.guard_smax != nullptr;
+    if (guard) {
+      p.gsmax = a.guard_smax;
+      p.flag_bits = a.guard_flags;
+      p.fix_rows = ctx->scratch_buf<uint32_t>("k2_fix_rows", std::max<uint64_t>(1, s->rows));
+      p.fix_heavy = ctx->scratch_buf<uint32_t>("k2_fix_heavy", std::max<uint64_t>(1, s->n_heavy));
+      p.fix_count = ctx->scratch_buf<unsigned int>("k2_fix_count", 2);
+      p.fix_hcount = p.fix_count + 1;
+      p.guard_part = ctx->scratch_buf<float>("k2_guard_part", std::max<uint64_t>(1, s->n_chunks));
+      p.guard_pre = ctx->scratch_buf<float>("k2_guard_pre", std::max<uint64_t>(1, s->rows) * 256);
+      static const float gk = [] {  // diagnostics: threshold in standard deviations (default 8)
+        const char* v = std::getenv("CATGNN_GUARD_SIGMA");
+        return v ? (float)std::atof(v) / 6.0f : 1.0f;
+      }();
+      p.guard_k = kGuardK * gk;
+      CG_CUDA(cudaMemsetAsync(p.fix_count, 0, 2 * sizeof(unsigned int), ctx->stream));
+    }
     AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, a.in_h != nullptr,
-                           a.in_zero_row && W4 == w4, &lpn);
+                           a.in_zero_row && W4 == w4, guard, &lpn);
     CG_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), ctx->stream));
     static const int detail = env_int("CATGNN_TIMING_DETAIL", 0);  // label per shard (rows)
     int t = ctx->begin_timed(0, ctx->timing ? "K2 agg w" + std::to_string(w4 * 4) + (a.in_h ? " f16" : "") +
@@ -728,11 +955,35 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     CG_CHECK_LAUNCH();
     ctx->launches++;
     if (s->n_heavy) {
-      AggFn fx = pick_fixup(w4);
+      AggFn fx = guard ? agg_fixup_kernel<2, true> : pick_fixup(w4);
       const unsigned g2 = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 16);
       fx<<<g2, 256, 0, ctx->stream>>>(p);
       CG_CHECK_LAUNCH();
       ctx->launches++;
+    }
+    static const int nofix = env_int("CATGNN_GUARD_NOFIX", 0);  // diagnostics (wrong results)
+    if (guard && !nofix) {  // exact fp32 recomputation of the flagged elements
+      int tf = ctx->begin_timed(3, ctx->timing ? std::string("(within K2 w256) guard exact fix") : std::string());
+      agg_exact_fix_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
+      CG_CHECK_LAUNCH();
+      if (s->n_heavy) {
+        agg_exact_fix_heavy_kernel<<<(unsigned)std::min<uint64_t>(s->n_heavy, ctx->num_sms * 4), 256, 0,
+                                     ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
+        CG_CHECK_LAUNCH();
+        ctx->launches++;
+      }
+      ctx->end_timed(tf);
+      ctx->launches++;
+      static const int stats = env_int("CATGNN_GUARD_STATS", 0);  // diagnostics: flagged rows per pass
+      if (stats) {
+        unsigned n = 0;
+        CG_CUDA(cudaMemcpyAsync(&n, p.fix_count, sizeof(n), cudaMemcpyDeviceToHost, ctx->stream));
+        CG_CUDA(cudaStreamSynchronize(ctx->stream));
+        unsigned nh = 0;
+        CG_CUDA(cudaMemcpy(&nh, p.fix_hcount, sizeof(nh), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[guard] rows %llu flagged rows %u + split rows %u of %llu\n", (unsigned long long)s->rows, n,
+                nh, (unsigned long long)s->n_heavy);
+      }
     }
     ctx->end_timed(t);
   }

@@ -672,8 +672,19 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
               const uint32_t rr = f / n8, cc = f % n8, grow = rbase + rr;
               if (grow < args.M) {
                 const float4 a = T[rr * kTileLd4 + 2 * cc], b = T[rr * kTileLd4 + 2 * cc + 1];
-                reinterpret_cast<uint4*>(e.out_h + (size_t)grow * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col0)[cc] =
-                    make_uint4(pack_h2(a.x, a.y), pack_h2(a.z, a.w), pack_h2(b.x, b.y), pack_h2(b.z, b.w));
+                const uint4 h = make_uint4(pack_h2(a.x, a.y), pack_h2(a.z, a.w), pack_h2(b.x, b.y), pack_h2(b.z, b.w));
+                const size_t o = (size_t)grow * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col0;
+                reinterpret_cast<uint4*>(e.out_h + o)[cc] = h;
+                if (e.out_hl) {  // rounding residual, scaled into the fp16 normal range
+                  const __half2* hh = reinterpret_cast<const __half2*>(&h);
+                  const float2 h0 = __half22float2(hh[0]), h1 = __half22float2(hh[1]);
+                  const float2 h2 = __half22float2(hh[2]), h3 = __half22float2(hh[3]);
+                  reinterpret_cast<uint4*>(e.out_hl + o)[cc] =
+                      make_uint4(pack_h2((a.x - h0.x) * 2048.f, (a.y - h0.y) * 2048.f),
+                                 pack_h2((a.z - h1.x) * 2048.f, (a.w - h1.y) * 2048.f),
+                                 pack_h2((b.x - h2.x) * 2048.f, (b.y - h2.y) * 2048.f),
+                                 pack_h2((b.z - h3.x) * 2048.f, (b.w - h3.y) * 2048.f));
+                }
               }
             }
           }
@@ -818,6 +829,7 @@ void check_epi_output(const GemmEpi& epi) {
   if (!epi.out && !epi.out_h) throw ConfigError("GEMM needs an output");
   if (epi.out && epi.out_h && !epi.store_cols) throw ConfigError("GEMM fp32 + fp16 outputs need store_cols");
   if (epi.rowmax && !epi.store_cols) throw ConfigError("GEMM row max needs store_cols (staged epilogue)");
+  if (epi.out_hl && (!epi.out_h || !epi.store_cols)) throw ConfigError("GEMM fp16 residual needs out_h and store_cols");
   if ((epi.ld_out % 4) || (epi.out_col % 4)) throw ConfigError("GEMM output stride must be a multiple of 4");
   if (epi.out_h && (((epi.ld_h ? epi.ld_h : epi.ld_out) % 8) || (epi.out_col % 8) || (epi.store_cols % 8)))
     throw ConfigError("GEMM fp16 output: stride, column and store_cols must be multiples of 8");

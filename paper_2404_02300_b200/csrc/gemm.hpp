@@ -34,6 +34,7 @@ struct GemmEpi {
   // (out and out_h may both be set: the staged path writes both copies)
   __half* out_h = nullptr;
   uint32_t ld_h = 0;  // out_h row stride in halves when both outputs are set (0: ld_out)
+  __half* out_hl = nullptr;  // with out_h: fp16 (v - fp16(v)) * 2^11, same layout (hi + lo * 2^-11 ~ v to 2^-22)
   float out_scale = 1.0f;
   // per output row: max |v| over its columns, merged with atomicMax on the
   // float bits (caller zero-fills; order-independent, so deterministic)

@@ -519,6 +519,18 @@ bool f16_bwd(const catgnn_model_s* M, size_t l) {
   return M->act_f16 && bf_layer(M, l) && M->cfg.kind == CATGNN_MODEL_GCN;
 }
 bool f16_fwd(const catgnn_model_s* M, size_t l) { return f16_bwd(M, l) && l + 1 == M->layers.size(); }
+// A hidden GCN layer's forward as a guarded fp16 pass (aggregate.cu epilogue_row
+// GUARD): K2 gathers fp16 T and flags every element whose pre-activation lies
+// within 8 standard deviations of the rounding error of zero; those (~0.5%)
+// are recomputed in fp32 from an fp32 copy of T, so every ReLU mask bit is the
+// fp32 path's.  256-wide layers (CATGNN_ACT_F16_GUARD=0: fp32 forward).
+const bool kGuardEnv = [] {
+  const char* v = std::getenv("CATGNN_ACT_F16_GUARD");
+  return v ? v[0] != '0' : true;
+}();
+bool f16_guard(const catgnn_model_s* M, size_t l) {
+  return kGuardEnv && f16_bwd(M, l) && l + 1 < M->layers.size() && M->layers[l].D_out == 256;
+}
 // fp16 row stride: 32 / 64 halves (one 64- / 128-byte line) for narrow rows
 uint32_t ld_h16(uint32_t w) { return w <= 32 ? 32 : w <= 64 ? 64 : round_up(w, 8); }
 // (rows + 1) x ld: row `rows` stays zero (K2's idle-slot target)
@@ -648,13 +660,25 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN / SGC transform-first
       const bool h16 = f16_fwd(M, l);
+      const bool guard = f16_guard(M, l);
       __half* mid_h = nullptr;
+      float* smax = nullptr;
+      __half* mid_lo = nullptr;
       GemmEpi e; e.rowscale = gcn ? S->dinv.p : nullptr;
       if (h16) {  // T as fp16 rows: the K2 pass's only input
         b.mid_ld = ld_h16(L.D_out);
         mid_h = act_h(ctx, nm("midh", l), rows, b.mid_ld);
         e.out_h = mid_h; e.ld_out = b.mid_ld;
         e.store_cols = round_up(L.D_out, 8);  // the vectors K2 reads, zero padding included
+      } else if (guard) {  // fp16 T gathered, its rounding residual for the flagged elements, per-row max |T|
+        b.mid_ld = ld_h16(L.D_out);
+        mid_h = act_h(ctx, nm("midh", l), rows, b.mid_ld);
+        mid_lo = act_h(ctx, nm("midl", l), rows, b.mid_ld);
+        smax = ctx->scratch_buf<float>(nm("smax", l), rows + 1);
+        CG_CUDA(cudaMemsetAsync(smax, 0, (rows + 1) * sizeof(float), ctx->stream));
+        e.out_h = mid_h; e.out_hl = mid_lo; e.ld_out = b.mid_ld;
+        e.rowmax = smax;
+        e.store_cols = round_up(L.D_out, 8);
       } else {
         b.mid_ld = L.ld_act;
         b.mid = act(ctx, nm("mid", l), rows + 1, b.mid_ld, fresh);  // + zero row (K2's idle-slot target)
@@ -680,6 +704,11 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       AggArgs a;
       a.in = b.mid; a.in_ld = b.mid_ld; a.out = b.out; a.out_ld = b.out_ld; a.width = L.D_out;
       if (h16) { a.in = nullptr; a.in_h = mid_h; }
+      else if (guard) {
+        a.in = nullptr; a.in_h = mid_h;
+        a.guard_smax = smax; a.guard_lo = mid_lo;
+        a.guard_flags = act_bits(ctx, nm("Hflags", l), rows, b.bits_words);
+      }
       else a.in_zero_row = true;
       a.self = 1; a.norm = agg_norm(M); a.bias = bias; a.relu = !last;
       a.bits_out = b.bits; a.bits_words = b.bits_words;

@@ -80,6 +80,13 @@ struct AggArgs {
   const void* in_h = nullptr;
   float in_scale = 1.0f;
   bool in_zero_row = false;  // fp32 input: row `rows` exists and is zero (fp16: always required)
+  // guarded fp16 forward of a ReLU layer (aggregate.cu epilogue_row GUARD):
+  // per-row max |T| of the rounded rows (rows + 1 entries, the zero row 0),
+  // flag bits (rows x bits_words), and the fp16 rounding residual of in_h
+  // times 2^11 (same layout) the flagged elements are recomputed with
+  const float* guard_smax = nullptr;
+  uint32_t* guard_flags = nullptr;
+  const void* guard_lo = nullptr;
   uint32_t in_ld = 0, in_col = 0;
   float* out = nullptr;  // rows x out_ld, columns [out_col, out_col+width)
   uint32_t out_ld = 0, out_col = 0;

@@ -21,6 +21,7 @@ CASES = [  # kind, in_dim, hidden, classes, layers  (covers aggregate-first and 
     ("gin", 12, 48, 6, 2),
     ("gin", 140, 256, 172, 2),  # 129-192-wide aggregations (16 lanes x 3 float4): 140 fwd, 172 fwd/bwd
     ("gcn", 150, 160, 12, 2),   # 152-wide aggregate-first with the GCN source scale and ReLU bits
+    ("gcn", 602, 256, 41, 2),   # the bench shape: guarded fp16 forward of the 256-wide hidden layer
 ]
 
 
@@ -71,7 +72,7 @@ def test_single_step_outputs_and_grads(graph, kind, in_dim, hidden, classes, lay
         assert rel_err(gb, rb) < 2e-3, (l, "b", rel_err(gb, rb))
 
 
-@pytest.mark.parametrize("in_dim,hidden,classes", [(602, 64, 41), (150, 160, 12), (64, 256, 172)])
+@pytest.mark.parametrize("in_dim,hidden,classes", [(602, 64, 41), (150, 160, 12), (64, 256, 172), (602, 256, 41)])
 def test_gcn_fp16_aggregation_inputs(graph, in_dim, hidden, classes):
     """The fp16 K2 inputs (GCN backward gradients, last-layer forward) against
     the all-fp32 path and the oracle: both within the 2e-3 gate, and the fp16
