@@ -24,6 +24,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -400,6 +401,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   }
   const char* base = lane_base<CPV>(p, li);
   const uint32_t ldb = row_bytes<CPV>(p);
+  const int zrow = p.zero_row;
   bool colok[VPL];
 #pragma unroll
   for (int q = 0; q < VPL; ++q) colok[q] = FULLW || li + LPN * q < (int)n_vec<CPV>(p);
@@ -459,18 +461,19 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
               if constexpr (ZR)  // idle slots load the zero row
-                v[uu][q] = colok[q] ? ld_nbr<VPL, LPN>(base, ldb, ok[uu] ? j : p.zero_row, q) : make_uint4(0u, 0u, 0u, 0u);
+                v[uu][q] = colok[q] ? ld_nbr<VPL, LPN>(base, ldb, ok[uu] ? j : zrow, q) : make_uint4(0u, 0u, 0u, 0u);
               else
                 v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
             }
           }
         } else {
           // lane groups: two shuffles per neighbour keep the register budget
-          // of the 4-CTA/SM narrow kernels
+          // of the 4-CTA/SM narrow kernels; 32-bit offsets from the window
+          const int boff = (int)(e - cb) + g;  // < 32
+          const int lim = (int)(e1 - cb);      // the row's end, relative to the window
 #pragma unroll
           for (int uu = 0; uu < UNROLL; ++uu) {
-            const int64_t ee = e + uu * G + g;
-            const int off = (int)(ee - cb);  // < 32 + B <= 64
+            const int off = boff + uu * G;  // < 32 + B <= 64
             const int ja = __shfl_sync(0xffffffffu, cur, off & 31);
             const int jb = __shfl_sync(0xffffffffu, nxt, off & 31);
             const int j = off < 32 ? ja : jb;
@@ -481,11 +484,11 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             } else {
               s[uu] = 1.f;
             }
-            ok[uu] = ee < e1;
+            ok[uu] = off < lim;
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
-              if constexpr (ZR)  // idle slots load the zero row
-                v[uu][q] = colok[q] ? ld_nbr<VPL, LPN>(base, ldb, ok[uu] ? j : p.zero_row, q) : make_uint4(0u, 0u, 0u, 0u);
+              if constexpr (ZR)  // idle slots and lanes past the row width load the zero row
+                v[uu][q] = ld_nbr<VPL, LPN>(base, ldb, (ok[uu] && colok[q]) ? j : zrow, q);
               else
                 v[uu][q] = (ok[uu] && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, j, q) : make_uint4(0u, 0u, 0u, 0u);
             }
@@ -652,14 +655,14 @@ __device__ __forceinline__ void fix_store(const AggKernelArgs& p, uint32_t r, ui
   if (v > 0.f) atomicOr(bw, 1u << (c % 32));
   else atomicAnd(bw, ~(1u << (c % 32)));
 }
-// the next up-to-4 flagged columns of row r at or after word w / remaining bits fw
-__device__ __forceinline__ int next_cols(const AggKernelArgs& p, uint32_t r, uint32_t& w, uint32_t& fw,
-                                         uint32_t (&cols)[4]) {
+// the next up-to-4 flagged columns of a row at or after word w / remaining
+// bits fw; the row's 8 flag words sit in lanes 0-7 of `words` (one load)
+__device__ __forceinline__ int next_cols(uint32_t words, uint32_t& w, uint32_t& fw, uint32_t (&cols)[4]) {
   int nc = 0;
   while (nc < 4) {
     while (!fw) {
-      if (++w >= p.bits_words) return nc;
-      fw = p.flag_bits[(size_t)r * p.bits_words + w];
+      if (++w >= 8) return nc;
+      fw = __shfl_sync(0xffffffffu, words, w);
     }
     cols[nc++] = w * 32 + (__ffs(fw) - 1);
     fw &= fw - 1;
@@ -674,9 +677,10 @@ __global__ void __launch_bounds__(256) agg_exact_fix_kernel(const AggKernelArgs 
     const uint32_t r = p.fix_rows[i];
     const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
     const float post = post_scale(p.norm, (float)(e1 - e0));
-    uint32_t w = 0, fw = p.flag_bits[(size_t)r * p.bits_words];
+    const uint32_t words = lane < 8 ? p.flag_bits[(size_t)r * 8 + lane] : 0u;
+    uint32_t w = 0, fw = __shfl_sync(0xffffffffu, words, 0);
     uint32_t cols[4];
-    for (int nc; (nc = next_cols(p, r, w, fw, cols)) > 0;) {
+    for (int nc; (nc = next_cols(words, w, fw, cols)) > 0;) {
       float a[4] = {0.f, 0.f, 0.f, 0.f};
       for (int64_t e = e0 + lane; e < e1; e += 32) {
         const size_t jb = (size_t)__ldg(p.col + e) * p.in_ld + p.in_col;
@@ -706,9 +710,10 @@ __global__ void __launch_bounds__(256) agg_exact_fix_heavy_kernel(const AggKerne
     const uint32_t r = p.fix_heavy[i];
     const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
     const float post = post_scale(p.norm, (float)(e1 - e0));
-    uint32_t w = 0, fw = p.flag_bits[(size_t)r * p.bits_words];
+    const uint32_t words = lane < 8 ? p.flag_bits[(size_t)r * 8 + lane] : 0u;
+    uint32_t w = 0, fw = __shfl_sync(0xffffffffu, words, 0);
     uint32_t cols[4];
-    for (int nc; (nc = next_cols(p, r, w, fw, cols)) > 0;) {
+    for (int nc; (nc = next_cols(words, w, fw, cols)) > 0;) {
       float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
       int64_t e = e0 + threadIdx.x;
       for (; e + 256 < e1; e += 512) {  // two edges in flight per thread
@@ -964,7 +969,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     static const int nofix = env_int("CATGNN_GUARD_NOFIX", 0);  // diagnostics (wrong results)
     if (guard && !nofix) {  // exact fp32 recomputation of the flagged elements
       int tf = ctx->begin_timed(3, ctx->timing ? std::string("(within K2 w256) guard exact fix") : std::string());
-      agg_exact_fix_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
+      agg_exact_fix_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
       CG_CHECK_LAUNCH();
       if (s->n_heavy) {
         agg_exact_fix_heavy_kernel<<<(unsigned)std::min<uint64_t>(s->n_heavy, ctx->num_sms * 4), 256, 0,
@@ -981,8 +986,21 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
         CG_CUDA(cudaStreamSynchronize(ctx->stream));
         unsigned nh = 0;
         CG_CUDA(cudaMemcpy(&nh, p.fix_hcount, sizeof(nh), cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[guard] rows %llu flagged rows %u + split rows %u of %llu\n", (unsigned long long)s->rows, n,
-                nh, (unsigned long long)s->n_heavy);
+        std::vector<uint32_t> fl(s->rows * 8);
+        CG_CUDA(cudaMemcpy(fl.data(), p.flag_bits, fl.size() * 4, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> rp(s->rows + 1);
+        CG_CUDA(cudaMemcpy(rp.data(), s->row_ptr.p, rp.size() * 8, cudaMemcpyDeviceToHost));
+        uint64_t el = 0, work = 0;
+        for (uint64_t r = 0; r < s->rows; ++r) {
+          int c = 0;
+          for (int w = 0; w < 8; ++w) c += __builtin_popcount(fl[r * 8 + w]);
+          el += c;
+          work += (uint64_t)c * (uint64_t)(rp[r + 1] - rp[r] + 1);
+        }
+        fprintf(stderr, "[guard] rows %llu flagged rows %u + split rows %u of %llu; elements %llu (%.3f%%), "
+                "residual loads %llu (%.2f per edge)\n", (unsigned long long)s->rows, n, nh,
+                (unsigned long long)s->n_heavy, (unsigned long long)el, 100.0 * el / (s->rows * 256.0),
+                (unsigned long long)work, (double)work / (double)s->nnz);
       }
     }
     ctx->end_timed(t);

@@ -68,15 +68,16 @@ class Workload:
 
     def pass_elem_bytes(self) -> list:
         """Bytes per gathered input element of each pass in passes() order
-        (gnn.cu f16_fwd / f16_bwd): GCN transform-first layers gather fp16
-        rows backward, and the last layer also forward; everything else fp32."""
+        (gnn.cu f16_fwd / f16_guard / f16_bwd): GCN transform-first layers
+        gather fp16 rows backward, and forward the last layer and 256-wide
+        hidden layers (guarded); everything else fp32."""
         fwd, bwd = [], []
         for l in range(self.layers):
             d_in = self.dim if l == 0 else self.hidden
             d_out = self.classes if l + 1 == self.layers else self.hidden
             agg_first = d_in <= d_out if self.model == "sage" else d_in < d_out
             h16 = self.model == "gcn" and not agg_first
-            fwd.append(2 if h16 and l + 1 == self.layers else 4)
+            fwd.append(2 if h16 and (l + 1 == self.layers or d_out == 256) else 4)
             if not (agg_first and l == 0):
                 bwd.append(2 if h16 else 4)
         return fwd + bwd[::-1]
