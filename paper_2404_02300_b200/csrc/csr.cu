@@ -6,9 +6,9 @@
 // (u,v) appends v to row u and, when u != v, u to row v.  Expanding edge k into
 // the two entries (u->v) at position 2k and (v->u) at 2k+1 (dropped for
 // self-loops) and STABLY sorting by source row reproduces that order exactly:
-// inside a row the entries stay in ascending (k, side) order.  The sort is an
-// LSD radix sort over only ceil(log2(rows+1)) key bits (CUB onesweep), the
-// offsets are a degree histogram + scan.  Everything is int32 column indices
+// inside a row the entries stay in ascending (k, side) order.  The sort is our
+// own stable LSD radix sort (radix.cu) over only ceil(log2(rows+1)) key bits,
+// the offsets are a degree histogram + scan.  Everything is int32 column indices
 // and int64 offsets (train.hpp:19's u32 offsets overflow at papers scale).
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "radix.hpp"
 #include "shard.hpp"
 
 namespace catgnn {
@@ -304,15 +305,10 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
     ctx->launches++;
     int end_bit = 1;
     while (end_bit < 32 && (1ull << end_bit) <= rows) ++end_bit;  // sentinel = rows must fit
-    size_t tmp_bytes = 0;
-    CG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, v_in, v_out,
-                                            (int64_t)n2, 0, end_bit, st));
-    void* tmp = ctx->scratch_buf<unsigned char>("k1_cub", tmp_bytes);
-    CG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, v_in, v_out,
-                                            (int64_t)n2, 0, end_bit, st));
-    ctx->launches += 4;
+    uint32_t *k_res = nullptr, *v_res = nullptr;
+    radix_sort_pairs(ctx, k_in, v_in, k_out, v_out, n2, end_bit, &k_res, &v_res);  // stable (radix.cu)
     // entries with a real source come first (sentinel = rows sorts last)
-    CG_CUDA(cudaMemcpyAsync(s->col.p, v_out, s->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(s->col.p, v_res, s->nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   }
   s->dinv.alloc(std::max<uint32_t>(1, rows));
   s->inv_deg.alloc(std::max<uint32_t>(1, rows));
