@@ -105,6 +105,13 @@ int catgnn_artifact_part_counts(catgnn_artifact a, uint32_t part, uint64_t* node
 int catgnn_artifact_replica_map(catgnn_artifact a, uint32_t part, uint64_t* ext_ids,
                                 uint8_t* owner, uint8_t* role, uint32_t* home);
 
+/* The same home map for a loaded partition shard, built on the shard's device
+ * (K1's radix sort of every partition's owned ids, then a binary search of
+ * the shard's replica table; completion.cpp:46-50): home[r] for each local
+ * row (host array of rows entries, may be NULL) and the number of halo rows
+ * (replicas this partition does not own).  Dense ids below 2^32. */
+int catgnn_shard_halo_map(catgnn_shard s, catgnn_artifact a, uint32_t* home, uint64_t* n_halo);
+
 /* ------------------------------------------------------------ shards (A3-A4) */
 /* load_training_data (train.cpp:216-287) for one shard: part >= 0 is a
  * partition shard (local row i = i-th record of part-<i>/nodes.tsv; features

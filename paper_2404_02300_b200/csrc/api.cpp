@@ -442,6 +442,28 @@ int catgnn_artifact_replica_map(catgnn_artifact a, uint32_t part, uint64_t* ext_
   });
 }
 
+int catgnn_shard_halo_map(catgnn_shard s, catgnn_artifact a, uint32_t* home, uint64_t* n_halo) {
+  return guarded([&] {
+    if (!s || !a) throw ConfigError("null argument");
+    if (s->ext_ids.empty() && s->rows) throw ConfigError("shard was not loaded from a partition");
+    CG_CUDA(cudaSetDevice(s->ctx->device));
+    if (!s->d_ext.p && s->rows) {  // the device replica table (also the feature gathers' index)
+      s->d_ext.alloc(s->rows);
+      CG_CUDA(cudaMemcpyAsync(s->d_ext.p, s->ext_ids.data(), s->rows * 8, cudaMemcpyHostToDevice, s->ctx->stream));
+    }
+    std::vector<uint32_t> ids, parts;
+    for (uint32_t q = 0; q < a->parts.size(); ++q)
+      for (size_t i = 0; i < a->parts[q].ext.size(); ++i)
+        if (a->parts[q].owner[i]) {
+          if (a->parts[q].ext[i] > 0xffffffffull) throw ConfigError("halo map: ids beyond 2^32");
+          ids.push_back((uint32_t)a->parts[q].ext[i]);
+          parts.push_back(q);
+        }
+    const uint64_t h = halo_map(s, ids.data(), parts.data(), ids.size(), a->num_nodes, home);
+    if (n_halo) *n_halo = h;
+  });
+}
+
 // --------------------------------------------------------------- shards
 int catgnn_shard_load(catgnn_ctx ctx, catgnn_artifact a, int32_t part, const char* input,
                       const char* features, catgnn_shard* out) {

@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "radix.hpp"
 #include "shard.hpp"
@@ -338,6 +340,60 @@ void map_ext_edges(catgnn_ctx ctx, const uint64_t* d_ext_ids, uint64_t rows,
   // load_training_data uses unordered_map::at (train.cpp:271): a missing
   // endpoint escapes as std::out_of_range, i.e. the CLI's "internal" category.
   if (h) throw InternalError("partition edge endpoint missing from its node table (unordered_map::at)");
+}
+
+namespace {
+__global__ void halo_lookup_kernel(const uint64_t* __restrict__ ext, uint64_t rows, const uint32_t* __restrict__ ids,
+                                   const uint32_t* __restrict__ parts, uint64_t n, uint32_t* __restrict__ home,
+                                   unsigned int* __restrict__ missing) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = ext[r];
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if ((uint64_t)ids[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    if (lo < n && ids[lo] == key) home[r] = parts[lo];
+    else { home[r] = 0xFFFFFFFFu; atomicAdd(missing, 1u); }
+  }
+}
+}  // namespace
+
+uint64_t halo_map(catgnn_shard_s* s, const uint32_t* owner_ids, const uint32_t* owner_parts, uint64_t n_owned,
+                  uint64_t num_ids, uint32_t* home_host) {
+  catgnn_ctx ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  if (num_ids > 0xffffffffull) throw ConfigError("halo map: ids beyond 2^32");
+  const uint64_t n = std::max<uint64_t>(1, n_owned);
+  uint32_t* k = ctx->scratch_buf<uint32_t>("halo_k", n);
+  uint32_t* v = ctx->scratch_buf<uint32_t>("halo_v", n);
+  uint32_t* k2 = ctx->scratch_buf<uint32_t>("halo_k2", n);
+  uint32_t* v2 = ctx->scratch_buf<uint32_t>("halo_v2", n);
+  uint32_t* home = ctx->scratch_buf<uint32_t>("halo_home", std::max<uint64_t>(1, s->rows));
+  unsigned int* missing = ctx->scratch_buf<unsigned int>("halo_missing", 1);
+  CG_CUDA(cudaMemcpyAsync(k, owner_ids, n_owned * 4, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemcpyAsync(v, owner_parts, n_owned * 4, cudaMemcpyHostToDevice, st));
+  CG_CUDA(cudaMemsetAsync(missing, 0, sizeof(unsigned int), st));
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < num_ids) ++bits;
+  uint32_t *ks = nullptr, *vs = nullptr;
+  radix_sort_pairs(ctx, k, v, k2, v2, n_owned, bits, &ks, &vs);
+  if (s->rows) {
+    halo_lookup_kernel<<<grid_for(s->rows), 256, 0, st>>>(s->d_ext.p, s->rows, ks, vs, n_owned, home, missing);
+    CG_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  unsigned int h_missing = 0;
+  CG_CUDA(cudaMemcpyAsync(&h_missing, missing, sizeof(h_missing), cudaMemcpyDeviceToHost, st));
+  std::vector<uint32_t> hh(s->rows);
+  if (s->rows) CG_CUDA(cudaMemcpyAsync(hh.data(), home, s->rows * 4, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaStreamSynchronize(st));
+  if (h_missing) throw DataError("replica without an owner partition");
+  uint64_t halo = 0;
+  for (uint64_t r = 0; r < s->rows; ++r) halo += s->owner.empty() ? 0 : (s->owner[r] == 0);
+  if (home_host && s->rows) std::memcpy(home_host, hh.data(), s->rows * 4);
+  return halo;
 }
 
 void copy_rows(catgnn_ctx ctx, const float* in, uint32_t in_ld, float* out, uint32_t out_ld,

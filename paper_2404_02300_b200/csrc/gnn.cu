@@ -208,6 +208,59 @@ __global__ void colsum_partial_kernel(const void* __restrict__ X, uint32_t ld, u
     __syncthreads();
   }
 }
+// fp16 rows (rs[r] * x / scale, the fp16 K2 inputs): 16-byte loads of 8
+// columns, tpr threads per row, 256/tpr rows in flight, 4 loads in flight per
+// thread, fixed-order partials per block (deterministic); the per-row division
+// by rs is one reciprocal per loaded vector.
+__global__ void colsum_h16_kernel(const __half* __restrict__ X, uint32_t ld, uint64_t rows, uint32_t width,
+                                  float* __restrict__ partial, const float* __restrict__ rsc) {
+  __shared__ float4 red[256][2];
+  const uint32_t w8 = (width + 7) / 8;
+  const uint64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const uint64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  const uint32_t tpr = min(w8, 256u), rpi = 256 / tpr;
+  const uint32_t c8 = threadIdx.x % tpr, rs = threadIdx.x / tpr;
+  auto ld8 = [&](uint64_t r, float4& a, float4& b) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(X + r * ld) + c8);
+    const float f = rsc ? 1.0f / __ldg(rsc + r) : 1.0f;
+    const float2 x0 = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 x1 = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    const float2 x2 = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+    const float2 x3 = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+    a = make_float4(x0.x * f, x0.y * f, x1.x * f, x1.y * f);
+    b = make_float4(x2.x * f, x2.y * f, x3.x * f, x3.y * f);
+  };
+  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), b0 = a0, a1 = a0, b1 = a0;
+  if (rs < rpi && c8 < w8) {
+    uint64_t r = r0 + rs;
+    for (; r + rpi < r1; r += 2 * rpi) {
+      float4 x, y, z, w;
+      ld8(r, x, y);
+      ld8(r + rpi, z, w);
+      a0.x += x.x; a0.y += x.y; a0.z += x.z; a0.w += x.w; b0.x += y.x; b0.y += y.y; b0.z += y.z; b0.w += y.w;
+      a1.x += z.x; a1.y += z.y; a1.z += z.z; a1.w += z.w; b1.x += w.x; b1.y += w.y; b1.z += w.z; b1.w += w.w;
+    }
+    if (r < r1) {
+      float4 x, y;
+      ld8(r, x, y);
+      a0.x += x.x; a0.y += x.y; a0.z += x.z; a0.w += x.w; b0.x += y.x; b0.y += y.y; b0.z += y.z; b0.w += y.w;
+    }
+    a0.x += a1.x; a0.y += a1.y; a0.z += a1.z; a0.w += a1.w; b0.x += b1.x; b0.y += b1.y; b0.z += b1.z; b0.w += b1.w;
+  }
+  red[threadIdx.x][0] = a0;
+  red[threadIdx.x][1] = b0;
+  __syncthreads();
+  if (rs == 0 && c8 < w8) {
+    float4 sa = red[c8][0], sb = red[c8][1];
+    for (uint32_t k = 1; k < rpi; ++k) {
+      const float4 va = red[k * tpr + c8][0], vb = red[k * tpr + c8][1];
+      sa.x += va.x; sa.y += va.y; sa.z += va.z; sa.w += va.w; sb.x += vb.x; sb.y += vb.y; sb.z += vb.z; sb.w += vb.w;
+    }
+    float* dst = partial + (size_t)blockIdx.x * w8 * 8 + c8 * 8;
+    dst[0] = sa.x; dst[1] = sa.y; dst[2] = sa.z; dst[3] = sa.w; dst[4] = sb.x; dst[5] = sb.y; dst[6] = sb.z; dst[7] = sb.w;
+  }
+}
+
 // One warp per column: lanes stride the block partials, then a fixed xor tree.
 __global__ void colsum_reduce_kernel(const float* __restrict__ partial, uint32_t blocks, uint32_t width,
                                      uint32_t pstride, float* __restrict__ out, float scale) {
@@ -418,10 +471,19 @@ void colsum(catgnn_ctx ctx, const float* X, uint32_t ld, uint64_t rows, uint32_t
   const uint32_t blocks = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (rows + 255) / 256), 592);
   const uint32_t pstride = round_up(width, 4);
   float* part = ctx->scratch_buf<float>("colsum_part", (size_t)blocks * pstride);
-  if (Xh) colsum_partial_kernel<true><<<blocks, 256, 0, ctx->stream>>>(Xh, ld, rows, width, part, rs);
-  else colsum_partial_kernel<false><<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part, nullptr);
-  CG_CHECK_LAUNCH();
-  colsum_reduce_kernel<<<(width + 7) / 8, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out, scale);
+  if (Xh) {
+    if (ld % 8) throw ConfigError("fp16 column sum needs a row stride multiple of 8");
+    const uint32_t hb = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(1, (rows + 63) / 64), 1184);
+    const uint32_t hs = round_up(width, 8);
+    float* hpart = ctx->scratch_buf<float>("colsum_part_h", (size_t)hb * hs);
+    colsum_h16_kernel<<<hb, 256, 0, ctx->stream>>>(Xh, ld, rows, width, hpart, rs);
+    CG_CHECK_LAUNCH();
+    colsum_reduce_kernel<<<(width + 7) / 8, 256, 0, ctx->stream>>>(hpart, hb, width, hs, out, scale);
+  } else {
+    colsum_partial_kernel<false><<<blocks, 256, 0, ctx->stream>>>(X, ld, rows, width, part, nullptr);
+    CG_CHECK_LAUNCH();
+    colsum_reduce_kernel<<<(width + 7) / 8, 256, 0, ctx->stream>>>(part, blocks, width, pstride, out, scale);
+  }
   CG_CHECK_LAUNCH();
   ctx->launches += 2;
 }

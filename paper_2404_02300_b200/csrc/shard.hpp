@@ -114,6 +114,11 @@ struct AggArgs {
 // build_adjacency) + aggregation plan + degree scales.  pairs are device
 // local-id pairs in edge order.
 void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges);
+// home partition of every shard row (owner ids / parts: every partition's owned
+// ids and their partition, host arrays, n_owned entries): device radix sort of
+// the owner table + binary search of the shard's d_ext.  Returns the halo rows.
+uint64_t halo_map(catgnn_shard_s* s, const uint32_t* owner_ids, const uint32_t* owner_parts, uint64_t n_owned,
+                  uint64_t num_ids, uint32_t* home_host);
 // Device mapping of external-id edges to local rows by binary search over the
 // ascending node table (load_training_data's local[] map, train.cpp:258-271).
 void map_ext_edges(catgnn_ctx ctx, const uint64_t* d_ext_ids, uint64_t rows,

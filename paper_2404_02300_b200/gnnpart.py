@@ -213,6 +213,13 @@ class Shard:
         return cls(h, ctx)
 
     # -- accessors -------------------------------------------------------
+    def halo_map(self, artifact: "Artifact"):
+        """(home u32 per local row, halo row count), built on the shard's device."""
+        home = np.zeros(self.rows, np.uint32)
+        n = C.c_uint64()
+        check(lib.catgnn_shard_halo_map(self.handle, artifact.handle, _ptr(home), C.byref(n)))
+        return home, n.value
+
     @property
     def info(self) -> ShardInfo:
         inf = ShardInfo()

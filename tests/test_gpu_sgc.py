@@ -124,6 +124,20 @@ def test_load_training_data_matches_reference(gp, small_artifact):
         assert np.array_equal(mine.features().astype(np.float64), theirs.features)
 
 
+def test_device_halo_map_matches_artifact(gp, small_artifact):
+    """catgnn_shard_halo_map (device radix sort of the owner table + binary
+    search of the replica table) equals the artifact's home map
+    (completion.cpp:46-50); halo rows are the non-owned replicas."""
+    data = gp.load_training_data(small_artifact)
+    art = gp.Artifact(small_artifact)
+    for i, sh in enumerate(data.shards):
+        ext, own, _, home = art.replica_map(i)
+        dev_home, halo = sh.halo_map(art)
+        assert np.array_equal(dev_home, home)
+        assert halo == int((own == 0).sum())
+        assert np.all(home[own == 1] == i)
+
+
 def test_load_without_split_features(gp, small_ds):
     # has_features = false: rows gathered from the global matrix (train.cpp:277-283)
     art = make_artifact(small_ds, p=2, with_features=False, tag="nofeat")
