@@ -934,11 +934,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
       p.fix_hcount = p.fix_count + 1;
       p.guard_part = ctx->scratch_buf<float>("k2_guard_part", std::max<uint64_t>(1, s->n_chunks));
       p.guard_pre = ctx->scratch_buf<float>("k2_guard_pre", std::max<uint64_t>(1, s->rows) * 256);
-      static const float gk = [] {  // diagnostics: threshold in standard deviations (default 8)
-        const char* v = std::getenv("CATGNN_GUARD_SIGMA");
-        return v ? (float)std::atof(v) / 6.0f : 1.0f;
-      }();
-      p.guard_k = kGuardK * gk;
+      p.guard_k = kGuardK;
       CG_CUDA(cudaMemsetAsync(p.fix_count, 0, 2 * sizeof(unsigned int), ctx->stream));
     }
     AggFn fn = pick_kernel(w4, a.pre != nullptr, a.mask_bits || a.bits_out, a.in_h != nullptr,
@@ -966,8 +962,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
       CG_CHECK_LAUNCH();
       ctx->launches++;
     }
-    static const int nofix = env_int("CATGNN_GUARD_NOFIX", 0);  // diagnostics (wrong results)
-    if (guard && !nofix) {  // exact fp32 recomputation of the flagged elements
+    if (guard) {  // exact fp32 recomputation of the flagged elements
       int tf = ctx->begin_timed(3, ctx->timing ? std::string("(within K2 w256) guard exact fix") : std::string());
       agg_exact_fix_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
       CG_CHECK_LAUNCH();

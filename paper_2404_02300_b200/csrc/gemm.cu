@@ -302,13 +302,6 @@ __device__ __forceinline__ float4 tf32_residual4(float4 v) {
   return make_float4(tf32_residual(v.x), tf32_residual(v.y), tf32_residual(v.z), tf32_residual(v.w));
 }
 
-// B residual for b_lo_tma: lo = x - tf32(x) over the whole operand buffer
-// (same rounding as the converters).
-__global__ void residual_kernel(const float* __restrict__ x, float* __restrict__ lo, uint64_t n) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    lo[i] = tf32_residual(x[i]);
-}
-
 __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
   if (e.rowscale && col >= e.scale_col_begin) v *= __ldg(e.rowscale + row);
   if (e.bias) v += __ldg(e.bias + col);
@@ -897,14 +890,9 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     throw ConfigError("GEMM epilogue operands must be 16-byte aligned");
 
   const uint32_t b_stage = BNh * BK * 4;
-  // 3xTF32 with a small, heavily reused B (the weights of a forward / input-
-  // gradient GEMM): its residual is computed once here and TMA-loaded with each
-  // stage, so the converters split only A (less shared-memory traffic and power)
-  static const int blo_env = [] {
-    const char* v = std::getenv("CATGNN_GEMM_B_LO");
-    return v ? std::atoi(v) : 0;  // A/B knob: measured no faster on reddit (off)
-  }();
-  const bool blt = split3 && blo_env && (uint64_t)N * K <= (4ull << 20) && M >= 4096 && splits == 1;
+  // (a precomputed, TMA-loaded B residual — b_lo_tma — measured no faster on
+  // reddit and is not used by the host: the converters split both operands)
+  const bool blt = false;
   const size_t stage_bytes = (size_t)A_STAGE + (size_t)b_stage * (blt ? 2 : 1);
   const size_t lo_bytes = (size_t)A_STAGE + (blt ? 0 : (size_t)b_stage);  // one residual slot
   static const int lo_env = [] {
@@ -953,16 +941,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   args.a_mn = a.mn_major ? 1u : 0u;
   args.b_mn = b.mn_major ? 1u : 0u;
   args.bm = bm;
-  {
-    static const int ef_env = [] {
-      const char* v = std::getenv("CATGNN_GEMM_EVICT_FIRST");
-      return v ? std::atoi(v) : 0;  // measured slower on the reddit step (off by default)
-    }();
-    // an operand is streamed when its row extent (M for A, N for B) is row-sized
-    // or it is the long contraction side of a split-K weight gradient
-    args.a_stream = ef_env && (M > 4096 || K > 4096) ? 1u : 0u;
-    args.b_stream = ef_env && (N > 4096 || K > 4096) ? 1u : 0u;
-  }
+  args.a_stream = args.b_stream = 0u;  // evict-first operand loads measured slower on the reddit step
   // instruction descriptor: D f32, A/B tf32, A/B major (bit 15/16), N>>3, M>>4
   args.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (args.a_mn << 15) | (args.b_mn << 16) | ((BN >> 3) << 17) |
                ((bm >> 4) << 24);
@@ -976,19 +955,8 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
     args.epi.partial = nullptr;
   }
   CUtensorMap ta = a.mn_major ? make_map_mn(A, M, K, lda) : make_map(A, M, K, lda, BM);
-  const float* Blo = B;
-  if (blt) {  // the residual of B's whole extent ([N][ldb] K-major, [K][ldb] MN-major)
-    const uint64_t rows_b = b.mn_major ? K : N, cols_b = b.mn_major ? N : K;
-    const uint64_t count = (rows_b - 1) * ldb + cols_b;
-    float* lo = ctx->scratch_buf<float>("gemm_b_lo", count);
-    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, 148 * 8));
-    residual_kernel<<<g, 256, 0, ctx->stream>>>(B, lo, count);
-    CG_CHECK_LAUNCH();
-    ctx->launches++;
-    Blo = lo;
-  }
   CUtensorMap tb = b.mn_major ? make_map_mn(B, N, K, ldb) : make_map(B, N, K, ldb, BNh);
-  CUtensorMap tbl = blt ? (b.mn_major ? make_map_mn(Blo, N, K, ldb) : make_map(Blo, N, K, ldb, BNh)) : tb;
+  const CUtensorMap& tbl = tb;
   // cudaFuncSetAttribute is per device: one flag set per device ordinal
   static std::mutex attr_mu;
   static std::map<int, std::array<bool, 4>> attr_set;

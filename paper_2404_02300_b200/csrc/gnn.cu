@@ -363,21 +363,12 @@ float* act(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld, 
 
 // Row stride of a layer activation.  Narrow rows are padded to 16 floats
 // (64 B) so every gathered row starts on a sector pair and the 44-wide class
-// rows of the reddit shape become 48 (agg_kernel<2,8>).  CATGNN_PAD=4 gives
-// round-to-4 rows, CATGNN_PAD=32 128-byte rows (A/B knobs).
-const uint32_t kPadNarrow = [] {
-  const char* v = std::getenv("CATGNN_PAD");
-  if (const char* o = std::getenv("CATGNN_PAD16")) if (o[0] == '0') return 4u;
-  return v ? (uint32_t)std::atoi(v) : 16u;
-}();
+// rows of the reddit shape become 48 (agg_kernel<2,8>).
+constexpr uint32_t kPadNarrow = 16;
 uint32_t act_width(uint32_t d) { return d < 128 ? round_up(d, kPadNarrow) : round_up(d, 4); }
 const bool kSageInPlace = [] {  // A/B knob (CATGNN_SAGE_INPLACE=0: copy h into [h | mean])
   const char* v = std::getenv("CATGNN_SAGE_INPLACE");
   return v ? v[0] != '0' : true;
-}();
-const bool kNarrowLd64 = [] {  // A/B knob; measured no faster on reddit (off)
-  const char* v = std::getenv("CATGNN_NARROW_LD64");
-  return v ? v[0] != '0' : false;
 }();
 
 void plan_layers(catgnn_model_s* M) {
@@ -390,11 +381,7 @@ void plan_layers(catgnn_model_s* M) {
     L.d_out = l + 1 == c.layers ? c.classes : c.hidden;
     L.K_in = l == 0 ? round_up(L.d_in, 4) : act_width(L.d_in);  // layer 0 reads the shard's x
     L.D_out = act_width(L.d_out);
-    // CATGNN_NARROW_LD64=1: narrow GCN/GIN activations (33-64 floats, e.g. the
-    // 41 classes padded to 48) stored 64 floats apart, so every gathered row
-    // starts on a 128-byte line (two L1 wavefronts per 48-float row instead of
-    // 2.5); measured no faster, the 48-wide pass is not wavefront-bound
-    L.ld_act = (kNarrowLd64 && c.kind != CATGNN_MODEL_SAGE && L.D_out > 32 && L.D_out <= 64) ? 64 : L.D_out;
+    L.ld_act = L.D_out;  // (64-float strides for 33-64-wide rows measured no faster: not wavefront bound)
     if (c.kind == CATGNN_MODEL_SAGE) {
       L.agg_first = L.d_in <= L.d_out;
       if (L.agg_first) {
