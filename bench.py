@@ -324,6 +324,28 @@ def run_reference(args, w, prep):
     print(json.dumps(line), flush=True)
 
 
+def gemm_precision(w):
+    """K3 operand precision per layer kind (gnn.cu bf_layer): transform-first
+    GCN / GIN layers run bf16x3 kind::f16 MMAs, the others 3xTF32 kind::tf32."""
+    kinds = []
+    for l in range(w.layers):
+        d_in = w.dim if l == 0 else w.hidden
+        d_out = w.classes if l + 1 == w.layers else w.hidden
+        agg_first = d_in <= d_out if w.model == "sage" else d_in < d_out
+        kinds.append("bf16x3 (tcgen05 kind::f16)" if w.model != "sage" and not agg_first
+                     else "3xTF32 (tcgen05 kind::tf32)")
+    return kinds
+
+
+def dtype_label(w):
+    eb = w.pass_elem_bytes()
+    agg = ("fp32 accumulation; gathered inputs " +
+           ("fp32" if all(e == 4 for e in eb) else
+            "fp16 on the passes " + ", ".join(str(x) for x, e in zip(w.passes(), eb) if e == 2) +
+            " (guarded forward / scaled gradients), fp32 otherwise"))
+    return f"f32 ({'/'.join(sorted(set(gemm_precision(w))))} tensor-core GEMMs; aggregation: {agg})"
+
+
 def workload_config(w, prep, args):
     m = prep["meta"]
     return {"workload": w.name, "gnn": f"{w.layers}-layer {w.model.upper()} hidden {w.hidden}",
@@ -332,8 +354,9 @@ def workload_config(w, prep, args):
             "partitioner": f"reference SPRING beta={w.beta} tau_vol={m['tau_vol']} + 1-hop completion",
             "replication_factor": m["rf"], "part_nnz": m["part_nnz"], "sum_over_max_edges": m["sum_over_max"],
             "aggregation_widths": w.passes(),
-            "aggregation_row_stride_floats": [act_width(x) for x in w.passes()], "sync_interval": args.sync,
-            "optimizer": "adam lr 0.01", "gemm_precision": "3xTF32 (tcgen05 kind::tf32)",
+            "aggregation_row_stride_floats": [act_width(x) for x in w.passes()],
+            "aggregation_input_bytes_per_element": w.pass_elem_bytes(), "sync_interval": args.sync,
+            "optimizer": "adam lr 0.01", "gemm_precision": gemm_precision(w),
             "step": "one full-batch local iteration per partition + averaging",
             "partitions_per_gpu": w.partitions // max(1, dist_env()[0]),
             "l2": "inputs larger than L2 (per-partition features 0.5 GB, activations > 126 MB)"}
@@ -683,10 +706,11 @@ def main():
             k = 2 * d_in if w.model == "sage" else d_in
             gemm_flops += 2 * rows_i * k * d_out * (3 if l > 0 else 2)
             d_in = d_out
-    gemm = {"kernel": "catgnn::gemm_tf32_kernel (K3 tcgen05 kind::tf32, 3xTF32)",
+    gemm = {"kernel": "catgnn::gemm_tf32_kernel (K3 tcgen05; " + ", ".join(sorted(set(gemm_precision(w)))) + ")",
             "ms_per_step": kt["gemm_ms"] / timed_steps,
             "achieved_tflops": gemm_flops / (kt["gemm_ms"] / timed_steps / 1e3) / 1e12 if kt["gemm_ms"] else None,
-            "peak_tflops_tf32": bf16 / 2, "peak_note": "dense TF32 = half the measured bf16 figure"}
+            "achieved_is": "useful flops (2MNK); the split-precision schemes issue 3 MMAs per product",
+            "peak_tflops_bf16": bf16, "peak_note": "measured dense bf16 (MEASURED_PEAKS.json); kind::tf32 runs at half"}
 
     # end-to-end through the C ABI: global features re-uploaded from pinned host memory each step, loss read back
     e2e = None
@@ -743,7 +767,7 @@ def main():
             cfg["shared_devices"] = bool(shared_devices)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 aggregation)",
+                "vs_baseline": None, "dtype": dtype_label(w),
                 "data": "synthetic (RMAT + reference SPRING partitions, random-init weights)",
                 "config": cfg, "roofline": roofline, "gemm": gemm,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "step_breakdown": breakdown,

@@ -67,13 +67,16 @@ def main():
     assert n == meta["num_ids"], (n, meta["num_ids"])
     t1 = time.time()
     labels, roles = synth.node_meta(n, classes, 0.01, 0.001, 0.002, seed=seed)
-    stream = torch.cuda.Stream()
-    ctx = gp.Context(0, stream.cuda_stream)  # the library launches on this stream: CUDA events time it
     torch.cuda.synchronize()
     tc = time.time()
-    parts = gp.complete_edges(e, home, roles, P, ctx=ctx)
+    cctx = gp.Context(0)  # completion scratch (the stream, per-partition sorts) freed with its context
+    parts = gp.complete_edges(e, home, roles, P, ctx=cctx)
+    cctx.synchronize()
+    cctx.close()
     t2 = time.time()
     del e
+    stream = torch.cuda.Stream()
+    ctx = gp.Context(0, stream.cuda_stream)  # the library launches on this stream: CUDA events time it
     rows = [int(p.ext.size) for p in parts]
     pedges = [int(p.edges.shape[0]) for p in parts]
     res["prep_box"] = dict(rmat_s=t1 - t0, device_completion_s=t2 - tc, active_ids=int((home != 0xFFFFFFFF).sum()),

@@ -18,7 +18,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-SCALE, EDGES, P, SEED, BETA = 27, 1_600_000_000, 16, 4, 1.05
+SCALE = int(os.environ.get("PAPERS_SCALE", 27))
+EDGES, P, SEED, BETA = 1_600_000_000, 16, 4, 1.05
 
 
 def main():
