@@ -164,6 +164,9 @@ __device__ __forceinline__ float4 shfl_xor4(const float4& v, int m) {
 __device__ __forceinline__ int ld_col(const AggKernelArgs& p, int64_t e) {
   return p.stream_hint ? __ldcs(p.col + e) : __ldg(p.col + e);
 }
+__device__ __forceinline__ int ld_col(const AggKernelArgs& p, const int* __restrict__ base, int e) {
+  return p.stream_hint ? __ldcs(base + e) : __ldg(base + e);
+}
 
 __device__ __forceinline__ float post_scale(int norm, float deg) {
   switch (norm) {
@@ -390,14 +393,18 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   static_assert(B <= 32, "batch must fit one index chunk");
   const int g = lane / LPN, li = lane % LPN;
   const bool writer = lane < LPN;
-  const int64_t E0 = __ldg(p.row_ptr + r0), E1 = __ldg(p.row_ptr + r1);
-  int64_t cb = E0;  // first edge of the current chunk
-  int cur = (cb + lane < E1) ? ld_col(p, cb + lane) : 0;
-  int nxt = (cb + 32 + lane < E1) ? ld_col(p, cb + 32 + lane) : 0;
+  // edge offsets are 32-bit, relative to the unit's first edge (a light unit
+  // holds < 2^31 edges); only the unit base is 64-bit
+  const int64_t E0 = __ldg(p.row_ptr + r0);
+  const int NE = (int)(__ldg(p.row_ptr + r1) - E0);
+  const int* __restrict__ colu = p.col + E0;
+  int cb = 0;  // first edge of the current chunk
+  int cur = (lane < NE) ? ld_col(p, colu, lane) : 0;
+  int nxt = (32 + lane < NE) ? ld_col(p, colu, 32 + lane) : 0;
   float curs = 1.f, nxts = 1.f;
   if (SC) {
-    curs = (cb + lane < E1) ? __ldg(sarr + cur) : 0.f;
-    nxts = (cb + 32 + lane < E1) ? __ldg(sarr + nxt) : 0.f;
+    curs = (lane < NE) ? __ldg(sarr + cur) : 0.f;
+    nxts = (32 + lane < NE) ? __ldg(sarr + nxt) : 0.f;
   }
   const char* base = lane_base<CPV>(p, li);
   const uint32_t ldb = row_bytes<CPV>(p);
@@ -407,12 +414,12 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
   for (int q = 0; q < VPL; ++q) colok[q] = FULLW || li + LPN * q < (int)n_vec<CPV>(p);
   for (int64_t rb = r0; rb < r1; rb += 32) {
     const int64_t rr = rb + lane;
-    const int64_t rpa = rr < r1 ? __ldg(p.row_ptr + rr) : 0;
-    const int64_t rpb = rr < r1 ? __ldg(p.row_ptr + rr + 1) : 0;
+    const int rpa = rr < r1 ? (int)(__ldg(p.row_ptr + rr) - E0) : 0;
+    const int rpb = rr < r1 ? (int)(__ldg(p.row_ptr + rr + 1) - E0) : 0;
     const int nr = (int)((r1 - rb) < 32 ? (r1 - rb) : 32);
     for (int i = 0; i < nr; ++i) {
       const int64_t r = rb + i;
-      const int64_t e0 = __shfl_sync(0xffffffffu, rpa, i), e1 = __shfl_sync(0xffffffffu, rpb, i);
+      const int e0 = __shfl_sync(0xffffffffu, rpa, i), e1 = __shfl_sync(0xffffffffu, rpb, i);
 #ifdef AGG_SKIP_SHORT  // diagnostics build: the cost of short rows (wrong results)
       if (e1 - e0 < AGG_SKIP_SHORT) continue;
 #endif
@@ -426,13 +433,13 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
 #pragma unroll
       for (int k = 0; k < VPL * CPV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       float ss = 0.f;  // GUARD: sum of the gathered rows' squared maxima (same on every lane)
-      for (int64_t e = e0; e < e1; e += B) {
+      for (int e = e0; e < e1; e += B) {
         while (e >= cb + 32) {  // warp-uniform: advance the index window by one chunk
           cb += 32;
           cur = nxt;
           curs = nxts;
-          const bool ok = cb + 32 + lane < E1;
-          nxt = ok ? ld_col(p, cb + 32 + lane) : 0;
+          const bool ok = cb + 32 + lane < NE;
+          nxt = ok ? ld_col(p, colu, cb + 32 + lane) : 0;
           if (SC) nxts = ok ? __ldg(sarr + nxt) : 0.f;
         }
         uint4 v[UNROLL][VPL];
@@ -441,7 +448,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
         if constexpr (G == 1) {
           // whole-warp rows: realign the window to this batch once (lane l <-
           // edge e + l), then each neighbour is one shuffle of a constant lane
-          const int off = (int)(e - cb) + lane;  // < 64
+          const int off = e - cb + lane;  // < 64
           const int wa = __shfl_sync(0xffffffffu, cur, off & 31);
           const int wb = __shfl_sync(0xffffffffu, nxt, off & 31);
           const int win = off < 32 ? wa : wb;
@@ -451,7 +458,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
             wins = off < 32 ? sa : sb;
           }
-          const int rem = (int)((e1 - e) < B ? (e1 - e) : B);  // valid neighbours of the batch
+          const int rem = min(e1 - e, B);  // valid neighbours of the batch
 #pragma unroll
           for (int uu = 0; uu < UNROLL; ++uu) {
             const int j = __shfl_sync(0xffffffffu, win, uu);
@@ -467,24 +474,26 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             }
           }
         } else {
-          // lane groups: two shuffles per neighbour keep the register budget
-          // of the 4-CTA/SM narrow kernels; 32-bit offsets from the window
-          const int boff = (int)(e - cb) + g;  // < 32
-          const int lim = (int)(e1 - cb);      // the row's end, relative to the window
+          // lane groups: the window is realigned once per batch (lane l <-
+          // edge e + l), then group g's neighbour of slot uu is one shuffle
+          // of lane uu*G + g
+          const int off = e - cb + lane;  // < 64
+          const int wa = __shfl_sync(0xffffffffu, cur, off & 31);
+          const int wb = __shfl_sync(0xffffffffu, nxt, off & 31);
+          const int win = off < 32 ? wa : wb;
+          float wins = 1.f;
+          if (PRE) {
+            const float sa = __shfl_sync(0xffffffffu, curs, off & 31);
+            const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
+            wins = off < 32 ? sa : sb;
+          }
+          const int rem = min(e1 - e, B);  // valid neighbours of the batch
 #pragma unroll
           for (int uu = 0; uu < UNROLL; ++uu) {
-            const int off = boff + uu * G;  // < 32 + B <= 64
-            const int ja = __shfl_sync(0xffffffffu, cur, off & 31);
-            const int jb = __shfl_sync(0xffffffffu, nxt, off & 31);
-            const int j = off < 32 ? ja : jb;
-            if (PRE) {
-              const float sa = __shfl_sync(0xffffffffu, curs, off & 31);
-              const float sb = __shfl_sync(0xffffffffu, nxts, off & 31);
-              s[uu] = off < 32 ? sa : sb;
-            } else {
-              s[uu] = 1.f;
-            }
-            ok[uu] = off < lim;
+            const int k = uu * G + g;
+            const int j = __shfl_sync(0xffffffffu, win, k);
+            s[uu] = PRE ? __shfl_sync(0xffffffffu, wins, k) : 1.f;
+            ok[uu] = k < rem;
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
               if constexpr (ZR)  // idle slots and lanes past the row width load the zero row
