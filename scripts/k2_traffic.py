@@ -66,7 +66,7 @@ def main():
     self_term = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
     passes, cur = [], None
     for d in seq:
-        if "agg_fixup" in d["kernel"] and cur is not None:
+        if ("agg_fixup" in d["kernel"] or "exact_fix" in d["kernel"]) and cur is not None:
             cur["time_us"] += d["gpu__time_duration.sum"]
             cur["dram_bytes"] += d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
             cur["l2_bytes"] += d["lts__t_bytes.sum"]
@@ -98,7 +98,7 @@ def main():
     res = {"workload": workload, "workload_key": w.key(),
            "source": "ncu --metrics " + ",".join(METRICS) + " --clock-control none -k regex:agg_ "
                      "(scripts/k2_traffic.py): every K2 launch of one eager bench step (all partitions, all "
-                     "passes; split-row fix-ups folded into their pass)",
+                     "passes; split-row fix-ups and the guard's exact-fix kernels folded into their pass)",
            "passes_per_step": len(passes), "per_step": tot,
            "dram_bytes_per_launch": tot["dram_bytes"] / len(passes),
            "traffic_over_compulsory": tot["dram_bytes"] / tot["compulsory_bytes"],
