@@ -373,7 +373,7 @@ def main():
     ap.add_argument("--ref-edges", type=int, default=300_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--lanes", type=int, default=int(os.environ.get("CATGNN_LANES", "1")),
+    ap.add_argument("--lanes", type=int, default=int(os.environ.get("CATGNN_LANES", "2")),
                     help="shard lanes: partitions of a rank trained on this many concurrent streams")
     ap.add_argument("--agg-sms", type=int, default=int(os.environ.get("CATGNN_LANE_AGG_SMS", "0")),
                     help="with lanes > 1: SMs a K2 grid covers (0 = all)")
@@ -513,16 +513,20 @@ def main():
 
     state = {"it": 0}
 
-    def step(e2e=False, t=0, n=1):
+    def step(e2e=False, t=0, n=1, serial=False):
         losses = []
         for c in ctxs[1:]:  # fork the lanes off the main stream (graph capture needs it)
             c.wait_for(ctx)
+        prev = ctx
         if e2e:
             if t == 0:
                 refresh_features(stores[0])
             if t + 1 < n:  # prefetch the next step's inputs on the copy stream
                 refresh_features(stores[(t + 1) % 2])
-        for r, s in zip(reps, shards):
+        for k, (r, s) in enumerate(zip(reps, shards)):
+            if serial:  # lanes in turn: per-kernel event times without overlap
+                ctxs[k % lanes].wait_for(prev)
+                prev = ctxs[k % lanes]
             if e2e:
                 s.gather_features(stores[t % 2])
             r.train_step(s, want_loss=False)
@@ -659,13 +663,26 @@ def main():
             launches0 = launch_count()
     with ClockSampler(local) as clk:
         total_ms = timed(args.steps, graph=graph)
+    launches_eager = launch_count() - launches0
+    if lanes > 1:
+        # concurrent lanes overlap kernels, so their event times would add up
+        # to more than the step: the per-kernel breakdown and the roofline come
+        # from one averaging period run with the lanes in turn (eager)
+        timing(False)
+        timing(True)
+        for _ in range(args.sync):
+            step(serial=True)
+        torch.cuda.synchronize()
+        graph_for_records = None
+    else:
+        graph_for_records = graph
     # per-kernel CUDA events: every launch of the timed region (eager), or the
     # graph's event nodes as recorded by its last replay (one averaging period)
     # (with lanes > 1 kernels of different lanes overlap: their event times add up
     # to more than the step and each includes the time it shared the GPU)
     kts = [c.kernel_time() for c in ctxs]
     kt = {k: sum(x[k] for x in kts) for k in kts[0]}
-    timed_steps = args.sync if graph is not None else args.steps
+    timed_steps = args.sync if (graph_for_records is not None or lanes > 1) else args.steps
     recs = {}
     for c in ctxs:
         for k, v in c.kernel_records().items():
@@ -674,7 +691,7 @@ def main():
     breakdown = {k: {"ms_per_step": round(v[0] / timed_steps, 4), "launches_per_step": v[1] / timed_steps}
                  for k, v in sorted(recs.items(), key=lambda kv: -kv[1][0])}
     timing(False)
-    launches = launches_per_replay * (args.steps // args.sync) if graph is not None else launch_count() - launches0
+    launches = launches_per_replay * (args.steps // args.sync) if graph is not None else launches_eager
     ms_step = total_ms / args.steps
 
     widths = w.passes()  # logical widths: algorithmic bytes exclude the row padding
@@ -771,6 +788,9 @@ def main():
                 "data": "synthetic (RMAT + reference SPRING partitions, random-init weights)",
                 "config": cfg, "roofline": roofline, "gemm": gemm,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "step_breakdown": breakdown,
+                "lanes": lanes, "kernel_times_from": ("one averaging period with the lanes in turn (per-kernel CUDA "
+                                                      "events without lane overlap)" if lanes > 1 else
+                                                      "the timed region's CUDA events"),
                 "global_nnz_edges_per_s": meta["nnz"] * len(widths) * args.steps / (total_ms / 1e3),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
