@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <initializer_list>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -126,6 +127,17 @@ struct catgnn_ctx_s {
     auto& b = scratch[name];
     b.reserve(count * sizeof(T));
     return reinterpret_cast<T*>(b.p);
+  }
+  // Free the named scratch buffers whose names start with one of `prefixes`
+  // (after the stream drained): one-time temporaries — K1's sort buffers, the
+  // edge-mapping staging — do not stay resident next to the activations.
+  void release_scratch(std::initializer_list<const char*> prefixes) {
+    cudaStreamSynchronize(stream);
+    for (auto it = scratch.begin(); it != scratch.end();) {
+      bool hit = false;
+      for (const char* p : prefixes) hit = hit || it->first.rfind(p, 0) == 0;
+      it = hit ? scratch.erase(it) : std::next(it);
+    }
   }
   cudaEvent_t take_event();
   // SMs the persistent K2 grid covers and CTAs (SMs) the persistent K3 grid

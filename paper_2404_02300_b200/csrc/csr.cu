@@ -322,6 +322,8 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
     ctx->launches++;
   }
   build_plan(s);
+  // K1's temporaries (expanded entries, radix buffers, plan scans: ~70 B per nnz)
+  ctx->release_scratch({"k1_", "radix_", "pairs", "edges_ext", "ext_ids"});
 }
 
 void map_ext_edges(catgnn_ctx ctx, const uint64_t* d_ext_ids, uint64_t rows,

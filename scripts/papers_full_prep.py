@@ -19,7 +19,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 SCALE = int(os.environ.get("PAPERS_SCALE", 27))
-EDGES, P, SEED, BETA = 1_600_000_000, 16, 4, 1.05
+EDGES, SEED, BETA = 1_600_000_000, 4, 1.05
+P = int(os.environ.get("PAPERS_P", 16))
 
 
 def main():
