@@ -311,6 +311,12 @@ __device__ __forceinline__ float apply_epi(const GemmEpi& e, uint32_t row, uint3
 }
 __device__ __forceinline__ void store_epi(const GemmEpi& e, uint32_t row, uint32_t col, float v) {
   if (e.out_h) e.out_h[(size_t)row * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col] = __float2half_rn(v);
+  if (e.out_bhi) {
+    const size_t o = (size_t)row * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col;
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    e.out_bhi[o] = h;
+    e.out_blo[o] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
   if (e.out) e.out[(size_t)row * e.ld_out + e.out_col + col] = v;
 }
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
@@ -631,7 +637,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
         // written (a multiple of 4 columns)
         const uint32_t ns = max(args.N, e.store_cols);
         const uint32_t nc = min(32u, ns - col0);
-        if (!e.partial && (nc == 32 || (e.store_cols && nc % (e.out_h ? 8 : 4) == 0))) {
+        if (!e.partial && (nc == 32 || (e.store_cols && nc % ((e.out_h || e.out_bhi) ? 8 : 4) == 0))) {
           const uint32_t mw = mrow ? mw_cur : 0xffffffffu;
           uint32_t bw = 0;
 #pragma unroll
@@ -678,6 +684,27 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
                                  pack_h2((b.x - h2.x) * 2048.f, (b.y - h2.y) * 2048.f),
                                  pack_h2((b.z - h3.x) * 2048.f, (b.w - h3.y) * 2048.f));
                 }
+              }
+            }
+          }
+          if (e.out_bhi) {  // bf16x3 pair rows: nc/8 16-byte vectors per row and half
+            const uint32_t n8 = nc / 8;
+            for (uint32_t f = lane; f < 32 * n8; f += 32) {
+              const uint32_t rr = f / n8, cc = f % n8, grow = rbase + rr;
+              if (grow < args.M) {
+                const float4 a = T[rr * kTileLd4 + 2 * cc], b = T[rr * kTileLd4 + 2 * cc + 1];
+                const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                uint32_t hw[4], lw[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+                  const __nv_bfloat162 l = __floats2bfloat162_rn(v[2 * k] - __low2float(h), v[2 * k + 1] - __high2float(h));
+                  hw[k] = *reinterpret_cast<const uint32_t*>(&h);
+                  lw[k] = *reinterpret_cast<const uint32_t*>(&l);
+                }
+                const size_t o = (size_t)grow * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col0;
+                reinterpret_cast<uint4*>(e.out_bhi + o)[cc] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                reinterpret_cast<uint4*>(e.out_blo + o)[cc] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
               }
             }
           }
@@ -819,7 +846,9 @@ uint32_t pow2_cols(uint32_t n) {
 }  // namespace
 
 void check_epi_output(const GemmEpi& epi) {
-  if (!epi.out && !epi.out_h) throw ConfigError("GEMM needs an output");
+  if (!epi.out && !epi.out_h && !epi.out_bhi) throw ConfigError("GEMM needs an output");
+  if (epi.out_bhi && (!epi.out_blo || !epi.store_cols || epi.store_cols % 8 || ((epi.ld_h ? epi.ld_h : epi.ld_out) % 8)))
+    throw ConfigError("GEMM bf16 pair output: hi and lo, store_cols and row stride multiples of 8");
   if (epi.out && epi.out_h && !epi.store_cols) throw ConfigError("GEMM fp32 + fp16 outputs need store_cols");
   if (epi.rowmax && !epi.store_cols) throw ConfigError("GEMM row max needs store_cols (staged epilogue)");
   if (epi.out_hl && (!epi.out_h || !epi.store_cols)) throw ConfigError("GEMM fp16 residual needs out_h and store_cols");

@@ -35,6 +35,10 @@ struct GemmEpi {
   __half* out_h = nullptr;
   uint32_t ld_h = 0;  // out_h row stride in halves when both outputs are set (0: ld_out)
   __half* out_hl = nullptr;  // with out_h: fp16 (v - fp16(v)) * 2^11, same layout (hi + lo * 2^-11 ~ v to 2^-22)
+  // bf16x3 pair output (hi = bf16(v), lo = bf16(v - hi); row stride ld_h or
+  // ld_out): the next bf16x3 GEMM's pre-split operand, written directly
+  __nv_bfloat16* out_bhi = nullptr;
+  __nv_bfloat16* out_blo = nullptr;
   float out_scale = 1.0f;
   // per output row: max |v| over its columns, merged with atomicMax on the
   // float bits (caller zero-fills; order-independent, so deterministic)

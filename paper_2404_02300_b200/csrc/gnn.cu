@@ -528,13 +528,15 @@ bool bf_layer(const catgnn_model_s* M, size_t l) {
          (k == CATGNN_MODEL_GCN || k == CATGNN_MODEL_GIN || k == CATGNN_MODEL_SGC);
 }
 
-// Named bf16x3 activation pair, zero-filled whenever its shape changes.
+// Named bf16x3 activation pair, zero-filled whenever its shape changes; hi and
+// lo are one allocation (lo follows hi), so a dead pair can host a rows x ld
+// fp32 array (backward lean).
 Split act16(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint32_t ld) {
   Split s;
   s.ld = ld;
   const size_t n = std::max<uint64_t>(1, rows) * ld;
-  s.hi = ctx->scratch_buf<uint16_t>(name + "_hi", n);
-  s.lo = ctx->scratch_buf<uint16_t>(name + "_lo", n);
+  s.hi = ctx->scratch_buf<uint16_t>(name + "_hl", 2 * n);
+  s.lo = s.hi + n;
   auto sig = std::make_pair(rows, ld);
   auto it = ctx->act_shape.find(name + "_s");
   if (it == ctx->act_shape.end() || it->second != sig) {
@@ -654,9 +656,11 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
     Bufs& b = B[l];
     b.in = in;
     b.in_ld = in_ld;
-    // transform-first K2 output consumed only by the next (bf16x3) layer's
-    // GEMMs: written as a bf16x3 pair, no fp32 copy
-    const bool h_split = !L.agg_first && !last && bf_layer(M, l + 1);
+    // output consumed only by the next (bf16x3) layer's GEMMs: written as a
+    // bf16x3 pair, no fp32 copy (by K2 for a transform-first layer, by the
+    // GEMM epilogue for an aggregate-first GCN / GIN layer)
+    const bool h_split = !last && bf_layer(M, l + 1) && !L.out_in_next_mid &&
+                         (!L.agg_first || M->cfg.kind != CATGNN_MODEL_SAGE);
     if (L.out_in_next_mid) {  // the next layer's [h | mean], left half
       b.out_ld = 2 * M->layers[l + 1].K_in;
       b.out = act(ctx, nm("mid", l + 1), rows, b.out_ld, fresh);
@@ -706,6 +710,15 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
       GemmEpi e; e.out = b.out; e.ld_out = b.out_ld; e.bias = bias; e.relu = !last;
       e.bits_out = b.bits; e.bits_words = b.bits_words;
       if (!L.out_in_next_mid) e.store_cols = b.out_ld;  // zero padding (bias is zero-padded)
+      if (h_split) {  // H_l straight into the next bf16x3 layer's operand pair
+        b.split = act16(ctx, nm("Hs", l), rows, round_up(L.D_out, 8));
+        e.out = nullptr;
+        e.out_bhi = reinterpret_cast<__nv_bfloat16*>(b.split.hi);
+        e.out_blo = reinterpret_cast<__nv_bfloat16*>(b.split.lo);
+        e.ld_out = b.split.ld;
+        e.store_cols = b.split.ld;
+        M->h_split_only[l] = true;
+      }
       gemm_tn(ctx, b.mid, b.mid_ld, M->params.p + L.off_w, L.w_cols, (uint32_t)rows, L.d_out, L.K_in, e, 1, kFwdPrecision);
     } else {  // GCN / GIN / SGC transform-first
       const bool h16 = f16_fwd(M, l);
@@ -777,7 +790,13 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
 }
 
 // Loss + backward; fills M->grads.  Returns the loss when want_loss.
-double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B, bool want_loss) {
+// lean (train steps): a hidden layer's output kept only as a bf16x3 pair is
+// dead once the next layer's weight gradient has read it, so that layer's
+// fp32 dZ (written by the next layer's dX GEMM) takes its place — one rows x
+// width activation less (a papers-scale GIN partition of 31 M rows then fits
+// one B200); forward_backward keeps every activation for export.
+double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B, bool want_loss,
+                bool lean = false) {
   catgnn_ctx ctx = M->ctx;
   cudaStream_t st = ctx->stream;
   const uint64_t rows = S->rows;
@@ -786,7 +805,15 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   const size_t nl = M->layers.size();
   // K4: dZ of the last layer
   const Layer& LL = M->layers[nl - 1];
-  float* dZ = act(ctx, nm("dZ", nl - 1), rows, LL.ld_act, false);
+  // A transform-first GCN / GIN / SGC last layer's fp32 T (its K2 input) is dead
+  // once the logits exist: K4 writes dZ over it (one rows x ld activation less —
+  // 22 GB on a 31 M-row papers-scale partition)
+  const bool reuse_t = !LL.agg_first && M->cfg.kind != CATGNN_MODEL_SAGE && B[nl - 1].mid &&
+                       B[nl - 1].mid_ld == LL.ld_act;
+  float* dZ = reuse_t ? B[nl - 1].mid : act(ctx, nm("dZ", nl - 1), rows, LL.ld_act, false);
+  M->dz_last = dZ;
+  M->dz_ptr.assign(nl, nullptr);
+  M->dz_ptr[nl - 1] = dZ;
   CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   const uint64_t ntr = S->h_train.size();
   // fp16 gradient rows carry 2^k <= n_train (|dZ| <= 1 / n_train)
@@ -841,7 +868,12 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
     // layer li-1's backward K2 gathers dZ_{li-1} as fp16 when it is an fp16
     // layer and this layer's dX GEMM produces it (bf16x3 transform-first)
     const bool prev_h = need_dx && f16_bwd(M, li - 1) && bf_layer(M, li);
-    float* dZprev = need_dx && !prev_h ? act(ctx, nm("dZ", li - 1), rows, L.K_in, false) : nullptr;
+    const bool onto_h = lean && need_dx && !prev_h && bf_layer(M, li) && M->h_split_only[li - 1] &&
+                        B[li - 1].split && B[li - 1].split.ld == L.K_in;
+    float* dZprev = need_dx && !prev_h
+                        ? (onto_h ? reinterpret_cast<float*>(B[li - 1].split.hi) : act(ctx, nm("dZ", li - 1), rows, L.K_in, false))
+                        : nullptr;
+    if (need_dx) M->dz_ptr[li - 1] = dZprev;
     __half* dzh_prev = prev_h ? act_h(ctx, nm("dZh", li - 1), rows, ld_h16(L.K_in)) : nullptr;
     if (sage && L.agg_first) {
       // dW = dZ^T cat (both operands read MN-major in place)
@@ -984,7 +1016,7 @@ __global__ void loss_accum_kernel(const double* __restrict__ loss_sum, double we
 void model_train_step(catgnn_model m, catgnn_shard s) {
   check_pair(m, s);
   auto B = forward(m, s);
-  backward(m, s, B, false);
+  backward(m, s, B, false, true);
   optimizer_step(m);
   m->last_shard = s;
 }
@@ -1171,7 +1203,7 @@ int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss) {
   return guarded([&] {
     check_pair(m, s);
     auto B = forward(m, s);
-    double l = backward(m, s, B, loss != nullptr);
+    double l = backward(m, s, B, loss != nullptr, true);
     optimizer_step(m);
     if (loss) *loss = l;
     m->last_shard = s;
@@ -1254,8 +1286,8 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
     if (what == 0 && layer < m->h_split_only.size() && m->h_split_only[layer]) {
       // H_l kept only as the bf16x3 pair: export hi + lo
       const uint32_t sld = round_up(L.D_out, 8);
-      const uint16_t* hi = m->ctx->scratch_buf<uint16_t>(nm("Hs", layer) + "_hi", 1);
-      const uint16_t* lo = m->ctx->scratch_buf<uint16_t>(nm("Hs", layer) + "_lo", 1);
+      const uint16_t* hi = m->ctx->scratch_buf<uint16_t>(nm("Hs", layer) + "_hl", 1);
+      const uint16_t* lo = hi + std::max<uint64_t>(1, s->rows) * sld;  // act16: lo follows hi
       if (width) *width = w;
       if (out && s->rows) {
         std::vector<uint16_t> h(s->rows * (size_t)sld), lw(s->rows * (size_t)sld);
@@ -1292,7 +1324,11 @@ int catgnn_model_export(catgnn_model m, uint32_t layer, int what, float* out, ui
       }
       return;
     }
-    else if (what == 2) { src = m->ctx->scratch_buf<float>(nm("dZ", layer), 1); ld = L.ld_act; }
+    else if (what == 2) {
+      src = (layer < m->dz_ptr.size() && m->dz_ptr[layer]) ? m->dz_ptr[layer]
+                                                           : m->ctx->scratch_buf<float>(nm("dZ", layer), 1);
+      ld = L.ld_act;
+    }
     else throw ConfigError("export: what must be 0 (H) or 2 (dZ)");
     if (width) *width = w;
     if (out && s->rows)

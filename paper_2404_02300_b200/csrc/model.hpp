@@ -55,6 +55,8 @@ struct catgnn_model_s {
     uint32_t ld = 0;
   };
   std::vector<DzF16> dz_f16;
+  const float* dz_last = nullptr;  // where the last backward kept the last layer's dZ (may alias its T)
+  std::vector<const float*> dz_ptr;  // per layer: the last backward's fp32 dZ buffer (lean aliasing)
 };
 
 namespace catgnn {
