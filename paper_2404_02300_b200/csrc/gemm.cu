@@ -640,6 +640,14 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
         if (!e.partial && (nc == 32 || (e.store_cols && nc % ((e.out_h || e.out_bhi) ? 8 : 4) == 0))) {
           const uint32_t mw = mrow ? mw_cur : 0xffffffffu;
           uint32_t bw = 0;
+          // fp16-only output of a whole chunk: each lane's row segment is 64
+          // contiguous bytes (two sectors), stored straight from registers —
+          // no staging round trip (the skinny-K GEMMs are epilogue bound)
+          // (the residual output only in the 4-epilogue-warp kernels: the 8-warp
+          // ones are capped at 128 registers)
+          const bool direct = e.out_h && !e.out && !e.out_bhi && nc == 32 && (EPIW == 4 || !e.out_hl);
+          uint32_t hw[16];
+          uint32_t lw[EPIW == 4 ? 16 : 1];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -660,7 +668,37 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
             bw |= ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3)) << (4 * i);
             if (e.rowmax && 4 * i < nc)
               rmax = fmaxf(rmax, fmaxf(fmaxf(fabsf(o.x), fabsf(o.y)), fmaxf(fabsf(o.z), fabsf(o.w))));
-            T[lane * kTileLd4 + i] = o;
+            if (direct) {
+              hw[2 * i] = pack_h2(o.x, o.y);
+              hw[2 * i + 1] = pack_h2(o.z, o.w);
+              if constexpr (EPIW == 4) {
+                if (e.out_hl) {  // rounding residual, scaled into the fp16 normal range
+                  const float2 h0 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * i]));
+                  const float2 h1 = __half22float2(*reinterpret_cast<const __half2*>(&hw[2 * i + 1]));
+                  lw[2 * i] = pack_h2((o.x - h0.x) * 2048.f, (o.y - h0.y) * 2048.f);
+                  lw[2 * i + 1] = pack_h2((o.z - h1.x) * 2048.f, (o.w - h1.y) * 2048.f);
+                }
+              }
+            } else {
+              T[lane * kTileLd4 + i] = o;
+            }
+          }
+          if (direct) {
+            if (e.bits_out && row_ok) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
+            if (row_ok) {
+              const size_t o = (size_t)row * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col0;
+              uint4* dst = reinterpret_cast<uint4*>(e.out_h + o);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) dst[k] = make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+              if constexpr (EPIW == 4) {
+                if (e.out_hl) {
+                  uint4* dl = reinterpret_cast<uint4*>(e.out_hl + o);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) dl[k] = make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+                }
+              }
+            }
+            continue;
           }
           if (nc < 32) bw &= (1u << nc) - 1u;  // staged columns past the stored ones are not results
           if (e.bits_out && row_ok) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
