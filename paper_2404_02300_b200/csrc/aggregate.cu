@@ -577,12 +577,59 @@ __global__ void __launch_bounds__(256, MINB) agg_kernel(const AggKernelArgs p) {
 // result is deterministic run to run.  Hub rows with ~100 chunks finish in
 // ~7 dependent loads instead of ~25 with one warp per row.
 constexpr int kFixWarps = 8;
+// split rows with at most this many chunks are combined by one warp each
+// (agg_fixup_warp_kernel); hubs with more keep a whole block
+constexpr int kWarpFixChunks = 16;
+template <int VPL, bool GUARD = false>
+__global__ void __launch_bounds__(256) agg_fixup_warp_kernel(const AggKernelArgs p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t h = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; h < p.n_heavy; h += nw) {
+    const int4 hv = __ldg(p.heavy + h);
+    if (hv.z > kWarpFixChunks) continue;  // a block-per-row hub (agg_fixup_kernel)
+    const int64_t r = hv.x;
+    float ss = 0.f;
+    if (GUARD) {
+      for (int c = lane; c < hv.z; c += 32) ss += __ldcg(p.guard_part + hv.y + c);
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+    }
+    float4 a0[VPL], a1[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) a0[q] = a1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* base = p.partials + (size_t)hv.y * p.w4 * 4;
+    const size_t cs = (size_t)p.w4 * 4;
+    int c = 0;
+    for (; c + 1 < hv.z; c += 2) {  // chunk pairs in flight, fixed combination order
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const uint32_t c4 = lane + 32 * q;
+        if (c4 < p.w4) {
+          add4(a0[q], __ldcg(reinterpret_cast<const float4*>(base + (size_t)c * cs + c4 * 4)));
+          add4(a1[q], __ldcg(reinterpret_cast<const float4*>(base + (size_t)(c + 1) * cs + c4 * 4)));
+        }
+      }
+    }
+    if (c < hv.z) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const uint32_t c4 = lane + 32 * q;
+        if (c4 < p.w4) add4(a0[q], __ldcg(reinterpret_cast<const float4*>(base + (size_t)c * cs + c4 * 4)));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) add4(a0[q], a1[q]);
+    const float deg = (float)(__ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r));
+    epilogue_row<VPL, 32, true, 1, GUARD>(p, r, deg, a0, lane, nullptr, ss);
+  }
+}
 template <int VPL, bool GUARD = false>
 __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
   __shared__ float4 part[kFixWarps][32 * VPL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint64_t h = blockIdx.x; h < p.n_heavy; h += gridDim.x) {
     const int4 hv = __ldg(p.heavy + h);
+    if (hv.z <= kWarpFixChunks) continue;  // combined by agg_fixup_warp_kernel
     const int64_t r = hv.x;
     float ss = 0.f;
     if (GUARD) {  // the guard's sum over the row's chunks (fixed order)
@@ -840,16 +887,16 @@ AggFn pick_kernel(uint32_t w4, bool pre, bool bits, bool h16, bool zr, bool guar
   }
 }
 
-AggFn pick_fixup(uint32_t w4) {
+AggFn pick_fixup(uint32_t w4, bool warp) {
   switch ((w4 + 31) / 32) {
-    case 1: return agg_fixup_kernel<1>;
-    case 2: return agg_fixup_kernel<2>;
-    case 3: return agg_fixup_kernel<3>;
-    case 4: return agg_fixup_kernel<4>;
-    case 5: return agg_fixup_kernel<5>;
-    case 6: return agg_fixup_kernel<6>;
-    case 7: return agg_fixup_kernel<7>;
-    default: return agg_fixup_kernel<8>;
+    case 1: return warp ? agg_fixup_warp_kernel<1> : agg_fixup_kernel<1>;
+    case 2: return warp ? agg_fixup_warp_kernel<2> : agg_fixup_kernel<2>;
+    case 3: return warp ? agg_fixup_warp_kernel<3> : agg_fixup_kernel<3>;
+    case 4: return warp ? agg_fixup_warp_kernel<4> : agg_fixup_kernel<4>;
+    case 5: return warp ? agg_fixup_warp_kernel<5> : agg_fixup_kernel<5>;
+    case 6: return warp ? agg_fixup_warp_kernel<6> : agg_fixup_kernel<6>;
+    case 7: return warp ? agg_fixup_warp_kernel<7> : agg_fixup_kernel<7>;
+    default: return warp ? agg_fixup_warp_kernel<8> : agg_fixup_kernel<8>;
   }
 }
 
@@ -964,11 +1011,18 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     fn<<<grid, 256, 0, ctx->stream>>>(p);
     CG_CHECK_LAUNCH();
     ctx->launches++;
-    if (s->n_heavy) {
-      AggFn fx = guard ? agg_fixup_kernel<2, true> : pick_fixup(w4);
-      const unsigned g2 = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 16);
-      fx<<<g2, 256, 0, ctx->stream>>>(p);
+    if (s->n_heavy) {  // split rows: warp per row up to kWarpFixChunks chunks, block per hub row
+      AggFn fw = guard ? agg_fixup_warp_kernel<2, true> : pick_fixup(w4, true);
+      const unsigned gw = (unsigned)std::min<uint64_t>((s->n_heavy + 7) / 8, (uint64_t)ctx->num_sms * 8);
+      fw<<<gw, 256, 0, ctx->stream>>>(p);
       CG_CHECK_LAUNCH();
+      if (s->n_big_heavy) {
+        AggFn fx = guard ? agg_fixup_kernel<2, true> : pick_fixup(w4, false);
+        const unsigned g2 = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 16);
+        fx<<<g2, 256, 0, ctx->stream>>>(p);
+        CG_CHECK_LAUNCH();
+        ctx->launches++;
+      }
       ctx->launches++;
     }
     if (guard) {  // exact fp32 recomputation of the flagged elements

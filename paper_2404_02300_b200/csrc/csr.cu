@@ -131,13 +131,15 @@ uint32_t env_unit_cost() {
 // plan_rows_kernel: per row, the units it emits (1 for a unit start, nch for a
 // heavy row, else 0), its heavy flag and its chunk count.
 __global__ void plan_rows_kernel(const int64_t* __restrict__ row_ptr, uint64_t rows, uint32_t U,
-                                 uint64_t row_cost, uint64_t* __restrict__ cost, uint32_t* __restrict__ nch) {
+                                 uint64_t row_cost, uint64_t* __restrict__ cost, uint32_t* __restrict__ nch,
+                                 unsigned long long* __restrict__ big) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
        r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t deg = (uint64_t)(row_ptr[r + 1] - row_ptr[r]);
     const bool heavy = deg > U;
     cost[r] = heavy ? 0 : deg + row_cost;
     nch[r] = heavy ? (uint32_t)((deg + U - 1) / U) : 0;
+    if (heavy && nch[r] > 16) atomicAdd(big, 1ull);  // aggregate.cu kWarpFixChunks
   }
 }
 // emit[r]: units row r opens (needs the exclusive cost prefix P)
@@ -208,7 +210,7 @@ void build_plan(catgnn_shard_s* s) {
   const uint64_t rows = s->rows;
   s->unit_cost = U;
   if (rows == 0) {
-    s->n_units = s->n_heavy = s->n_chunks = 0;
+    s->n_units = s->n_heavy = s->n_chunks = s->n_big_heavy = 0;
     s->units.alloc(1);
     s->heavy.alloc(1);
     return;
@@ -226,7 +228,9 @@ void build_plan(catgnn_shard_s* s) {
   CG_CUDA(cudaMemsetAsync(nch + rows, 0, 4, st));
   CG_CUDA(cudaMemsetAsync(emit + rows, 0, 4, st));
   CG_CUDA(cudaMemsetAsync(ish + rows, 0, 4, st));
-  plan_rows_kernel<<<grid_for(rows), 256, 0, st>>>(s->row_ptr.p, rows, U, row_cost, cost, nch);
+  unsigned long long* big = ctx->scratch_buf<unsigned long long>("k1_plan_big", 1);
+  CG_CUDA(cudaMemsetAsync(big, 0, 8, st));
+  plan_rows_kernel<<<grid_for(rows), 256, 0, st>>>(s->row_ptr.p, rows, U, row_cost, cost, nch, big);
   CG_CHECK_LAUNCH();
   exclusive_scan(ctx, cost, P, n1);
   plan_emit_kernel<<<grid_for(rows), 256, 0, st>>>(P, nch, rows, U, emit, ish);
@@ -237,14 +241,16 @@ void build_plan(catgnn_shard_s* s) {
   exclusive_scan(ctx, e64, upos, n1);
   exclusive_scan(ctx, h64, hpos, n1);
   exclusive_scan(ctx, c64, cpos, n1);
-  uint64_t tot[3];
+  uint64_t tot[4];
   CG_CUDA(cudaMemcpyAsync(&tot[0], upos + rows, 8, cudaMemcpyDeviceToHost, st));
   CG_CUDA(cudaMemcpyAsync(&tot[1], hpos + rows, 8, cudaMemcpyDeviceToHost, st));
   CG_CUDA(cudaMemcpyAsync(&tot[2], cpos + rows, 8, cudaMemcpyDeviceToHost, st));
+  CG_CUDA(cudaMemcpyAsync(&tot[3], big, 8, cudaMemcpyDeviceToHost, st));
   CG_CUDA(cudaStreamSynchronize(st));
   s->n_units = tot[0];
   s->n_heavy = tot[1];
   s->n_chunks = tot[2];
+  s->n_big_heavy = tot[3];
   if (s->n_units >= 0x7fffffffull || s->n_chunks >= 0x7fffffffull)
     throw ConfigError("aggregation plan exceeds the int32 unit range");
   s->units.alloc(std::max<uint64_t>(1, s->n_units));

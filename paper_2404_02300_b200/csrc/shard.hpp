@@ -33,6 +33,7 @@ struct catgnn_shard_s {
   catgnn::DevBuf<int4> units;
   catgnn::DevBuf<int4> heavy;
   uint64_t n_units = 0, n_heavy = 0, n_chunks = 0;
+  uint64_t n_big_heavy = 0;  // split rows with more than 16 chunks (block-per-row fix-up)
   uint32_t unit_cost = 0;
   // features
   uint32_t dim = 0, ld = 0;
