@@ -823,6 +823,51 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ partial, uint32_t s
     store_epi(e, row, col, apply_epi(e, row, col, acc));
   }
 }
+// Split-K sums of a plain fp32 output (the weight gradients: no epilogue ops),
+// four columns per thread, four splits' loads in flight, summed in split order
+// (the same order as gemm_reduce_kernel: deterministic, identical results).
+__global__ void gemm_reduce4_kernel(const float4* __restrict__ partial, uint32_t splits, uint32_t M, uint32_t N,
+                                    float* __restrict__ out, uint32_t ld_out, uint32_t out_col) {
+  const uint64_t total4 = (uint64_t)M * N / 4;
+  const uint32_t n4 = N / 4;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total4;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t z = 0;
+    for (; z + 3 < splits; z += 4) {
+      const float4 a = __ldcg(partial + (uint64_t)z * total4 + i), b = __ldcg(partial + (uint64_t)(z + 1) * total4 + i);
+      const float4 c = __ldcg(partial + (uint64_t)(z + 2) * total4 + i), d = __ldcg(partial + (uint64_t)(z + 3) * total4 + i);
+      acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+      acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w;
+      acc.x += c.x; acc.y += c.y; acc.z += c.z; acc.w += c.w;
+      acc.x += d.x; acc.y += d.y; acc.z += d.z; acc.w += d.w;
+    }
+    for (; z < splits; ++z) {
+      const float4 a = __ldcg(partial + (uint64_t)z * total4 + i);
+      acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+    }
+    const uint32_t row = (uint32_t)(i / n4), c4 = (uint32_t)(i % n4);
+    *reinterpret_cast<float4*>(out + (size_t)row * ld_out + out_col + c4 * 4) = acc;
+  }
+}
+// the split-K reduction: the vectorised kernel when the output is a plain
+// 16-byte aligned fp32 matrix, else the general one
+void launch_reduce(catgnn_ctx ctx, const float* partial, uint32_t splits, uint32_t M, uint32_t N, const GemmEpi& epi) {
+  const bool plain = epi.out && !epi.out_h && !epi.out_bhi && !epi.rowscale && !epi.bias && !epi.relu &&
+                     !epi.mask_bits && !epi.bits_out && !epi.rowmax && epi.out_scale == 1.0f && N % 4 == 0 &&
+                     epi.ld_out % 4 == 0 && epi.out_col % 4 == 0;
+  const uint64_t total = (uint64_t)M * N;
+  if (plain) {
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total / 4 + 255) / 256, 148 * 16));
+    gemm_reduce4_kernel<<<g, 256, 0, ctx->stream>>>(reinterpret_cast<const float4*>(partial), splits, M, N, epi.out,
+                                                    epi.ld_out, epi.out_col);
+  } else {
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
+    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(partial, splits, M, N, epi);
+  }
+  CG_CHECK_LAUNCH();
+  ctx->launches++;
+}
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -1063,13 +1108,7 @@ void gemm(catgnn_ctx ctx, GemmOperand a, GemmOperand b, uint32_t M, uint32_t N, 
   }
   CG_CHECK_LAUNCH();
   ctx->launches++;
-  if (splits > 1) {
-    const uint64_t total = (uint64_t)M * N;
-    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
-    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(partial, splits, M, N, epi);
-    CG_CHECK_LAUNCH();
-    ctx->launches++;
-  }
+  if (splits > 1) launch_reduce(ctx, partial, splits, M, N, epi);
   ctx->end_timed(t);
 }
 
@@ -1261,13 +1300,7 @@ void gemm_bf16x3(catgnn_ctx ctx, SplitOperand a, SplitOperand b, uint32_t M, uin
   }
   CG_CHECK_LAUNCH();
   ctx->launches++;
-  if (splits > 1) {
-    const uint64_t total = (uint64_t)M * N;
-    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
-    gemm_reduce_kernel<<<g, 256, 0, ctx->stream>>>(partial, splits, M, N, epi);
-    CG_CHECK_LAUNCH();
-    ctx->launches++;
-  }
+  if (splits > 1) launch_reduce(ctx, partial, splits, M, N, epi);
   ctx->end_timed(t);
 }
 
