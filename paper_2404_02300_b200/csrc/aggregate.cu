@@ -432,7 +432,7 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
       float4 acc[VPL * CPV];
 #pragma unroll
       for (int k = 0; k < VPL * CPV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      float ss = 0.f;  // GUARD: sum of the gathered rows' squared maxima (same on every lane)
+      float ss = 0.f;  // GUARD: per lane, the squared maxima of the window slots it held (summed at the row end)
       for (int e = e0; e < e1; e += B) {
         while (e >= cb + 32) {  // warp-uniform: advance the index window by one chunk
           cb += 32;
@@ -459,12 +459,12 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
             wins = off < 32 ? sa : sb;
           }
           const int rem = min(e1 - e, B);  // valid neighbours of the batch
+          if (GUARD && lane < rem) ss = fmaf(wins, wins, ss);  // lane l holds edge e + l's row max
 #pragma unroll
           for (int uu = 0; uu < UNROLL; ++uu) {
             const int j = __shfl_sync(0xffffffffu, win, uu);
-            s[uu] = SC ? __shfl_sync(0xffffffffu, wins, uu) : 1.f;
+            s[uu] = PRE ? __shfl_sync(0xffffffffu, wins, uu) : 1.f;
             ok[uu] = uu < rem;
-            if (GUARD && ok[uu]) ss = fmaf(s[uu], s[uu], ss);
 #pragma unroll
             for (int q = 0; q < VPL; ++q) {
               if constexpr (ZR)  // idle slots load the zero row
@@ -512,6 +512,10 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
       for (int m = LPN; m < 32; m <<= 1)
 #pragma unroll
         for (int k = 0; k < VPL * CPV; ++k) add4(acc[k], shfl_xor4(acc[k], m));
+      if (GUARD) {
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+      }
       if (writer) epilogue_row<VPL, LPN, BITS, CPV, GUARD>(p, r, (float)(e1 - e0), acc, li, &selfv, ss);
     }
   }

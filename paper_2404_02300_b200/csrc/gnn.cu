@@ -93,7 +93,7 @@ __global__ void softmax_ce_kernel(const float* __restrict__ Z, uint32_t ldz, uin
     for (uint32_t c = lane; c < C; c += 32) {
       float p = expf(z[c] - m) / s;
       if ((int)c == y) p -= 1.0f;
-      dZ[(size_t)r * lddz + c] = p * inv_n;
+      if (dZ) dZ[(size_t)r * lddz + c] = p * inv_n;
       if (dZh) dZh[(size_t)r * ldh + c] = __float2half_rn((rs ? sc : 1.f) * (p * inv_n) * hscale);
       else if (rs) dZs[(size_t)r * lddz + c] = sc * (p * inv_n);
     }
@@ -810,11 +810,14 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
   // 22 GB on a 31 M-row papers-scale partition)
   const bool reuse_t = !LL.agg_first && M->cfg.kind != CATGNN_MODEL_SAGE && B[nl - 1].mid &&
                        B[nl - 1].mid_ld == LL.ld_act;
-  float* dZ = reuse_t ? B[nl - 1].mid : act(ctx, nm("dZ", nl - 1), rows, LL.ld_act, false);
+  // with fp16 backward inputs the last layer's dZ exists only as the fp16 K2
+  // input (its bias gradient sums those rows): no fp32 copy is written
+  const bool last_h = f16_bwd(M, nl - 1);
+  float* dZ = last_h ? nullptr : reuse_t ? B[nl - 1].mid : act(ctx, nm("dZ", nl - 1), rows, LL.ld_act, false);
   M->dz_last = dZ;
   M->dz_ptr.assign(nl, nullptr);
   M->dz_ptr[nl - 1] = dZ;
-  CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
+  if (dZ) CG_CUDA(cudaMemsetAsync(dZ, 0, std::max<uint64_t>(1, rows) * LL.ld_act * 4, st));
   const uint64_t ntr = S->h_train.size();
   // fp16 gradient rows carry 2^k <= n_train (|dZ| <= 1 / n_train)
   const float gscale = std::ldexp(1.0f, (int)std::floor(std::log2((double)std::max<uint64_t>(ntr, 1))));
@@ -855,7 +858,7 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
     const Layer& L = M->layers[li];
     const Bufs& b = B[li];
     float* gW = M->grads.p + L.off_w;
-    if (dzh && li + 1 < nl) {
+    if (dzh) {
       const auto& z = M->dz_f16[li];
       colsum(ctx, nullptr, z.ld, rows, L.d_out, M->grads.p + L.off_b, dzh, z.rs, 1.0f / z.scale);
     } else {

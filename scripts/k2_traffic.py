@@ -5,7 +5,8 @@ line's roofline (all passes, not 2 of 32).
     python scripts/k2_traffic.py [WORKLOAD] [OUT.json]
 
 Runs `ncu --metrics ... -k regex:agg_ python bench.py --steps 1 --warmup 1
---graph 0 --no-e2e --no-cpu-baseline` (one eager warm-up step + one timed step),
+--graph 0 --no-e2e --no-cpu-baseline --lanes 1` (one eager warm-up step + one timed
+step, partitions in order on one stream),
 keeps the timed step's launches (the second half), and tags each agg_kernel
 launch with its partition and pass (the step runs partitions in order, each
 with its epoch's passes in workload.passes() order; split-row fix-ups are
@@ -48,7 +49,7 @@ def main():
         env = dict(os.environ, CATGNN_WORKLOAD=workload)
         cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:agg_", "--csv",
                "--log-file", log, sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1",
-               "--graph", "0", "--no-e2e", "--no-cpu-baseline"]
+               "--graph", "0", "--no-e2e", "--no-cpu-baseline", "--lanes", "1"]
         subprocess.run(cmd, env=env, check=True, stdout=subprocess.DEVNULL)
     launches = {}
     with open(log) as f:

@@ -3,7 +3,7 @@
 #   scripts/profile.sh [K2 launches to capture] [K3 launches to capture]
 set -x
 export CATGNN_CACHE=${CATGNN_CACHE:-/tmp/catgnn_cache}
-ARGS="--steps 1 --warmup 1 --no-e2e --no-cpu-baseline --graph 0"
+ARGS="--steps 1 --warmup 1 --no-e2e --no-cpu-baseline --graph 0 --lanes 1"
 NK2=${1:-4}
 NK3=${2:-5}
 python bench.py $ARGS > /dev/null 2> gpurun_out/prep.err   # build the cache

@@ -4,7 +4,7 @@
 set -x
 mkdir -p gpurun_out
 export CATGNN_CACHE=/tmp/catgnn_cache
-ARGS="--steps 1 --warmup 1 --no-e2e --no-cpu-baseline --graph 0"
+ARGS="--steps 1 --warmup 1 --no-e2e --no-cpu-baseline --graph 0 --lanes 1"
 python bench.py $ARGS > /dev/null 2> gpurun_out/prep.err
 timeout 900 python scripts/k2_traffic.py reddit_gcn gpurun_out/r02_k2_traffic_reddit_gcn.json > gpurun_out/k2t.log 2>&1
 cp gpurun_out/r02_k2_traffic_reddit_gcn.json profiles/
@@ -18,6 +18,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-fi
     python bench.py $ARGS > /dev/null 2>&1
 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
 python bench.py --impl reference > gpurun_out/r02_bench_reference_arm.json 2> gpurun_out/r02_bench_ref.err
-python bench.py --workload products_sage --no-cpu-baseline > gpurun_out/r02_bench_products_sage.json 2> /dev/null
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/r02_full_tests.log 2>&1; tail -2 gpurun_out/r02_full_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+
 python bench.py --workload papers_gin_s24 --no-cpu-baseline > gpurun_out/r02_bench_papers_gin_s24.json 2> /dev/null
 tail -c 400 gpurun_out/r02_bench.json gpurun_out/r02_bench_reference_arm.json
