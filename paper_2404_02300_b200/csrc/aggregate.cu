@@ -730,7 +730,7 @@ __device__ __forceinline__ int next_cols(uint32_t words, uint32_t& w, uint32_t& 
   return nc;
 }
 __device__ __forceinline__ float lo_at(const __half* __restrict__ lo, size_t i) { return __half2float(__ldg(lo + i)); }
-__global__ void __launch_bounds__(256) agg_exact_fix_kernel(const AggKernelArgs p, const __half* __restrict__ lo) {
+__global__ void __launch_bounds__(256, 8) agg_exact_fix_kernel(const AggKernelArgs p, const __half* __restrict__ lo) {
   const int lane = threadIdx.x & 31;
   const unsigned n = *p.fix_count;
   for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
