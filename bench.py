@@ -385,7 +385,7 @@ def main():
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         raise SystemExit(self_launch(args.gpus))
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     w = W.WORKLOADS[args.workload]
     world, rank, local = dist_env()
     if world != args.gpus:

@@ -21,7 +21,7 @@ from dataclasses import asdict, dataclass
 
 import numpy as np
 
-from . import synth
+from paper_2404_02300_b200 import synth
 
 
 @dataclass(frozen=True)
@@ -143,7 +143,7 @@ def prepare(w: Workload, log=print, native: bool = True) -> dict:
         try:
             import torch
             if torch.cuda.is_available():
-                from . import gnnpart as gp
+                from paper_2404_02300_b200 import gnnpart as gp
                 parts = gp.complete_edges(e, home, roles, w.partitions)
         except Exception as ex:  # pragma: no cover
             log(f"[prep] device completion unavailable ({ex}); NumPy completion")

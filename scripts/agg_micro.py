@@ -10,7 +10,8 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2404_02300_b200 import gnnpart as gp, workloads as W  # noqa: E402
+from paper_2404_02300_b200 import gnnpart as gp
+from benchdata import workloads as W  # noqa: E402
 
 w = W.WORKLOADS[os.environ.get("WORKLOAD", "reddit_gcn")]
 prep = W.prepare(w, lambda *a: None)

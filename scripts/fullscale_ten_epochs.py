@@ -33,7 +33,7 @@ SEED, HIDDEN, LR = 7, 256, 0.01
 
 def oracle_shard(prep, i):
     from oracle import gnn_oracle as go, ref
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     p = W.load_part(prep, i)
     rows = p["ext"].size
     local = np.searchsorted(p["ext"], p["edges"].ravel()).astype(np.uint32).reshape(-1, 2)
@@ -63,7 +63,7 @@ def worker(prep, i, init_flat, conn, name):
 
 
 def _workload(name=None):
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     return W.WORKLOADS[name or WORKLOAD]
 
 
@@ -73,7 +73,7 @@ def _kind(w):
 
 
 def load_global(prep):
-    from paper_2404_02300_b200 import workloads as W  # noqa: F401
+    from benchdata import workloads as W  # noqa: F401
     X = np.load(os.path.join(prep["dir"], "features.npy"), mmap_mode="r")
     labels = np.load(os.path.join(prep["dir"], "labels.npy"))
     roles = np.load(os.path.join(prep["dir"], "roles.npy"))
@@ -85,7 +85,7 @@ def load_global(prep):
 def run_gpu(epochs=EPOCHS, name=None):
     """The B200 half: all partitions through the library (s = 1), then the
     averaged model's test accuracy on the global graph.  Returns a dict."""
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     from paper_2404_02300_b200 import gnn, gnnpart as gp
     w = _workload(name)
     prep = W.prepare(w, lambda *a: None)
@@ -117,7 +117,7 @@ def run_oracle(epochs=EPOCHS, name=None):
     partition order in the parent, as model_average), then the test accuracy of
     the averaged model on the global graph."""
     from oracle import gnn_oracle as go
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     w = _workload(name)
     prep = W.prepare(w, lambda *a: None)
     X, labels, roles, edges = load_global(prep)

@@ -39,7 +39,7 @@ def compulsory_bytes(nnz, rows, width, eb):
 def main():
     workload = sys.argv[1] if len(sys.argv) > 1 else "reddit_gcn"
     out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", f"r02_k2_traffic_{workload}.json")
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     w = W.WORKLOADS[workload]
     prep = W.prepare(w, lambda *a: None)
     meta = prep["meta"]

@@ -4,7 +4,8 @@ timeout 1200 python -m pytest tests/test_gpu_sgc.py tests/test_gpu_completion.py
 python - <<'PY'
 import time, numpy as np, sys
 sys.path.insert(0, '.')
-from paper_2404_02300_b200 import gnnpart as gp, workloads as W
+from paper_2404_02300_b200 import gnnpart as gp
+from benchdata import workloads as W
 w = W.WORKLOADS['reddit_gcn']; prep = W.prepare(w, lambda *a: None); part = W.load_part(prep, 0)
 ctx = gp.Context(0)
 for i in range(3):

@@ -25,7 +25,7 @@ def main():
     widths = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "41,256").split(",")]
     import bench
     from oracle import ref
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     w = W.WORKLOADS[workload]
     prep = W.prepare(w, lambda *a: None, native=False)
     d = prep["dir"]

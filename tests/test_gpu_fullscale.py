@@ -26,7 +26,8 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 @pytest.mark.parametrize("workload", ["reddit_gcn", "products_sage", "papers_gin_s24"])
 def test_partition_one_step_matches_oracle(workload):
-    from paper_2404_02300_b200 import gnnpart as gp, workloads as W
+    from paper_2404_02300_b200 import gnnpart as gp
+    from benchdata import workloads as W
     from paper_2404_02300_b200.gnn import GNNModel
     w = W.WORKLOADS[workload]
     kind = {"gcn": go.GCN, "sage": go.SAGE, "gin": go.GIN}[w.model]
@@ -62,7 +63,7 @@ def test_ten_epochs_match_frozen_oracle():
     fx = json.load(open(os.path.join(here, "golden", "fullscale_reddit_gcn.json")))
     sys.path.insert(0, os.path.join(os.path.dirname(here), "scripts"))
     import fullscale_ten_epochs as F
-    from paper_2404_02300_b200 import workloads as W
+    from benchdata import workloads as W
     assert W.WORKLOADS["reddit_gcn"].key() == fx["workload_key"]
     assert (F.SEED, F.HIDDEN, F.LR) == (fx["seed"], fx["hidden"], fx["lr"])
     g = F.run_gpu(fx["epochs"], "reddit_gcn")
