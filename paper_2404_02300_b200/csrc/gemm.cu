@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
           // no staging round trip (the skinny-K GEMMs are epilogue bound)
           // (the residual output only in the 4-epilogue-warp kernels: the 8-warp
           // ones are capped at 128 registers)
-          const bool direct = e.out_h && !e.out && !e.out_bhi && nc == 32 && (EPIW == 4 || !e.out_hl);
+          const bool direct = e.out_h && !e.out && !e.out_bhi && nc % 8 == 0 && (EPIW == 4 || !e.out_hl);
           uint32_t hw[16];
           uint32_t lw[EPIW == 4 ? 16 : 1];
 #pragma unroll
@@ -684,17 +684,20 @@ __global__ void __launch_bounds__(threads_for<EPIW>(), 1)
             }
           }
           if (direct) {
+            if (nc < 32) bw &= (1u << nc) - 1u;
             if (e.bits_out && row_ok) e.bits_out[(size_t)row * e.bits_words + col0 / 32] = bw;
             if (row_ok) {
               const size_t o = (size_t)row * (e.ld_h ? e.ld_h : e.ld_out) + e.out_col + col0;
               uint4* dst = reinterpret_cast<uint4*>(e.out_h + o);
 #pragma unroll
-              for (int k = 0; k < 4; ++k) dst[k] = make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+              for (int k = 0; k < 4; ++k)
+                if (8 * k < (int)nc) dst[k] = make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
               if constexpr (EPIW == 4) {
                 if (e.out_hl) {
                   uint4* dl = reinterpret_cast<uint4*>(e.out_hl + o);
 #pragma unroll
-                  for (int k = 0; k < 4; ++k) dl[k] = make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+                  for (int k = 0; k < 4; ++k)
+                    if (8 * k < (int)nc) dl[k] = make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
                 }
               }
             }
