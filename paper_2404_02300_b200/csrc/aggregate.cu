@@ -50,6 +50,8 @@ struct AggKernelArgs {
   uint32_t in_ld, in_col;
   float in_scale;                   // folded into the post scale (fp16 inputs stored scaled by 1/in_scale)
   int zero_row;                     // fp16 inputs: index of an all-zero row (= rows), the target of idle loads
+  const int32_t* __restrict__ row_map;  // row views: a view row's row in the buffers
+  const float* __restrict__ post_arr;   // per-row post scale (filtered views), else from the degree
   // guarded fp16 forward (GUARD): per-row max |T_j| of the fp16-rounded rows,
   // flagged-column bits, the rows with flags and their count, the threshold
   // factor (see epilogue_row)
@@ -193,13 +195,14 @@ __device__ __forceinline__ float post_scale(int norm, float deg) {
 // they are flagged (flag_bits), their fp16-path pre-activation kept
 // (guard_pre) and their row listed (fix_rows / fix_heavy) for the exact fix.
 template <int VPL, int LPN, bool BITS, int CPV, bool GUARD = false>
-__device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t r, float deg,
+__device__ __forceinline__ void epilogue_row(const AggKernelArgs& p, int64_t rv, float deg,
                                              const float4 (&acc)[VPL * CPV], int li,
                                              const float4 (*selfv)[VPL * CPV] = nullptr, float s2 = 0.f) {
+  const int64_t r = p.row_map ? (int64_t)__ldg(p.row_map + rv) : rv;  // the row in the output / input buffers
   // lanes [0, LPN) run this together (bit words are assembled across them)
   constexpr unsigned kLanes = LPN == 32 ? 0xffffffffu : ((1u << LPN) - 1u);
   constexpr int kGroup = LPN < 8 / CPV ? LPN : 8 / CPV;  // lanes whose nibbles form one 32-bit word
-  const float post = post_scale(p.norm, deg) * p.in_scale;
+  const float post = (p.post_arr ? __ldg(p.post_arr + r) : post_scale(p.norm, deg)) * p.in_scale;
   const float selfs = p.pre ? __ldg(p.pre + r) : 1.0f;
   uint32_t nib[VPL * CPV];  // (out > 0) per column of each float4, for bits_out
   uint32_t fnib[VPL * CPV];  // GUARD: flagged columns
@@ -424,9 +427,10 @@ __device__ __forceinline__ void light_unit(const AggKernelArgs& p, int64_t r0, i
       if (e1 - e0 < AGG_SKIP_SHORT) continue;
 #endif
       float4 selfv[VPL * CPV];
+      const int64_t rsrc = p.row_map ? (int64_t)__ldg(p.row_map + r) : r;  // own input row (row views)
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
-        const uint4 sv = (p.self && writer && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, (int)r, q) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 sv = (p.self && writer && colok[q]) ? ld_nbr<VPL, LPN>(base, ldb, (int)rsrc, q) : make_uint4(0u, 0u, 0u, 0u);
         raw_to_f4<CPV>(selfv + q * CPV, sv);
       }
       float4 acc[VPL * CPV];
@@ -933,6 +937,7 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
   if (a.in == a.out && a.in && a.in_ld != a.out_ld) throw ConfigError("aggregation cannot run in place");
   if (s->rows == 0 || a.width == 0) return;
   if (!a.out && !a.out_hi) throw ConfigError("aggregation needs an output");
+  if (a.guard_smax && a.row_map) throw ConfigError("guarded aggregation over a row view");
   if (a.guard_smax && (!a.in_h || a.width != 256 || !a.bits_out || !a.relu || a.pre || a.mask_bits || a.residual ||
                        !a.guard_flags || !a.guard_lo || a.bits_words != 8))
     throw ConfigError("guarded fp16 aggregation: fp16 input, 256 columns, ReLU with bit output, fp16 residual");
@@ -957,7 +962,9 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     p.in = a.in;
     p.in_h = static_cast<const __half*>(a.in_h);
     p.in_scale = a.in_scale;
-    p.zero_row = (int)s->rows;
+    p.zero_row = (int)(a.zero_row >= 0 ? a.zero_row : (int64_t)s->rows);
+    p.row_map = a.row_map;
+    p.post_arr = a.post_arr;
     p.in_ld = a.in_ld;
     p.in_col = a.in_col + c4 * 4;
     p.out = a.out;

@@ -142,6 +142,8 @@ void set_labels(catgnn_shard_s* s, const int32_t* labels, const uint32_t* tr, ui
   s->h_labels.assign(labels ? labels : nullptr, labels ? labels + s->rows : nullptr);
   if (!labels) s->h_labels.assign(s->rows, 0);
   s->h_train.assign(tr, tr + ntr);
+  s->train_sub.reset();  // train-row views of the old roles (csr.cu)
+  s->train_nbr.reset();
   s->h_val.assign(va, va + nva);
   s->h_test.assign(te, te + nte);
   for (auto* v : {&s->h_train, &s->h_val, &s->h_test})

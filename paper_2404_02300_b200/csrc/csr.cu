@@ -262,7 +262,131 @@ void build_plan(catgnn_shard_s* s) {
   ctx->launches += 4;
 }
 
+// train-row views (train_rows_view / train_nbr_view)
+__global__ void view_deg_kernel(const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ rows_sel,
+                                uint64_t n, uint64_t* __restrict__ deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = rows_sel[i];
+    deg[i] = (uint64_t)(row_ptr[r + 1] - row_ptr[r]);
+  }
+}
+// warp per selected row: its neighbour list copied in order
+__global__ void view_copy_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                 const uint32_t* __restrict__ rows_sel, uint64_t n,
+                                 const int64_t* __restrict__ vptr, int32_t* __restrict__ vcol) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t r = rows_sel[i];
+    const int64_t b = row_ptr[r], e = row_ptr[r + 1], o = vptr[i];
+    for (int64_t k = b + lane; k < e; k += 32) vcol[o + (k - b)] = col[k];
+  }
+}
+__global__ void mark_rows_kernel(const uint32_t* __restrict__ rows_sel, uint64_t n, uint8_t* __restrict__ flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    flag[rows_sel[i]] = 1;
+}
+// warp per row: neighbours that are flagged (counted, then compacted in order)
+__global__ void filter_count_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                    uint64_t rows, const uint8_t* __restrict__ flag, uint64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    uint32_t c = 0;
+    for (int64_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) c += flag[col[k]];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+    if (lane == 0) cnt[r] = c;
+  }
+}
+__global__ void filter_copy_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                   uint64_t rows, const uint8_t* __restrict__ flag, const int64_t* __restrict__ fptr,
+                                   int32_t* __restrict__ fcol) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t o = fptr[r];
+    const int64_t e1 = row_ptr[r + 1];
+    for (int64_t k0 = row_ptr[r]; k0 < e1; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const int32_t j = k < e1 ? col[k] : 0;
+      const bool keep = k < e1 && flag[j];
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) fcol[o + __popc(m & ((1u << lane) - 1u))] = j;
+      o += __popc(m);
+    }
+  }
+}
+
+unsigned warps_grid(uint64_t n) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, 148ull * 16));
+}
+
+// A view shard sharing the parent's context: CSR (row_ptr from per-row counts)
+// + its own K2 work plan.
+std::unique_ptr<catgnn_shard_s> make_view(catgnn_shard_s* s, uint64_t rows, const uint64_t* d_cnt) {
+  auto v = std::make_unique<catgnn_shard_s>();
+  v->ctx = s->ctx;
+  v->rows = rows;
+  v->row_ptr.alloc(rows + 1);
+  uint64_t* tmp = s->ctx->scratch_buf<uint64_t>("sub_scan", rows + 1);
+  CG_CUDA(cudaMemcpyAsync(tmp, d_cnt, rows * 8, cudaMemcpyDeviceToDevice, s->ctx->stream));
+  CG_CUDA(cudaMemsetAsync(tmp + rows, 0, 8, s->ctx->stream));
+  exclusive_scan(s->ctx, tmp, reinterpret_cast<uint64_t*>(v->row_ptr.p), rows + 1);
+  int64_t nnz = 0;
+  CG_CUDA(cudaMemcpyAsync(&nnz, v->row_ptr.p + rows, 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+  CG_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  v->nnz = (uint64_t)nnz;
+  v->col.alloc(std::max<uint64_t>(1, v->nnz));
+  return v;
+}
+
 }  // namespace
+
+catgnn_shard_s* train_rows_view(catgnn_shard_s* s) {
+  const uint64_t n = s->h_train.size();
+  if (!n) return nullptr;
+  if (!s->train_sub) {
+    cudaStream_t st = s->ctx->stream;
+    uint64_t* deg = s->ctx->scratch_buf<uint64_t>("sub_cnt", n);
+    view_deg_kernel<<<grid_for(n), 256, 0, st>>>(s->row_ptr.p, s->d_train.p, n, deg);
+    CG_CHECK_LAUNCH();
+    auto v = make_view(s, n, deg);
+    view_copy_kernel<<<warps_grid(n), 256, 0, st>>>(s->row_ptr.p, s->col.p, s->d_train.p, n, v->row_ptr.p, v->col.p);
+    CG_CHECK_LAUNCH();
+    v->row_map.alloc(n);
+    CG_CUDA(cudaMemcpyAsync(v->row_map.p, s->d_train.p, n * 4, cudaMemcpyDeviceToDevice, st));
+    build_plan(v.get());
+    s->ctx->launches += 3;
+    s->ctx->release_scratch({"k1_", "sub_"});
+    s->train_sub = std::move(v);
+  }
+  return s->train_sub.get();
+}
+
+catgnn_shard_s* train_nbr_view(catgnn_shard_s* s) {
+  const uint64_t n = s->h_train.size();
+  if (!n || !s->rows) return nullptr;
+  if (!s->train_nbr) {
+    cudaStream_t st = s->ctx->stream;
+    uint8_t* flag = s->ctx->scratch_buf<uint8_t>("sub_flag", s->rows);
+    CG_CUDA(cudaMemsetAsync(flag, 0, s->rows, st));
+    mark_rows_kernel<<<grid_for(n), 256, 0, st>>>(s->d_train.p, n, flag);
+    CG_CHECK_LAUNCH();
+    uint64_t* cnt = s->ctx->scratch_buf<uint64_t>("sub_cnt", s->rows);
+    filter_count_kernel<<<warps_grid(s->rows), 256, 0, st>>>(s->row_ptr.p, s->col.p, s->rows, flag, cnt);
+    CG_CHECK_LAUNCH();
+    auto v = make_view(s, s->rows, cnt);
+    filter_copy_kernel<<<warps_grid(s->rows), 256, 0, st>>>(s->row_ptr.p, s->col.p, s->rows, flag, v->row_ptr.p,
+                                                           v->col.p);
+    CG_CHECK_LAUNCH();
+    build_plan(v.get());
+    s->ctx->launches += 4;
+    s->ctx->release_scratch({"k1_", "sub_"});
+    s->train_nbr = std::move(v);
+  }
+  return s->train_nbr.get();
+}
 
 void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
   catgnn_ctx ctx = s->ctx;
@@ -270,6 +394,8 @@ void build_csr(catgnn_shard_s* s, const uint32_t* d_pairs, uint64_t num_edges) {
   if (s->rows >= 0x7fffffffull) throw ConfigError("shard rows exceed the int32 column index range");
   const uint32_t rows = (uint32_t)s->rows;
   s->num_edges = num_edges;
+  s->train_sub.reset();  // views of the previous CSR
+  s->train_nbr.reset();
   s->row_ptr.alloc(rows + 1);
   int32_t* deg = ctx->scratch_buf<int32_t>("k1_deg", rows + 1);
   int* bad = ctx->scratch_buf<int>("k1_flag", 1);

@@ -637,7 +637,10 @@ uint32_t* act_bits(catgnn_ctx ctx, const std::string& name, uint64_t rows, uint3
 std::string nm(const char* base, size_t l) { return std::string(base) + std::to_string(l); }
 
 // Forward over the shard; returns the logits buffer (rows x D_out of the last layer).
-std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
+// lean (train steps): the last layer's logits are computed for the train rows
+// only (the loss reads nothing else; K2 over the shard's train-row view) —
+// forward_backward and evaluation compute every row.
+std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S, bool lean = false) {
   catgnn_ctx ctx = M->ctx;
   const uint64_t rows = S->rows;
   const bool gcn = M->cfg.kind == CATGNN_MODEL_GCN;
@@ -780,7 +783,12 @@ std::vector<Bufs> forward(catgnn_model_s* M, catgnn_shard_s* S) {
         a.out_hi = b.split.hi; a.out_lo = b.split.lo; a.out_s_ld = b.split.ld;
         M->h_split_only[l] = true;
       }
-      aggregate(S, a);
+      catgnn_shard_s* V = (lean && last && bf_layer(M, l)) ? train_rows_view(S) : nullptr;
+      if (V) {  // train rows only: the view's rows map back to the shard's
+        a.row_map = V->row_map.p;
+        a.zero_row = (int64_t)rows;
+      }
+      aggregate(V ? V : S, a);
     }
     in = b.out;
     in_ld = b.out_ld;
@@ -938,7 +946,16 @@ double backward(catgnn_model_s* M, catgnn_shard_s* S, const std::vector<Bufs>& B
         a.in = nullptr; a.in_h = dzh; a.in_ld = z.ld; a.pre = nullptr; a.in_scale = 1.0f / z.scale;
       }
       a.out = nullptr; a.out_hi = dT.hi; a.out_lo = dT.lo; a.out_s_ld = dT.ld; a.width = L.D_out;
-      aggregate(S, a);
+      // the last layer's gradient is non-zero on the train rows only: gather from
+      // those neighbours (the shard's train-neighbour view; every row keeps its
+      // full degree's post scale)
+      catgnn_shard_s* V = (lean && li == nl - 1 && ntr) ? train_nbr_view(S) : nullptr;
+      if (V) {
+        a.zero_row = (int64_t)rows;
+        if (a.norm == kNormGcn) a.post_arr = S->dinv.p;
+        else if (a.norm != kNormNone) V = nullptr;  // (no per-row table for other norms)
+      }
+      aggregate(V ? V : S, a);
       GemmEpi e; e.out = gW; e.ld_out = L.w_cols;  // dW = dT^T H_{l-1} (both MN-major, in place)
       gemm_bf16x3(ctx, op16(dT, true), op16(b.in_split, true), L.d_out, L.w_cols, (uint32_t)rows, e, 0);
       if (need_dx) {  // dZ_{l-1} = mask (dT W)
@@ -1018,7 +1035,7 @@ __global__ void loss_accum_kernel(const double* __restrict__ loss_sum, double we
 
 void model_train_step(catgnn_model m, catgnn_shard s) {
   check_pair(m, s);
-  auto B = forward(m, s);
+  auto B = forward(m, s, true);
   backward(m, s, B, false, true);
   optimizer_step(m);
   m->last_shard = s;
@@ -1205,7 +1222,7 @@ int catgnn_model_forward_backward(catgnn_model m, catgnn_shard s, double* loss) 
 int catgnn_model_train_step(catgnn_model m, catgnn_shard s, double* loss) {
   return guarded([&] {
     check_pair(m, s);
-    auto B = forward(m, s);
+    auto B = forward(m, s, true);
     double l = backward(m, s, B, loss != nullptr, true);
     optimizer_step(m);
     if (loss) *loss = l;

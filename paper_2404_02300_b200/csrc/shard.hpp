@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "common.hpp"
@@ -58,6 +59,13 @@ struct catgnn_shard_s {
   std::vector<uint8_t> owner, role;
   catgnn::DevBuf<uint64_t> d_ext;  // device copy of ext_ids (feature gathers)
   uint64_t ext_max = 0;
+  // Train-row views of the CSR for the lean train step (gnn.cu): the last
+  // layer's logits matter only on train rows (train_sub: those rows' full
+  // neighbour lists, row_map = their rows here) and its gradient is non-zero
+  // only on them (train_nbr: every row, neighbours restricted to train rows, in
+  // order).  Built on first use, dropped when the labels or the CSR change.
+  std::unique_ptr<catgnn_shard_s> train_sub, train_nbr;
+  catgnn::DevBuf<int32_t> row_map;  // a view's rows in its parent (train_sub)
 };
 
 namespace catgnn {
@@ -80,6 +88,13 @@ struct AggArgs {
   // being predicated off).
   const void* in_h = nullptr;
   float in_scale = 1.0f;
+  // the shard is a row view (train_sub): output / self / mask rows are
+  // row_map[r]; post_arr: per-row post scale (a filtered view's rows keep their
+  // full degree's scale); zero_row: the input's zero row when the view has
+  // fewer rows than the input (default: the shard's rows)
+  const int32_t* row_map = nullptr;
+  const float* post_arr = nullptr;
+  int64_t zero_row = -1;
   bool in_zero_row = false;  // fp32 input: row `rows` exists and is zero (fp16: always required)
   // guarded fp16 forward of a ReLU layer (aggregate.cu epilogue_row GUARD):
   // per-row max |T| of the rounded rows (rows + 1 entries, the zero row 0),
@@ -126,6 +141,9 @@ void map_ext_edges(catgnn_ctx ctx, const uint64_t* d_ext_ids, uint64_t rows,
                    const uint64_t* d_edges_ext, uint64_t num_edges, uint32_t* d_pairs);
 // K2: neighbourhood aggregation over the shard CSR.
 void aggregate(catgnn_shard_s* s, const AggArgs& a);
+// The train-row views (built on first use; nullptr when the shard has no train rows).
+catgnn_shard_s* train_rows_view(catgnn_shard_s* s);
+catgnn_shard_s* train_nbr_view(catgnn_shard_s* s);
 // Copy rows x width between strided buffers (hops = 0 propagate).
 void copy_rows(catgnn_ctx ctx, const float* in, uint32_t in_ld, float* out, uint32_t out_ld,
                uint64_t rows, uint32_t width);
