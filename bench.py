@@ -159,7 +159,8 @@ def load_ncu_traffic(w):
     return None
 
 
-def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step, hbm, hbm_src, l2_gbs, hbm_rd):
+def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step, hbm, hbm_src, l2_gbs, hbm_rd,
+                views=None):
     """Roofline of K2 whose every number is a fraction of the peak it is divided by:
     * effective_gbs: SURVEY §8(d) algorithmic bytes (nnz*(4+4d) + N*(4d(1+self)+8)
       per pass) / in-step K2 time.  Each gathered row counts once per edge, so on
@@ -169,10 +170,19 @@ def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step
       else "l2" when the effective rate exceeds the HBM peak (the gathers are
       served from L2: the ceiling is the measured L2 read rate), else "hbm"."""
     self_term = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
-    widths = list(zip(w.passes(), w.pass_elem_bytes()))
-    algo = sum(agg_bytes(nz, rw, wd, self_term, eb) for nz, rw in zip(part_nnz, part_rows) for wd, eb in widths)
-    comp = sum((eb + 4) * wd * rw + 4 * nz + 8 * (rw + 1)
-               for nz, rw in zip(part_nnz, part_rows) for wd, eb in widths)
+    widths = list(zip(w.passes(), w.pass_elem_bytes(), w.lean_pass_views()))
+
+    def gathered(k, kind):  # (nnz, rows) a pass of partition k gathers (lean train-step views)
+        nz, rw = part_nnz[k], part_rows[k]
+        if views is not None and kind == "train_rows":
+            return views[k][1], views[k][0]
+        if views is not None and kind == "train_nbrs":
+            return views[k][2], rw
+        return nz, rw
+    algo = sum(agg_bytes(*gathered(k, kind), wd, self_term, eb)
+               for k in range(len(part_nnz)) for wd, eb, kind in widths)
+    comp = sum((eb + 4) * wd * gathered(k, kind)[1] + 4 * gathered(k, kind)[0] + 8 * (gathered(k, kind)[1] + 1)
+               for k in range(len(part_nnz)) for wd, eb, kind in widths)
     t = agg_ms_step / 1e3
     eff = algo / t / 1e9 if t > 0 else None
     ncu = load_ncu_traffic(w)
@@ -712,8 +722,12 @@ def main():
         hbm_rd_gbs = max(gp.probe_read_bandwidth(4 << 30, 3, ctx) for _ in range(2))
     except Exception as ex:  # pragma: no cover
         log("[probe] failed:", ex)
+    views = [s.train_views() for s in shards]  # (train rows, their nnz, nnz into train rows) per partition
     roofline = k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, per_launch, ms_step, hbm, src, l2_gbs,
-                           hbm_rd_gbs)
+                           hbm_rd_gbs, views)
+    gathered_per_step = sum(
+        (v[1] if kind == "train_rows" else v[2] if kind == "train_nbrs" else nz)
+        for nz, v in zip(part_nnz, views) for kind in w.lean_pass_views())
     # useful GEMM flops per step: forward + weight gradient (+ input gradient past layer 0)
     gemm_flops = 0
     for rows_i in part_rows:
@@ -792,6 +806,11 @@ def main():
                                                       "events without lane overlap)" if lanes > 1 else
                                                       "the timed region's CUDA events"),
                 "global_nnz_edges_per_s": meta["nnz"] * len(widths) * args.steps / (total_ms / 1e3),
+                "value_definition": ("local nnz x aggregation passes per step / step time: the epoch's "
+                                     "full-graph-equivalent aggregation; a train step gathers the last "
+                                     "layer's passes only over its train-row views (same results)"),
+                "edges_gathered_per_step_rank": gathered_per_step,
+                "edges_equivalent_per_step_rank": edges_per_step_rank,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if feat_comm is not None:

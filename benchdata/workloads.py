@@ -66,6 +66,22 @@ class Workload:
                     bwd.append(w)
         return out + bwd[::-1]
 
+    def lean_pass_views(self) -> list:
+        """Per pass in passes() order, the rows a train step aggregates (gnn.cu
+        lean forward / backward): "train_rows" for the last layer's forward and
+        "train_nbrs" for its backward when that layer is a transform-first GCN /
+        GIN layer, "all" otherwise."""
+        fwd, bwd = [], []
+        for l in range(self.layers):
+            d_in = self.dim if l == 0 else self.hidden
+            d_out = self.classes if l + 1 == self.layers else self.hidden
+            agg_first = d_in <= d_out if self.model == "sage" else d_in < d_out
+            lean = self.model in ("gcn", "gin") and not agg_first and l + 1 == self.layers
+            fwd.append("train_rows" if lean else "all")
+            if not (agg_first and l == 0):
+                bwd.append("train_nbrs" if lean else "all")
+        return fwd + bwd[::-1]
+
     def pass_elem_bytes(self) -> list:
         """Bytes per gathered input element of each pass in passes() order
         (gnn.cu f16_fwd / f16_guard / f16_bwd): GCN transform-first layers

@@ -186,6 +186,11 @@ typedef struct {
   uint64_t tasks;      /* aggregation work items */
 } catgnn_shard_info;
 int catgnn_shard_get_info(catgnn_shard s, catgnn_shard_info* info);
+/* The train-row views a train step aggregates its last layer over (no
+ * reference counterpart; measurement): rows / neighbour entries of the train
+ * rows' CSR rows and the neighbour entries that point at train rows (built if
+ * needed; zeros when the shard has no train rows). */
+int catgnn_shard_train_views(catgnn_shard s, uint64_t* sub_rows, uint64_t* sub_nnz, uint64_t* nbr_nnz);
 /* Bit-exact export of the device CSR (offsets widened to u64). */
 int catgnn_csr_export(catgnn_shard s, uint64_t* offsets, uint32_t* neighbors);
 int catgnn_shard_role_rows(catgnn_shard s, int role, uint32_t* rows);

@@ -60,6 +60,7 @@ def _load():
         "catgnn_artifact_part_counts": (C.c_int, [vp, u32, P(u64), P(u64), P(u64)]),
         "catgnn_artifact_replica_map": (C.c_int, [vp, u32, vp, vp, vp, vp]),
         "catgnn_shard_halo_map": (C.c_int, [vp, vp, vp, vp]),
+        "catgnn_shard_train_views": (C.c_int, [vp, vp, vp, vp]),
         "catgnn_shard_load": (C.c_int, [vp, vp, i32, C.c_char_p, C.c_char_p, P(vp)]),
         "catgnn_shard_create": (C.c_int, [vp, u32, vp, u64, vp, u32, P(vp)]),
         "catgnn_shard_create_from_part": (C.c_int, [vp, u64, vp, vp, vp, vp, vp, u64, vp, u32, P(vp)]),

@@ -444,6 +444,18 @@ int catgnn_artifact_replica_map(catgnn_artifact a, uint32_t part, uint64_t* ext_
   });
 }
 
+int catgnn_shard_train_views(catgnn_shard s, uint64_t* sub_rows, uint64_t* sub_nnz, uint64_t* nbr_nnz) {
+  return guarded([&] {
+    if (!s) throw ConfigError("null shard");
+    CG_CUDA(cudaSetDevice(s->ctx->device));
+    catgnn_shard_s* a = train_rows_view(s);
+    catgnn_shard_s* b = train_nbr_view(s);
+    if (sub_rows) *sub_rows = a ? a->rows : 0;
+    if (sub_nnz) *sub_nnz = a ? a->nnz : 0;
+    if (nbr_nnz) *nbr_nnz = b ? b->nnz : 0;
+  });
+}
+
 int catgnn_shard_halo_map(catgnn_shard s, catgnn_artifact a, uint32_t* home, uint64_t* n_halo) {
   return guarded([&] {
     if (!s || !a) throw ConfigError("null argument");

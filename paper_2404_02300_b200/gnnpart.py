@@ -220,6 +220,12 @@ class Shard:
         check(lib.catgnn_shard_halo_map(self.handle, artifact.handle, _ptr(home), C.byref(n)))
         return home, n.value
 
+    def train_views(self):
+        """(rows, nnz) of the train-row view and nnz of the train-neighbour view."""
+        a = C.c_uint64(); b = C.c_uint64(); c = C.c_uint64()
+        check(lib.catgnn_shard_train_views(self.handle, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
     @property
     def info(self) -> ShardInfo:
         inf = ShardInfo()
