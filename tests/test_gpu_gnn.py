@@ -451,3 +451,34 @@ def test_nccl_collectives_inside_cuda_graph(graph):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(m.get_params(), (p0 * 2.0 * 0.5 * 0.5).astype(np.float32))
     comm.close()
+
+
+@pytest.mark.parametrize("kind,in_dim,hidden,classes,layers", [
+    ("gcn", 602, 64, 41, 2), ("gcn", 602, 256, 41, 2), ("gin", 140, 64, 6, 2), ("gcn", 96, 64, 12, 3)])
+def test_lean_train_step_matches_full_passes(graph, kind, in_dim, hidden, classes, layers):
+    """train_step (gnn.cu lean mode) aggregates the last layer's forward over the
+    train rows' view and its backward over the train-neighbour view; its
+    gradients equal forward_backward's full passes (only the split of heavy
+    rows into partial sums differs), and the views' sizes equal a NumPy count
+    over the exported CSR."""
+    from paper_2404_02300_b200 import gnnpart as gp
+    from paper_2404_02300_b200.gnn import GNNModel
+    rng = np.random.default_rng(7)
+    n = graph["n"]
+    X = rng.normal(size=(n, in_dim)).astype(np.float32)
+    labels = rng.integers(0, classes, n).astype(np.int32)
+    train = np.sort(rng.choice(n, size=n // 20, replace=False)).astype(np.uint32)
+    s = gp.Shard.from_edges(n, graph["pairs"], X)
+    s.set_labels(labels, train)
+    adj = s.adjacency()
+    off, nb = adj.offsets.astype(np.int64), adj.neighbors.astype(np.int64)
+    is_tr = np.zeros(n, bool)
+    is_tr[train] = True
+    assert s.train_views() == (train.size, int(np.diff(off)[train].sum()), int(is_tr[nb].sum()))
+    a = GNNModel(kind, layers, in_dim, hidden, classes, seed=2)
+    b = GNNModel(kind, layers, in_dim, hidden, classes, seed=2)
+    la = a.forward_backward(s)
+    lb = b.train_step(s, want_loss=True)
+    assert abs(la - lb) <= 1e-6 * abs(la)
+    for (gA, ga), (gB, gb) in zip(a.unflatten(a.get_grads()), b.unflatten(b.get_grads())):
+        assert rel_err(gB, gA) < 1e-5 and rel_err(gb, ga) < 1e-5
