@@ -181,8 +181,9 @@ def k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, agg_launches, ms_step
         return nz, rw
     algo = sum(agg_bytes(*gathered(k, kind), wd, self_term, eb)
                for k in range(len(part_nnz)) for wd, eb, kind in widths)
-    comp = sum((eb + 4) * wd * gathered(k, kind)[1] + 4 * gathered(k, kind)[0] + 8 * (gathered(k, kind)[1] + 1)
-               for k in range(len(part_nnz)) for wd, eb, kind in widths)
+    # compulsory: every input row of the shard once, indices and offsets once, each output row once
+    comp = sum(eb * wd * part_rows[k] + 4 * wd * gathered(k, kind)[1] + 4 * gathered(k, kind)[0]
+               + 8 * (gathered(k, kind)[1] + 1) for k in range(len(part_nnz)) for wd, eb, kind in widths)
     t = agg_ms_step / 1e3
     eff = algo / t / 1e9 if t > 0 else None
     ncu = load_ncu_traffic(w)
@@ -723,6 +724,9 @@ def main():
     except Exception as ex:  # pragma: no cover
         log("[probe] failed:", ex)
     views = [s.train_views() for s in shards]  # (train rows, their nnz, nnz into train rows) per partition
+    if os.environ.get("CATGNN_VIEWS_OUT"):  # scripts/k2_traffic.py: per-pass gathered rows / nnz
+        with open(os.environ["CATGNN_VIEWS_OUT"], "w") as f:
+            json.dump(views, f)
     roofline = k2_roofline(w, mine, part_nnz, part_rows, agg_ms_step, per_launch, ms_step, hbm, src, l2_gbs,
                            hbm_rd_gbs, views)
     gathered_per_step = sum(

@@ -29,11 +29,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
          "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6, "%": 1, "": 1}
 
 
-def compulsory_bytes(nnz, rows, width, eb):
-    """Each distinct input row read once (eb bytes per element), column indices
-    and row offsets once, each output row written once (what an infinite cache
-    would move)."""
-    return (eb + 4) * width * rows + 4 * nnz + 8 * (rows + 1)
+def compulsory_bytes(nnz, rows_in, rows, width, eb):
+    """Each input row read once (eb bytes per element; all rows_in of the shard,
+    an upper bound for a train-row view), column indices and row offsets once,
+    each output row written once (what an infinite cache would move)."""
+    return eb * width * rows_in + 4 * width * rows + 4 * nnz + 8 * (rows + 1)
 
 
 def main():
@@ -46,7 +46,7 @@ def main():
     log = os.environ.get("K2_TRAFFIC_CSV") or os.path.join(ROOT, "gpurun_out", f"k2_traffic_{workload}.csv")
     if not os.environ.get("K2_TRAFFIC_CSV"):  # else: re-summarise an existing capture
         os.makedirs(os.path.dirname(log), exist_ok=True)
-        env = dict(os.environ, CATGNN_WORKLOAD=workload)
+        env = dict(os.environ, CATGNN_WORKLOAD=workload, CATGNN_VIEWS_OUT=log + ".views.json")
         cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:agg_", "--csv",
                "--log-file", log, sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1",
                "--graph", "0", "--no-e2e", "--no-cpu-baseline", "--lanes", "1"]
@@ -64,6 +64,9 @@ def main():
     seq = seq[len(seq) // 2:]  # the timed step (warm-up and timed steps launch the same sequence)
     widths = w.passes()
     ebs = w.pass_elem_bytes()
+    kinds = w.lean_pass_views()
+    with open(log + ".views.json") as f:  # (train rows, their nnz, nnz into train rows) per partition
+        views = json.load(f)
     self_term = {"gcn": 1, "gin": 1, "sage": 0}[w.model]
     passes, cur = [], None
     for d in seq:
@@ -77,14 +80,20 @@ def main():
         part, pi = i // len(widths), i % len(widths)
         width, eb = widths[pi], ebs[pi]
         nnz, rows = meta["part_nnz"][part], meta["part_rows"][part]
+        rows_in = rows
+        if kinds[pi] == "train_rows":  # the lean train step's views (gnn.cu forward / backward(lean))
+            rows, nnz = views[part][0], views[part][1]
+        elif kinds[pi] == "train_nbrs":
+            nnz = views[part][2]
         cur = {"partition": part, "pass": pi, "width": width, "elem_bytes": eb, "kernel": d["kernel"],
+               "view": kinds[pi], "nnz": nnz, "rows": rows,
                "time_us": d["gpu__time_duration.sum"],
                "dram_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
                "dram_read": d["dram__bytes_read.sum"], "dram_write": d["dram__bytes_write.sum"],
                "l2_bytes": d["lts__t_bytes.sum"], "l2_hit_pct": d["lts__t_sector_hit_rate.pct"],
                "l1_hit_pct": d["l1tex__t_sector_hit_rate.pct"], "fixups": 0,
                "algorithmic_bytes": nnz * (4 + eb * width) + rows * (eb * width * self_term + 4 * width + 8),
-               "compulsory_bytes": compulsory_bytes(nnz, rows, width, eb)}
+               "compulsory_bytes": compulsory_bytes(nnz, rows_in, rows, width, eb)}
         passes.append(cur)
     assert len(passes) == w.partitions * len(widths), (len(passes), w.partitions, widths)
     tot = {k: sum(p[k] for p in passes) for k in ("time_us", "dram_bytes", "l2_bytes", "algorithmic_bytes",
