@@ -734,10 +734,12 @@ __device__ __forceinline__ int next_cols(uint32_t words, uint32_t& w, uint32_t& 
   return nc;
 }
 __device__ __forceinline__ float lo_at(const __half* __restrict__ lo, size_t i) { return __half2float(__ldg(lo + i)); }
-__global__ void __launch_bounds__(256, 8) agg_exact_fix_kernel(const AggKernelArgs p, const __half* __restrict__ lo) {
+// light rows: warp per row, warps [w0, w0 + nw) of the grid
+__device__ __forceinline__ void exact_fix_light(const AggKernelArgs& p, const __half* __restrict__ lo, unsigned w0,
+                                                unsigned nw) {
   const int lane = threadIdx.x & 31;
   const unsigned n = *p.fix_count;
-  for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+  for (unsigned i = w0; i < n; i += nw) {
     const uint32_t r = p.fix_rows[i];
     const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
     const float post = post_scale(p.norm, (float)(e1 - e0));
@@ -765,12 +767,12 @@ __global__ void __launch_bounds__(256, 8) agg_exact_fix_kernel(const AggKernelAr
     }
   }
 }
-__global__ void __launch_bounds__(256) agg_exact_fix_heavy_kernel(const AggKernelArgs p,
-                                                                  const __half* __restrict__ lo) {
-  __shared__ float red[8][4];
+// split (hub) rows: block per row, blocks [b0, b0 + nb)
+__device__ __forceinline__ void exact_fix_heavy(const AggKernelArgs& p, const __half* __restrict__ lo,
+                                                float (&red)[8][4], unsigned b0, unsigned nb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned n = *p.fix_hcount;
-  for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+  for (unsigned i = b0; i < n; i += nb) {
     const uint32_t r = p.fix_heavy[i];
     const int64_t e0 = __ldg(p.row_ptr + r), e1 = __ldg(p.row_ptr + r + 1);
     const float post = post_scale(p.norm, (float)(e1 - e0));
@@ -812,6 +814,22 @@ __global__ void __launch_bounds__(256) agg_exact_fix_heavy_kernel(const AggKerne
       __syncthreads();
     }
   }
+}
+__global__ void __launch_bounds__(256, 8) agg_exact_fix_kernel(const AggKernelArgs p, const __half* __restrict__ lo) {
+  exact_fix_light(p, lo, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
+}
+__global__ void __launch_bounds__(256) agg_exact_fix_heavy_kernel(const AggKernelArgs p,
+                                                                  const __half* __restrict__ lo) {
+  __shared__ float red[8][4];
+  exact_fix_heavy(p, lo, red, blockIdx.x, gridDim.x);
+}
+// one launch for both: the first hb blocks take the hub rows (dispatched first,
+// so their long edge walks overlap the light rows instead of following them)
+__global__ void __launch_bounds__(256, 8) agg_exact_fix_merged_kernel(const AggKernelArgs p,
+                                                                      const __half* __restrict__ lo, unsigned hb) {
+  __shared__ float red[8][4];
+  if (blockIdx.x < hb) exact_fix_heavy(p, lo, red, blockIdx.x, hb);
+  else exact_fix_light(p, lo, ((blockIdx.x - hb) * blockDim.x + threadIdx.x) >> 5, ((gridDim.x - hb) * blockDim.x) >> 5);
 }
 
 using AggFn = void (*)(const AggKernelArgs);
@@ -1038,9 +1056,16 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     }
     if (guard) {  // exact fp32 recomputation of the flagged elements
       int tf = ctx->begin_timed(3, ctx->timing ? std::string("(within K2 w256) guard exact fix") : std::string());
-      agg_exact_fix_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
+      static const int merged = env_int("CATGNN_FIX_MERGED", 1);
+      const unsigned hb = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 2);
+      if (merged) {
+        agg_exact_fix_merged_kernel<<<ctx->num_sms * 8 + hb, 256, 0, ctx->stream>>>(
+            p, static_cast<const __half*>(a.guard_lo), hb);
+      } else {
+        agg_exact_fix_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
+      }
       CG_CHECK_LAUNCH();
-      if (s->n_heavy) {
+      if (s->n_heavy && !merged) {
         agg_exact_fix_heavy_kernel<<<(unsigned)std::min<uint64_t>(s->n_heavy, ctx->num_sms * 4), 256, 0,
                                      ctx->stream>>>(p, static_cast<const __half*>(a.guard_lo));
         CG_CHECK_LAUNCH();
