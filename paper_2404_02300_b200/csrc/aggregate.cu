@@ -588,11 +588,11 @@ constexpr int kFixWarps = 8;
 // split rows with at most this many chunks are combined by one warp each
 // (agg_fixup_warp_kernel); hubs with more keep a whole block
 constexpr int kWarpFixChunks = 16;
-template <int VPL, bool GUARD = false>
-__global__ void __launch_bounds__(256) agg_fixup_warp_kernel(const AggKernelArgs p) {
+// warps [w0, w0 + nw) of the grid, one split row each
+template <int VPL, bool GUARD>
+__device__ __forceinline__ void fixup_warp_rows(const AggKernelArgs& p, uint64_t w0, uint64_t nw) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t h = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; h < p.n_heavy; h += nw) {
+  for (uint64_t h = w0; h < p.n_heavy; h += nw) {
     const int4 hv = __ldg(p.heavy + h);
     if (hv.z > kWarpFixChunks) continue;  // a block-per-row hub (agg_fixup_kernel)
     const int64_t r = hv.x;
@@ -631,11 +631,12 @@ __global__ void __launch_bounds__(256) agg_fixup_warp_kernel(const AggKernelArgs
     epilogue_row<VPL, 32, true, 1, GUARD>(p, r, deg, a0, lane, nullptr, ss);
   }
 }
-template <int VPL, bool GUARD = false>
-__global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
-  __shared__ float4 part[kFixWarps][32 * VPL];
+// blocks [b0, b0 + nb), one hub row each
+template <int VPL, bool GUARD>
+__device__ __forceinline__ void fixup_hub_rows(const AggKernelArgs& p, float4 (&part)[kFixWarps][32 * VPL],
+                                               uint64_t b0, uint64_t nb) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t h = blockIdx.x; h < p.n_heavy; h += gridDim.x) {
+  for (uint64_t h = b0; h < p.n_heavy; h += nb) {
     const int4 hv = __ldg(p.heavy + h);
     if (hv.z <= kWarpFixChunks) continue;  // combined by agg_fixup_warp_kernel
     const int64_t r = hv.x;
@@ -688,6 +689,26 @@ __global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
     }
     __syncthreads();
   }
+}
+template <int VPL, bool GUARD = false>
+__global__ void __launch_bounds__(256) agg_fixup_warp_kernel(const AggKernelArgs p) {
+  fixup_warp_rows<VPL, GUARD>(p, (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5,
+                              ((uint64_t)gridDim.x * blockDim.x) >> 5);
+}
+template <int VPL, bool GUARD = false>
+__global__ void __launch_bounds__(256) agg_fixup_kernel(const AggKernelArgs p) {
+  __shared__ float4 part[kFixWarps][32 * VPL];
+  fixup_hub_rows<VPL, GUARD>(p, part, blockIdx.x, gridDim.x);
+}
+// both in one launch: the first hb blocks look for hub rows (dispatched first,
+// so a hub's long combine overlaps the warp-per-row combines)
+template <int VPL, bool GUARD = false>
+__global__ void __launch_bounds__(256) agg_fixup_merged_kernel(const AggKernelArgs p, unsigned hb) {
+  __shared__ float4 part[kFixWarps][32 * VPL];
+  if (blockIdx.x < hb) fixup_hub_rows<VPL, GUARD>(p, part, blockIdx.x, hb);
+  else
+    fixup_warp_rows<VPL, GUARD>(p, ((blockIdx.x - hb) * (uint64_t)blockDim.x + threadIdx.x) >> 5,
+                                ((uint64_t)(gridDim.x - hb) * blockDim.x) >> 5);
 }
 
 // Exact recomputation of the guard's flagged elements (epilogue_row GUARD).
@@ -1043,9 +1064,19 @@ void aggregate(catgnn_shard_s* s, const AggArgs& a) {
     if (s->n_heavy) {  // split rows: warp per row up to kWarpFixChunks chunks, block per hub row
       AggFn fw = guard ? agg_fixup_warp_kernel<2, true> : pick_fixup(w4, true);
       const unsigned gw = (unsigned)std::min<uint64_t>((s->n_heavy + 7) / 8, (uint64_t)ctx->num_sms * 8);
-      fw<<<gw, 256, 0, ctx->stream>>>(p);
-      CG_CHECK_LAUNCH();
-      if (s->n_big_heavy) {
+      static const int fix_merged = env_int("CATGNN_FIX_MERGED", 1);
+      const unsigned vpl = (w4 + 31) / 32;
+      if (s->n_big_heavy && fix_merged && vpl <= 2) {
+        const unsigned hb = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 16);
+        auto fm = guard ? agg_fixup_merged_kernel<2, true>
+                        : (vpl == 1 ? agg_fixup_merged_kernel<1> : agg_fixup_merged_kernel<2>);
+        fm<<<hb + gw, 256, 0, ctx->stream>>>(p, hb);
+        CG_CHECK_LAUNCH();
+      } else {
+        fw<<<gw, 256, 0, ctx->stream>>>(p);
+        CG_CHECK_LAUNCH();
+      }
+      if (s->n_big_heavy && !(fix_merged && vpl <= 2)) {
         AggFn fx = guard ? agg_fixup_kernel<2, true> : pick_fixup(w4, false);
         const unsigned g2 = (unsigned)std::min<uint64_t>(s->n_heavy, (uint64_t)ctx->num_sms * 16);
         fx<<<g2, 256, 0, ctx->stream>>>(p);
