@@ -10,7 +10,7 @@ timeout 900 python scripts/k2_traffic.py reddit_gcn gpurun_out/r02_k2_traffic_re
 cp gpurun_out/r02_k2_traffic_reddit_gcn.json profiles/
 ncu --set full --clock-control none --import-source on -k regex:agg_kernel -s 0 -c 4 \
     -o gpurun_out/r02_k2_full -f python bench.py $ARGS > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:exact_fix -s 0 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:exact_fix -s 0 -c 1 \
     -o gpurun_out/r02_fix_full -f python bench.py $ARGS > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm_tf32 -s 0 -c 5 \
     -o gpurun_out/r02_k3_full -f python bench.py $ARGS > /dev/null 2>&1
